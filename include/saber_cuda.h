@@ -1,0 +1,309 @@
+/*
+ * saber_cuda.h — the drop-in C ABI of the B200 SABER engine.
+ *
+ * The reference (SaberSim, /root/reference/proj) has no C ABI: its boundary is
+ * the installed C++20 API of sabersim::saber_core.  Every entry point below
+ * replaces one call of that API on the hot path; the citation says which
+ * (paths relative to proj/core/include/saber/ and proj/core/src/).
+ *
+ *   saber_cuda_sweep          <- SweepResult sweep(const SweepGrid&, const SimConfig&, int jobs)
+ *                                 simloop.hpp:96-99, simloop.cpp:130-277
+ *   saber_cuda_run_batch      <- RunOutput run(const SimConfig&)               simloop.hpp:49
+ *                                 RunOutput run_with_requests(const SimConfig&, std::vector<Request>)
+ *                                 simloop.hpp:53-54, simloop.cpp:50-116
+ *                                 (many independent trajectories per call)
+ *   saber_cuda_fit_batch      <- SpeedModel fit(const std::vector<LoadSpeedSample>&, ModelFamily)
+ *                                 estimator.hpp:61, estimator.cpp:241-346
+ *                                 CalibrationReport calibrate(const std::vector<LoadSpeedSample>&)
+ *                                 calibration.hpp:54, calibration.cpp:137-168
+ *                                 (many independent curves per call)
+ *   saber_cuda_predict_table  <- double predict(const SpeedModel&, int)       estimator.hpp:39
+ *
+ * Conventions: plain C, POD structs, caller-owned memory, no exceptions.  Every
+ * function returns a saber_status; on failure saber_cuda_last_error() holds a
+ * one-line message.  Status codes map onto the reference's exception types:
+ *   SABER_EINVAL  -> std::invalid_argument   (config / validation errors)
+ *   SABER_EDOMAIN -> std::domain_error       (predict with load < 1)
+ *   SABER_EFIT    -> saber::FitError         (per curve, see saber_fit_out)
+ *   SABER_ECUDA   -> std::runtime_error      (device failure; CLI exit 3)
+ * There is no CPU fallback: with no usable sm_100 device every compute call
+ * returns SABER_ECUDA.
+ */
+#ifndef SABER_CUDA_H
+#define SABER_CUDA_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SABER_CUDA_ABI_VERSION 1
+
+typedef enum {
+  SABER_OK = 0,
+  SABER_EINVAL = 1,
+  SABER_EDOMAIN = 2,
+  SABER_EFIT = 3,
+  SABER_ECUDA = 4,
+  SABER_ECAPACITY = 5, /* a caller-sized buffer (e.g. decision trace) is too small */
+  SABER_EINTERNAL = 6  /* an invariant the reference would throw logic_error on */
+} saber_status;
+
+/* Task catalog (types.cpp:10-18), in catalog order. */
+enum { SABER_TASK_QNA = 0, SABER_TASK_GENERATION = 1, SABER_TASK_SUMMARY = 2,
+       SABER_TASK_TRANSLATION = 3, SABER_TASK_CUSTOM = -1 };
+/* ModelFamily (estimator.hpp:21). */
+enum { SABER_USL = 0, SABER_LOGISTIC = 1, SABER_LINEAR = 2 };
+/* SchedulerMode (types.hpp:76). */
+enum { SABER_MODE_SABER = 0, SABER_MODE_STATIC = 1 };
+/* DecisionKind (scheduler.hpp:46). */
+enum { SABER_ADMIT_HIGH = 0, SABER_ADMIT_LOW = 1, SABER_REJECT_OWN = 2,
+       SABER_REJECT_ACTIVE = 3, SABER_DEMOTE = 4 };
+
+/* SpeedModel (estimator.hpp:29-33). Linear uses params[0..1]. */
+typedef struct {
+  int32_t family;
+  double params[3];
+} saber_model;
+
+/* WorkloadMix (types.hpp:31-33): fraction per catalog task; present[t]=0 means
+ * the task is absent from the map (a present zero-fraction task is legal). */
+typedef struct {
+  double frac[4];
+  int32_t present[4];
+} saber_mix;
+
+/* One trajectory's result row: SweepRow (simloop.hpp:63-73) + MetricsReport
+ * (metrics.hpp:63-69) scalars, decision statistics and the reference-algorithm
+ * event counts used for the roofline.  All fields are 8 bytes so
+ * a row buffer can be all-reduced as uint64 (disjoint shards sum exactly). */
+typedef struct {
+  double goodput;     /* met / n */
+  double ratio_mean;  /* NaN when nothing completed */
+  double ratio_std;
+  double cv;
+  int64_t n;          /* requests in the trajectory; 0 = row not simulated here */
+  int64_t completed;
+  int64_t met;
+  int64_t decisions;
+  int64_t n_kind[5];  /* by DecisionKind */
+  uint64_t decision_hash; /* hash of the ordered decision log */
+  int64_t issued_by_task[4];
+  int64_t met_by_task[4];
+  int64_t ticks, passes, decode_updates, prefill_updates;
+  int64_t refresh_entries, gate_candidates, ledger_scanned, rng_draws;
+  double last_arrival;
+  double horizon;
+} saber_traj_row;
+
+/* Decision record (scheduler.hpp:48-55). Absent speeds: has_* = 0. */
+typedef struct {
+  double time;
+  uint64_t request_id;
+  int32_t kind;
+  int32_t load_before;
+  int32_t has_pred, has_req;
+  double pred_speed;
+  double req_speed;
+} saber_decision;
+
+/* --------------------------------------------------------------------------
+ * Sweep (simloop.hpp:56-99).  Rows are in the reference's grid order:
+ * mix -> rps -> [caps..., saber] -> repeat (seed = base.seed + repeat).
+ * -------------------------------------------------------------------------- */
+typedef struct {
+  /* SweepGrid */
+  const int32_t* mixes; /* preset ids: 1 = "w1", 2 = "w2", 3 = "w3" */
+  int32_t n_mixes;
+  const double* rps;
+  int32_t n_rps;
+  const int32_t* caps;
+  int32_t n_caps;
+  int32_t with_saber;
+  /* base SimConfig (simloop.hpp:23-31) */
+  int32_t num_requests;
+  double length_jitter;
+  int32_t window_size;
+  double tick;
+  int32_t has_model;
+  saber_model model;
+  saber_model ground_truth;
+  double prefill_rate;
+  int32_t has_horizon;
+  double horizon;
+  int32_t repeats;
+  uint64_t seed;
+  /* execution */
+  int32_t device;        /* CUDA ordinal */
+  int32_t shard_index;   /* this process simulates rows r with r % shard_count == shard_index */
+  int32_t shard_count;   /* 1 = everything */
+} saber_sweep_desc;
+
+/* MixSummary (simloop.hpp:80-89), one per mix, in grid order. */
+typedef struct {
+  double saber_mean_goodput;
+  double best_static_mean_goodput;
+  double delta;
+  double saber_pooled_cv;
+  double best_static_pooled_cv;
+  double saber_rps_mean_cv;
+  double best_static_rps_mean_cv;
+} saber_mix_summary;
+
+typedef struct {
+  saber_traj_row* rows;            /* [n_rows] or NULL */
+  double* completion_times;        /* [n_rows][num_requests] or NULL (NaN = never) */
+  saber_mix_summary* summary;      /* [n_mixes] or NULL (needs shard_count == 1) */
+  int32_t* best_cap_by_rps;        /* [n_mixes][n_rps] or NULL; 0 when no caps */
+  /* telemetry, filled by the call */
+  int64_t n_rows;
+  double device_ms;                /* CUDA-event time of the device work */
+  int32_t kernel_launches;
+} saber_sweep_out;
+
+/* Number of rows a sweep produces (= SweepResult::rows.size()). */
+int64_t saber_cuda_sweep_rows(const saber_sweep_desc* desc);
+
+/* One-shot sweep, host buffers in and out (the end-to-end path). */
+saber_status saber_cuda_sweep(const saber_sweep_desc* desc, saber_sweep_out* out);
+
+/* Staged sweep for device-resident timing and multi-GPU reduction:
+ *   create  : validate, host prologue (per-seed workload draws), device buffers, H2D
+ *   run     : all device work on `stream` (workload expansion, scheduler RNG
+ *             streams, trajectory simulation, per-row metrics)
+ *   summarize: per-cell means, best-cap argmax, pooled CVs from the device rows
+ *   fetch   : D2H into an out struct
+ * The device row / completion buffers are exposed so a caller can all-reduce
+ * them across ranks (rows of other shards are zero, so a uint64 sum gathers). */
+typedef struct saber_sweep_plan saber_sweep_plan;
+typedef struct {
+  void* rows;              /* saber_traj_row[n_rows] on device */
+  size_t rows_bytes;
+  void* completion_times;  /* double[n_rows][num_requests] on device */
+  size_t completion_bytes;
+  int64_t n_rows;
+  int64_t rows_this_shard;
+} saber_sweep_buffers;
+
+saber_status saber_cuda_sweep_plan_create(const saber_sweep_desc* desc, saber_sweep_plan** plan);
+saber_status saber_cuda_sweep_plan_run(saber_sweep_plan* plan, void* cuda_stream);
+saber_status saber_cuda_sweep_plan_summarize(saber_sweep_plan* plan, void* cuda_stream);
+saber_status saber_cuda_sweep_plan_buffers(saber_sweep_plan* plan, saber_sweep_buffers* out);
+saber_status saber_cuda_sweep_plan_fetch(saber_sweep_plan* plan, saber_sweep_out* out);
+/* CUDA-event time and launches of the last plan_run (+ summarize). */
+saber_status saber_cuda_sweep_plan_stats(saber_sweep_plan* plan, double* device_ms,
+                                         double* sim_kernel_ms, int32_t* launches);
+void saber_cuda_sweep_plan_destroy(saber_sweep_plan* plan);
+
+/* --------------------------------------------------------------------------
+ * Trajectory batch (run / run_with_requests).  Each trajectory is either
+ * generated (generate(): WorkloadSpec + its seed) or replayed from explicit
+ * requests (ids 0..n-1 in arrival order).
+ * -------------------------------------------------------------------------- */
+typedef struct {
+  double arrival_time;
+  double sla_seconds;
+  double deadline;         /* absolute; the reference keeps it independent of sla */
+  int32_t input_tokens;
+  int32_t max_output_tokens;
+  int32_t task;            /* SABER_TASK_* (CUSTOM for non-catalog names) */
+  int32_t pad_;
+} saber_request;
+
+typedef struct {
+  /* WorkloadSpec (workload.hpp:15-21); ignored when `requests` is set */
+  saber_mix mix;
+  double rps;
+  int32_t num_requests;
+  uint64_t workload_seed;
+  double length_jitter;
+  /* replay (run_with_requests): num_requests entries, or NULL */
+  const saber_request* requests;
+  /* SchedulerConfig (types.hpp:78-83) */
+  int32_t mode;
+  int32_t window_size;
+  double tick;
+  int32_t static_batch_size;
+  /* SimConfig rest */
+  int32_t has_model;
+  saber_model model;
+  saber_model ground_truth;
+  double prefill_rate;
+  int32_t has_horizon;
+  double horizon;
+  uint64_t seed;           /* scheduler seed (SimConfig::seed) */
+} saber_traj_spec;
+
+typedef struct {
+  const saber_traj_spec* specs;
+  int32_t n_traj;
+  int32_t device;
+} saber_run_batch_desc;
+
+typedef struct {
+  saber_traj_row* rows;          /* [n_traj] */
+  /* per-request outputs, [n_traj][max_n] or NULL (RunRecord, metrics.hpp:20-30) */
+  double* arrival_times;
+  double* admit_times;           /* NaN = never admitted */
+  double* completion_times;      /* NaN = never completed */
+  uint8_t* demoted;              /* final_tier == "low" */
+  int32_t max_n;                 /* row stride of the per-request arrays */
+  /* full decision logs (decisions.csv), optional: trajectory k writes at
+   * decisions + k*decision_cap; counts in n_decisions[k] */
+  saber_decision* decisions;
+  int64_t decision_cap;
+  int64_t* n_decisions;
+  double device_ms;
+  int32_t kernel_launches;
+} saber_run_batch_out;
+
+saber_status saber_cuda_run_batch(const saber_run_batch_desc* desc, saber_run_batch_out* out);
+
+/* --------------------------------------------------------------------------
+ * Batched fitting (estimator.cpp:33-375, calibration.cpp:137-168).
+ * Curve c owns samples [offsets[c], offsets[c+1]).
+ * -------------------------------------------------------------------------- */
+typedef struct {
+  const int32_t* loads;    /* LoadSpeedSample::load */
+  const double* speeds;    /* LoadSpeedSample::speed */
+  const int64_t* offsets;  /* [n_curves + 1] */
+  int32_t n_curves;
+  int32_t family_mask;     /* bit f => fit family f; calibrate needs 0x7 */
+  int32_t calibrate;       /* 1 => also select best family (calibrate()) */
+  int32_t device;
+} saber_fit_desc;
+
+typedef struct {
+  /* per family f (0..2) and curve c: index [f * n_curves + c] */
+  double* params;          /* [3 * n_curves][3]: fitted params or FitError best params */
+  double* r2;              /* fit_r2, or FitError best_sse when status != 0 */
+  int32_t* status;         /* 0 ok, 1 FitError (estimator.hpp:46-58), -1 not fitted */
+  int32_t* best_family;    /* [n_curves] calibrate(): -1 when no family fit */
+  int32_t* iterations;     /* [3 * n_curves] total LM iterations over the 5 starts (or NULL) */
+  double device_ms;
+  int32_t kernel_launches;
+} saber_fit_out;
+
+saber_status saber_cuda_fit_batch(const saber_fit_desc* desc, saber_fit_out* out);
+
+/* predict(model, L) for L = 1..max_load into table[0..max_load-1], computed
+ * exactly as the engine's device tables are (estimator.cpp:16-31). */
+saber_status saber_cuda_predict_table(const saber_model* model, int32_t max_load, double* table);
+
+/* --------------------------------------------------------------------------
+ * Misc.
+ * -------------------------------------------------------------------------- */
+const char* saber_cuda_last_error(void);
+int32_t saber_cuda_abi_version(void);
+/* Number of usable sm_100 devices (0 on a CPU-only host). */
+int32_t saber_cuda_device_count(void);
+/* FP64 FMA throughput microbenchmark on `device` (TFLOP/s, 2 flops per DFMA),
+ * used as the roofline denominator for the FP64 path. */
+saber_status saber_cuda_fp64_peak(int32_t device, double* tflops);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SABER_CUDA_H */

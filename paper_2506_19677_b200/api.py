@@ -1,0 +1,596 @@
+"""Python mirror of the reference's public API for the hot path.
+
+Names, argument meaning and error behaviour follow proj/core/include/saber/
+(simloop.hpp, estimator.hpp, calibration.hpp, workload.hpp, types.hpp), so a
+caller of the reference finds the same surface:
+
+    sweep(grid, base, jobs=0)       -> SweepResult      simloop.hpp:96-99
+    run(config)                     -> RunOutput        simloop.hpp:49
+    run_with_requests(config, reqs) -> RunOutput        simloop.hpp:53-54
+    fit(samples, family)            -> SpeedModel       estimator.hpp:61
+    calibrate(samples)              -> CalibrationReport calibration.hpp:54
+    predict(model, load), max_speed(model)              estimator.hpp:39-42
+
+Every call goes through the C ABI (include/saber_cuda.h) into the sm_100a
+kernels; nothing here computes a simulation or a fit on the CPU.
+Exceptions: InvalidArgument (std::invalid_argument), DomainError
+(std::domain_error), FitError, CalibrationError, and SaberError for device
+failures.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import math
+from dataclasses import dataclass, field
+from typing import Dict, List, Optional, Sequence, Tuple
+
+import numpy as np
+
+from . import _native as N
+
+# ----------------------------------------------------------------- constants
+TASK_NAMES = ["code_qna", "code_generation", "code_summary", "code_translation"]
+TASK_INDEX = {n: i for i, n in enumerate(TASK_NAMES)}
+FAMILIES = ["usl", "logistic", "linear"]
+DECISION_KINDS = ["admit_high", "admit_low", "reject_own", "reject_active", "demote"]
+
+
+class ModelFamily:
+    Usl, Logistic, Linear = 0, 1, 2
+
+
+class SchedulerMode:
+    Saber, Static = 0, 1
+
+
+class InvalidArgument(ValueError):
+    """std::invalid_argument"""
+
+
+class DomainError(ValueError):
+    """std::domain_error"""
+
+
+class FitError(RuntimeError):
+    """saber::FitError (estimator.hpp:46-58)."""
+
+    def __init__(self, what, family, best_params, best_sse):
+        super().__init__(what)
+        self.family = family
+        self.best_params = list(best_params)
+        self.best_sse = best_sse
+
+
+class CalibrationError(RuntimeError):
+    """saber::CalibrationError (calibration.hpp:15-18)."""
+
+
+def _check(status: int):
+    if status == N.SABER_OK:
+        return
+    msg = N.lib().saber_cuda_last_error().decode()
+    if status == N.SABER_EINVAL:
+        raise InvalidArgument(msg)
+    if status == N.SABER_EDOMAIN:
+        raise DomainError(msg)
+    raise N.SaberError(status, msg)
+
+
+# --------------------------------------------------------------------- types
+@dataclass
+class TaskProfile:
+    name: str
+    avg_input_tokens: int
+    avg_output_tokens: int
+    sla_seconds: float
+
+
+def task_catalog() -> List[TaskProfile]:
+    """types.cpp:10-18"""
+    return [TaskProfile("code_qna", 186, 43, 1.0), TaskProfile("code_generation", 463, 387, 8.0),
+            TaskProfile("code_summary", 31, 30, 1.0), TaskProfile("code_translation", 670, 617, 12.0)]
+
+
+@dataclass
+class WorkloadMix:
+    proportions: Dict[str, float] = field(default_factory=dict)
+
+
+def preset_mix(mix_id: str) -> WorkloadMix:
+    """types.cpp:27-47"""
+    if mix_id == "w1":
+        return WorkloadMix({"code_translation": 0.4, "code_generation": 0.4, "code_qna": 0.1,
+                            "code_summary": 0.1})
+    if mix_id == "w2":
+        return WorkloadMix({"code_qna": 0.4, "code_summary": 0.4, "code_generation": 0.1,
+                            "code_translation": 0.1})
+    if mix_id == "w3":
+        return WorkloadMix({"code_qna": 0.25, "code_generation": 0.25, "code_summary": 0.25,
+                            "code_translation": 0.25})
+    raise InvalidArgument(f"unknown mix preset: {mix_id}")
+
+
+@dataclass
+class SpeedModel:
+    family: int = ModelFamily.Usl
+    params: Tuple[float, float, float] = (0.0, 0.0, 0.0)
+    fit_r2: Optional[float] = None
+
+
+@dataclass
+class WorkloadSpec:
+    mix: WorkloadMix = field(default_factory=lambda: preset_mix("w3"))
+    rps: float = 1.0
+    num_requests: int = 100
+    seed: int = 0
+    length_jitter: float = 0.2
+
+
+@dataclass
+class SchedulerConfig:
+    mode: int = SchedulerMode.Saber
+    window_size: int = 8
+    tick: float = 0.01
+    static_batch_size: int = 0
+
+
+@dataclass
+class EngineConfig:
+    ground_truth: SpeedModel = field(
+        default_factory=lambda: SpeedModel(ModelFamily.Usl, (100.0, 0.05, 0.001)))
+    prefill_rate: float = 2000.0
+
+
+@dataclass
+class SimConfig:
+    workload: WorkloadSpec = field(default_factory=WorkloadSpec)
+    scheduler: SchedulerConfig = field(default_factory=SchedulerConfig)
+    model: Optional[SpeedModel] = None
+    engine: EngineConfig = field(default_factory=EngineConfig)
+    horizon: Optional[float] = None
+    repeats: int = 3
+    seed: int = 0
+
+
+@dataclass
+class Request:
+    id: int
+    task: str
+    arrival_time: float
+    input_tokens: int
+    max_output_tokens: int
+    sla_seconds: float
+    deadline: float
+
+
+@dataclass
+class RunRecord:
+    request_id: int
+    task: str
+    arrival_time: float
+    admit_time: Optional[float]
+    completion_time: Optional[float]
+    sla: float
+    met_sla: bool
+    final_tier: str
+
+
+@dataclass
+class Decision:
+    time: float
+    request_id: int
+    kind: int
+    load_before: int
+    pred_speed: Optional[float]
+    req_speed: Optional[float]
+
+
+@dataclass
+class MetricsReport:
+    goodput: float
+    ratio_mean: float
+    ratio_std: float
+    cv: float
+    completed: int
+    decision_count: int
+    decision_kinds: List[int]
+    decision_hash: int
+    counters: Dict[str, int]
+
+
+@dataclass
+class RunOutput:
+    records: List[RunRecord]
+    decisions: Optional[List[Decision]]
+    metrics: MetricsReport
+
+
+@dataclass
+class SweepGrid:
+    mixes: List[str] = field(default_factory=list)
+    rps_list: List[float] = field(default_factory=list)
+    caps: List[int] = field(default_factory=list)
+    with_saber: bool = False
+
+
+@dataclass
+class SweepRow:
+    mix: str
+    rps: float
+    scheduler: int
+    static_cap: int
+    repeat_seed: int
+    goodput: float
+    ratio_mean: float
+    ratio_std: float
+    cv: float
+
+
+@dataclass
+class MixSummary:
+    saber_mean_goodput: float
+    best_static_mean_goodput: float
+    delta: float
+    saber_pooled_cv: float
+    best_static_pooled_cv: float
+    saber_rps_mean_cv: float
+    best_static_rps_mean_cv: float
+    best_cap_by_rps: Dict[float, int]
+
+
+@dataclass
+class SweepResult:
+    rows: List[SweepRow]
+    summary: Dict[str, MixSummary]
+    # engine extras: the raw per-trajectory rows (decision hashes, counters)
+    traj_rows: Optional[np.ndarray] = None
+    device_ms: float = 0.0
+
+
+def default_rps_sweep() -> List[float]:
+    """workload.cpp:81-85"""
+    return [1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 15, 20]
+
+
+# ----------------------------------------------------------------- helpers
+def _model(m: SpeedModel) -> N.saber_model:
+    x = N.saber_model()
+    x.family = int(m.family)
+    p = list(m.params) + [0.0] * (3 - len(m.params))
+    for i in range(3):
+        x.params[i] = float(p[i])
+    return x
+
+
+def _mix(m: WorkloadMix) -> N.saber_mix:
+    x = N.saber_mix()
+    for name, frac in m.proportions.items():
+        if name not in TASK_INDEX:
+            raise InvalidArgument(f"mix references unknown task: {name}")
+        x.frac[TASK_INDEX[name]] = float(frac)
+        x.present[TASK_INDEX[name]] = 1
+    return x
+
+
+def _row_dtype():
+    fields = []
+    for name, ct in N.saber_traj_row._fields_:
+        length = getattr(ct, "_length_", None)
+        base = ct._type_ if length else ct
+        np_t = np.uint64 if name == "decision_hash" else (np.int64 if base is C.c_int64 else np.float64)
+        fields.append((name, np_t, (length,)) if length else (name, np_t))
+    return np.dtype(fields)
+
+
+ROW_DTYPE = _row_dtype()
+assert ROW_DTYPE.itemsize == C.sizeof(N.saber_traj_row)
+
+COUNTER_NAMES = ["ticks", "passes", "decode_updates", "prefill_updates", "refresh_entries",
+                 "gate_candidates", "ledger_scanned", "rng_draws"]
+
+
+def _spec_from_config(cfg: SimConfig, requests: Optional[Sequence[Request]] = None,
+                      keepalive=None) -> N.saber_traj_spec:
+    s = N.saber_traj_spec()
+    w = cfg.workload
+    s.mix = _mix(w.mix)
+    s.rps = float(w.rps)
+    s.num_requests = int(w.num_requests if requests is None else len(requests))
+    s.workload_seed = int(w.seed) & 0xFFFFFFFFFFFFFFFF
+    s.length_jitter = float(w.length_jitter)
+    if requests is not None:
+        arr = (N.saber_request * max(1, len(requests)))()
+        for i, r in enumerate(requests):
+            if r.id != i:
+                raise InvalidArgument("run: request ids must be 0..n-1")
+            q = arr[i]
+            q.arrival_time = r.arrival_time
+            q.sla_seconds = r.sla_seconds
+            q.deadline = r.deadline
+            q.input_tokens = r.input_tokens
+            q.max_output_tokens = r.max_output_tokens
+            q.task = TASK_INDEX.get(r.task, -1)
+        s.requests = arr
+        if keepalive is not None:
+            keepalive.append(arr)
+    sc = cfg.scheduler
+    s.mode = int(sc.mode)
+    s.window_size = int(sc.window_size)
+    s.tick = float(sc.tick)
+    s.static_batch_size = int(sc.static_batch_size)
+    s.has_model = 1 if cfg.model is not None else 0
+    if cfg.model is not None:
+        s.model = _model(cfg.model)
+    s.ground_truth = _model(cfg.engine.ground_truth)
+    s.prefill_rate = float(cfg.engine.prefill_rate)
+    s.has_horizon = 1 if cfg.horizon is not None else 0
+    s.horizon = float(cfg.horizon) if cfg.horizon is not None else 0.0
+    s.seed = int(cfg.seed) & 0xFFFFFFFFFFFFFFFF
+    return s
+
+
+# ----------------------------------------------------------------- run path
+@dataclass
+class BatchResult:
+    rows: np.ndarray                     # ROW_DTYPE [n_traj]
+    completion_times: np.ndarray         # [n_traj][max_n] NaN = never
+    arrival_times: Optional[np.ndarray] = None
+    admit_times: Optional[np.ndarray] = None
+    demoted: Optional[np.ndarray] = None
+    decisions: Optional[List[np.ndarray]] = None
+    device_ms: float = 0.0
+    kernel_launches: int = 0
+
+
+DECISION_DTYPE = np.dtype([("time", np.float64), ("request_id", np.uint64), ("kind", np.int32),
+                           ("load_before", np.int32), ("has_pred", np.int32), ("has_req", np.int32),
+                           ("pred_speed", np.float64), ("req_speed", np.float64)])
+assert DECISION_DTYPE.itemsize == C.sizeof(N.saber_decision)
+
+
+def run_batch(configs: Sequence[SimConfig], requests: Optional[Sequence[Optional[Sequence[Request]]]] = None,
+              records: bool = False, decisions: bool = False, decision_cap: int = 1 << 16,
+              device: int = 0) -> BatchResult:
+    """Many independent run()/run_with_requests() trajectories in one launch."""
+    T = len(configs)
+    if T == 0:
+        raise InvalidArgument("run_batch: no trajectories")
+    keep: list = []
+    specs = (N.saber_traj_spec * T)()
+    for k, cfg in enumerate(configs):
+        reqs = requests[k] if requests is not None else None
+        specs[k] = _spec_from_config(cfg, reqs, keep)
+    max_n = max(int(s.num_requests) for s in specs)
+    rows = np.zeros(T, dtype=ROW_DTYPE)
+    comp = np.full((T, max_n), np.nan)
+    arr = np.full((T, max_n), np.nan) if records else None
+    adm = np.full((T, max_n), np.nan) if records else None
+    dem = np.zeros((T, max_n), dtype=np.uint8) if records else None
+    dec = np.zeros((T, decision_cap), dtype=DECISION_DTYPE) if decisions else None
+    ndec = np.zeros(T, dtype=np.int64) if decisions else None
+    d = N.saber_run_batch_desc()
+    d.specs = specs
+    d.n_traj = T
+    d.device = device
+    o = N.saber_run_batch_out()
+    P = C.POINTER
+    o.rows = rows.ctypes.data_as(P(N.saber_traj_row))
+    o.completion_times = comp.ctypes.data_as(P(C.c_double))
+    o.max_n = max_n
+    if records:
+        o.arrival_times = arr.ctypes.data_as(P(C.c_double))
+        o.admit_times = adm.ctypes.data_as(P(C.c_double))
+        o.demoted = dem.ctypes.data_as(P(C.c_uint8))
+    if decisions:
+        o.decisions = dec.ctypes.data_as(P(N.saber_decision))
+        o.decision_cap = decision_cap
+        o.n_decisions = ndec.ctypes.data_as(P(C.c_int64))
+    _check(N.lib().saber_cuda_run_batch(C.byref(d), C.byref(o)))
+    decs = [dec[k, : ndec[k]].copy() for k in range(T)] if decisions else None
+    return BatchResult(rows, comp, arr, adm, dem, decs, o.device_ms, o.kernel_launches)
+
+
+def _run_output(cfg: SimConfig, res: BatchResult, k: int, requests=None) -> RunOutput:
+    row = res.rows[k]
+    n = int(row["n"])
+    recs = []
+    if res.arrival_times is not None:
+        names = [r.task for r in requests] if requests is not None else None
+        for i in range(n):
+            c = res.completion_times[k, i]
+            a = res.arrival_times[k, i]
+            ad = res.admit_times[k, i]
+            sla = requests[i].sla_seconds if requests is not None else None
+            recs.append(RunRecord(i, names[i] if names else "", float(a),
+                                  None if math.isnan(ad) else float(ad),
+                                  None if math.isnan(c) else float(c), sla if sla is not None else float("nan"),
+                                  (not math.isnan(c)) and sla is not None and (c - a) <= sla,
+                                  "low" if res.demoted[k, i] else "high"))
+    decs = None
+    if res.decisions is not None:
+        decs = [Decision(float(x["time"]), int(x["request_id"]), int(x["kind"]), int(x["load_before"]),
+                         float(x["pred_speed"]) if x["has_pred"] else None,
+                         float(x["req_speed"]) if x["has_req"] else None) for x in res.decisions[k]]
+    m = MetricsReport(float(row["goodput"]), float(row["ratio_mean"]), float(row["ratio_std"]),
+                      float(row["cv"]), int(row["completed"]), int(row["decisions"]),
+                      [int(v) for v in row["n_kind"]], int(row["decision_hash"]),
+                      {c: int(row[c]) for c in COUNTER_NAMES})
+    return RunOutput(recs, decs, m)
+
+
+def run(config: SimConfig, decisions: bool = True, device: int = 0) -> RunOutput:
+    """simloop.cpp:113-116: generate() then the tick loop, on the GPU."""
+    res = run_batch([config], records=True, decisions=decisions, decision_cap=1 << 20, device=device)
+    return _run_output(config, res, 0)
+
+
+def run_with_requests(config: SimConfig, requests: Sequence[Request], decisions: bool = True,
+                      device: int = 0) -> RunOutput:
+    """simloop.cpp:50-111 over a caller-supplied workload (replay)."""
+    if len(requests) == 0:
+        raise InvalidArgument("run: no requests")
+    res = run_batch([config], [requests], records=True, decisions=decisions,
+                    decision_cap=1 << 20, device=device)
+    return _run_output(config, res, 0, requests)
+
+
+# ---------------------------------------------------------------- sweep path
+class SweepPlan:
+    """Staged sweep (saber_cuda_sweep_plan_*): create once, run many times."""
+
+    def __init__(self, grid: SweepGrid, base: SimConfig, device: int = 0, shard_index: int = 0,
+                 shard_count: int = 1):
+        self.grid = grid
+        self.base = base
+        self._keep = []
+        d = N.saber_sweep_desc()
+        mix_ids = []
+        for m in grid.mixes:
+            if m not in ("w1", "w2", "w3"):
+                raise InvalidArgument(f"unknown mix preset: {m}")
+            mix_ids.append(int(m[1:]))
+        mixes = (C.c_int32 * max(1, len(mix_ids)))(*mix_ids)
+        rps = (C.c_double * max(1, len(grid.rps_list)))(*[float(r) for r in grid.rps_list])
+        caps = (C.c_int32 * max(1, len(grid.caps)))(*[int(c) for c in grid.caps])
+        self._keep += [mixes, rps, caps]
+        d.mixes, d.n_mixes = mixes, len(mix_ids)
+        d.rps, d.n_rps = rps, len(grid.rps_list)
+        d.caps, d.n_caps = caps, len(grid.caps)
+        d.with_saber = 1 if grid.with_saber else 0
+        d.num_requests = base.workload.num_requests
+        d.length_jitter = base.workload.length_jitter
+        d.window_size = base.scheduler.window_size
+        d.tick = base.scheduler.tick
+        d.has_model = 1 if base.model is not None else 0
+        if base.model is not None:
+            d.model = _model(base.model)
+        d.ground_truth = _model(base.engine.ground_truth)
+        d.prefill_rate = base.engine.prefill_rate
+        d.has_horizon = 1 if base.horizon is not None else 0
+        d.horizon = float(base.horizon) if base.horizon is not None else 0.0
+        d.repeats = base.repeats
+        d.seed = int(base.seed) & 0xFFFFFFFFFFFFFFFF
+        d.device = device
+        d.shard_index = shard_index
+        d.shard_count = shard_count
+        self.desc = d
+        self.n_rows = int(N.lib().saber_cuda_sweep_rows(C.byref(d)))
+        h = C.c_void_p()
+        _check(N.lib().saber_cuda_sweep_plan_create(C.byref(d), C.byref(h)))
+        self.handle = h
+
+    def run(self, stream: int = 0):
+        _check(N.lib().saber_cuda_sweep_plan_run(self.handle, C.c_void_p(stream)))
+
+    def summarize(self, stream: int = 0):
+        _check(N.lib().saber_cuda_sweep_plan_summarize(self.handle, C.c_void_p(stream)))
+
+    def buffers(self) -> N.saber_sweep_buffers:
+        b = N.saber_sweep_buffers()
+        _check(N.lib().saber_cuda_sweep_plan_buffers(self.handle, C.byref(b)))
+        return b
+
+    def stats(self):
+        a, b, c = C.c_double(), C.c_double(), C.c_int32()
+        _check(N.lib().saber_cuda_sweep_plan_stats(self.handle, C.byref(a), C.byref(b), C.byref(c)))
+        return a.value, b.value, c.value
+
+    def fetch(self, completion=False, summary=True):
+        rows = np.zeros(self.n_rows, dtype=ROW_DTYPE)
+        o = N.saber_sweep_out()
+        o.rows = rows.ctypes.data_as(C.POINTER(N.saber_traj_row))
+        comp = None
+        if completion:
+            comp = np.empty((self.n_rows, self.desc.num_requests))
+            o.completion_times = comp.ctypes.data_as(C.POINTER(C.c_double))
+        summ = best = None
+        if summary:
+            summ = (N.saber_mix_summary * self.desc.n_mixes)()
+            best = np.zeros((self.desc.n_mixes, self.desc.n_rps), dtype=np.int32)
+            o.summary = summ
+            o.best_cap_by_rps = best.ctypes.data_as(C.POINTER(C.c_int32))
+        _check(N.lib().saber_cuda_sweep_plan_fetch(self.handle, C.byref(o)))
+        return rows, comp, summ, best
+
+    def close(self):
+        if self.handle:
+            N.lib().saber_cuda_sweep_plan_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def sweep_row_keys(grid: SweepGrid, base: SimConfig):
+    """(mix, rps, mode, cap, seed) per row in the reference's grid order (simloop.cpp:137-152)."""
+    keys = []
+    for m in grid.mixes:
+        for r in grid.rps_list:
+            for c in grid.caps:
+                for i in range(base.repeats):
+                    keys.append((m, float(r), SchedulerMode.Static, int(c), base.seed + i))
+            if grid.with_saber:
+                for i in range(base.repeats):
+                    keys.append((m, float(r), SchedulerMode.Saber, 0, base.seed + i))
+    return keys
+
+
+def sweep(grid: SweepGrid, base: SimConfig, jobs: int = 0, device: int = 0,
+          completion: bool = False) -> SweepResult:
+    """simloop.cpp:130-277 on the GPU.  `jobs` is accepted for API parity; the
+    device decides its own parallelism and the output never depends on it."""
+    del jobs
+    if not grid.mixes or not grid.rps_list or (not grid.caps and not grid.with_saber):
+        raise InvalidArgument("sweep: empty grid")
+    if grid.with_saber and base.model is None:
+        raise InvalidArgument("sweep: saber variant requires a model")
+    plan = SweepPlan(grid, base, device=device)
+    try:
+        plan.run()
+        plan.summarize()
+        rows, comp, summ, best = plan.fetch(completion=completion)
+        dev_ms = plan.stats()[0]
+    finally:
+        plan.close()
+    out_rows = []
+    for (m, r, mode, cap, seed), row in zip(sweep_row_keys(grid, base), rows):
+        out_rows.append(SweepRow(m, r, mode, cap, seed, float(row["goodput"]), float(row["ratio_mean"]),
+                                 float(row["ratio_std"]), float(row["cv"])))
+    summary = {}
+    for k, m in enumerate(grid.mixes):
+        s = summ[k]
+        caps = {float(r): int(best[k, j]) for j, r in enumerate(grid.rps_list)} if grid.caps else {}
+        summary[m] = MixSummary(s.saber_mean_goodput, s.best_static_mean_goodput, s.delta,
+                                s.saber_pooled_cv, s.best_static_pooled_cv, s.saber_rps_mean_cv,
+                                s.best_static_rps_mean_cv, caps)
+    res = SweepResult(out_rows, summary, rows, dev_ms)
+    if completion:
+        res.completion_times = comp
+    return res
+
+
+# ---------------------------------------------------------------- estimator
+def predict(model: SpeedModel, load: int) -> float:
+    """estimator.cpp:234-237 (host table builder shared with the engine)."""
+    if load < 1:
+        raise DomainError("predict: load must be >= 1")
+    tab = (C.c_double * load)()
+    _check(N.lib().saber_cuda_predict_table(C.byref(_model(model)), load, tab))
+    return tab[load - 1]
+
+
+def max_speed(model: SpeedModel) -> float:
+    return predict(model, 1)
+
+
+def device_count() -> int:
+    return int(N.lib().saber_cuda_device_count())
+
+
+def fp64_peak_tflops(device: int = 0) -> float:
+    v = C.c_double()
+    _check(N.lib().saber_cuda_fp64_peak(device, C.byref(v)))
+    return v.value

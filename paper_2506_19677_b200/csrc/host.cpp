@@ -1,0 +1,1083 @@
+// host.cpp — host orchestration behind the C ABI (include/saber_cuda.h).
+//
+// Responsibilities:
+//   * validation with the reference's error semantics (types.cpp:94-100,
+//     workload.cpp:41-48, simloop.cpp:38-48, 130-136);
+//   * the per-seed workload prologue: std::mt19937_64 draws and glibc log
+//      — the only host arithmetic on the path, kept here
+//     because glibc's log is not correctly rounded and the device cannot
+//     reproduce it bit-for-bit;
+//   * predict tables per model (glibc exp for the logistic);
+//   * device memory (a grow-only per-device cache), H2D/D2H, kernel launches.
+// Compiled with g++ without FMA contraction, like the reference.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <random>
+#include <string>
+#include <vector>
+
+#include "saber_internal.h"
+
+using namespace saberb200;
+
+namespace {
+
+thread_local std::string g_err;
+
+saber_status fail(saber_status s, const std::string& msg) {
+  g_err = msg;
+  return s;
+}
+
+#define CUDA_TRY(expr)                                                                  \
+  do {                                                                                  \
+    cudaError_t e_ = (expr);                                                            \
+    if (e_ != cudaSuccess)                                                              \
+      return fail(SABER_ECUDA, std::string(#expr) + ": " + cudaGetErrorString(e_));    \
+  } while (0)
+
+#define LAUNCH_TRY(expr)                                                                    \
+  do {                                                                                      \
+    if ((expr) != 0)                                                                        \
+      return fail(SABER_ECUDA,                                                              \
+                  std::string("kernel launch failed: ") + cudaGetErrorString(cudaGetLastError())); \
+  } while (0)
+
+// ---------------------------------------------------------------- devices --
+saber_status use_device(int device) {
+  int count = 0;
+  cudaError_t e = cudaGetDeviceCount(&count);
+  if (e != cudaSuccess || count == 0)
+    return fail(SABER_ECUDA, "no CUDA device available (the engine has no CPU fallback)");
+  if (device < 0 || device >= count)
+    return fail(SABER_EINVAL, "device ordinal " + std::to_string(device) + " out of range");
+  cudaDeviceProp prop;
+  CUDA_TRY(cudaGetDeviceProperties(&prop, device));
+  if (prop.major != 10)
+    return fail(SABER_ECUDA, std::string("device is not sm_100 (Blackwell): ") + prop.name);
+  CUDA_TRY(cudaSetDevice(device));
+  return SABER_OK;
+}
+
+// -------------------------------------------------- grow-only device cache --
+struct Block {
+  void* p;
+  size_t bytes;
+};
+std::mutex g_pool_mu;
+std::map<int, std::multimap<size_t, void*>> g_free;  // device -> size -> ptr
+
+void* pool_alloc(int device, size_t bytes) {
+  bytes = (bytes + 255) & ~static_cast<size_t>(255);
+  if (bytes == 0) bytes = 256;
+  {
+    std::lock_guard<std::mutex> lk(g_pool_mu);
+    auto& fl = g_free[device];
+    auto it = fl.lower_bound(bytes);
+    if (it != fl.end() && it->first <= 2 * bytes + (1 << 20)) {
+      void* p = it->second;
+      fl.erase(it);
+      return p;
+    }
+  }
+  void* p = nullptr;
+  if (cudaMalloc(&p, bytes) != cudaSuccess) return nullptr;
+  return p;
+}
+void pool_free(int device, void* p, size_t bytes) {
+  if (!p) return;
+  bytes = (bytes + 255) & ~static_cast<size_t>(255);
+  if (bytes == 0) bytes = 256;
+  std::lock_guard<std::mutex> lk(g_pool_mu);
+  g_free[device].emplace(bytes, p);
+}
+
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  int device = 0;
+  DevBuf() = default;
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  ~DevBuf() { release(); }
+  void release() {
+    pool_free(device, p, bytes);
+    p = nullptr;
+    bytes = 0;
+  }
+  bool alloc(int dev, size_t n) {
+    release();
+    device = dev;
+    bytes = n;
+    p = pool_alloc(dev, n);
+    return p != nullptr;
+  }
+  template <class T>
+  T* as() const {
+    return static_cast<T*>(p);
+  }
+};
+
+#define ALLOC_TRY(buf, dev, n)                                                         \
+  do {                                                                                 \
+    if (!(buf).alloc((dev), (n)))                                                      \
+      return fail(SABER_ECUDA, "device allocation of " + std::to_string(n) + " bytes failed"); \
+  } while (0)
+
+// ------------------------------------------------------ reference arithmetic --
+const int kAvgInH[4] = {186, 463, 31, 670};
+const int kAvgOutH[4] = {43, 387, 30, 617};
+const double kSlaH[4] = {1.0, 8.0, 1.0, 12.0};
+// std::map<std::string,...> order: code_generation, code_qna, code_summary, code_translation
+const int kAlphaH[4] = {SABER_TASK_GENERATION, SABER_TASK_QNA, SABER_TASK_SUMMARY,
+                        SABER_TASK_TRANSLATION};
+constexpr uint64_t kSchedulerSeedSalt = 0x9e3779b97f4a7c15ull;  // scheduler.cpp:14
+
+// estimator.cpp:16-31 (eval), restated with libstdc++'s min/max/clamp.
+double eval_model(const saber_model& m, double load) {
+  const double* p = m.params;
+  switch (m.family) {
+    case SABER_USL: {
+      const double denom = 1.0 + p[1] * (load - 1.0) + p[2] * load * (load - 1.0);
+      return p[0] / denom;
+    }
+    case SABER_LOGISTIC: {
+      double arg = p[1] * (load - p[2]);
+      arg = std::min(std::max(arg, -700.0), 700.0);
+      return p[0] / (1.0 + std::exp(arg));
+    }
+    case SABER_LINEAR:
+      return std::max(p[0] * load + p[1], 1e-6);
+  }
+  return 0.0;
+}
+
+bool valid_family(int f) { return f == SABER_USL || f == SABER_LOGISTIC || f == SABER_LINEAR; }
+
+saber_status validate_mix(const saber_mix& mix) {
+  bool any = false;
+  double sum = 0.0;
+  for (int a = 0; a < 4; ++a) {
+    const int t = kAlphaH[a];
+    if (!mix.present[t]) continue;
+    any = true;
+    if (mix.frac[t] < 0.0 || mix.frac[t] > 1.0)
+      return fail(SABER_EINVAL, "mix fraction out of [0,1]");
+    sum += mix.frac[t];
+  }
+  if (!any) return fail(SABER_EINVAL, "mix has no tasks");
+  if (std::abs(sum - 1.0) > 1e-9)
+    return fail(SABER_EINVAL, "mix fractions sum to " + std::to_string(sum));
+  return SABER_OK;
+}
+
+saber_mix preset(int id) {
+  saber_mix m{};
+  for (int t = 0; t < 4; ++t) m.present[t] = 1;
+  if (id == 1) {  // types.cpp:28-33
+    m.frac[SABER_TASK_TRANSLATION] = 0.4;
+    m.frac[SABER_TASK_GENERATION] = 0.4;
+    m.frac[SABER_TASK_QNA] = 0.1;
+    m.frac[SABER_TASK_SUMMARY] = 0.1;
+  } else if (id == 2) {  // types.cpp:35-40
+    m.frac[SABER_TASK_QNA] = 0.4;
+    m.frac[SABER_TASK_SUMMARY] = 0.4;
+    m.frac[SABER_TASK_GENERATION] = 0.1;
+    m.frac[SABER_TASK_TRANSLATION] = 0.1;
+  } else {  // w3, types.cpp:42-46
+    for (int t = 0; t < 4; ++t) m.frac[t] = 0.25;
+  }
+  return m;
+}
+
+// Cumulative thresholds in map order, summed exactly as sample_task does.
+void mix_thresholds(const saber_mix& m, double* th, int8_t* task, int8_t* last) {
+  double cum = 0.0;
+  int k = 0;
+  *last = -1;
+  for (int a = 0; a < 4; ++a) {
+    const int t = kAlphaH[a];
+    if (!m.present[t]) continue;
+    cum += m.frac[t];
+    th[k] = cum;
+    task[k] = static_cast<int8_t>(t);
+    *last = static_cast<int8_t>(t);
+    ++k;
+  }
+  for (; k < 4; ++k) {
+    th[k] = 0.0;
+    task[k] = -1;
+  }
+}
+
+// Per-seed draws of generate() (workload.cpp:52-79): 4 per request in order
+// gap, task, input length, output length; the gap kept as glibc -log(1-u).
+void seed_draws(uint64_t seed, int n, double* out4, double* neglog_sum) {
+  std::mt19937_64 rng(seed);
+  double s = 0.0;
+  for (int i = 0; i < n; ++i) {
+    const double u = static_cast<double>(rng() >> 11) * 0x1.0p-53;
+    const double nl = -std::log(1.0 - u);
+    out4[4 * i + 0] = nl;
+    out4[4 * i + 1] = static_cast<double>(rng() >> 11) * 0x1.0p-53;
+    out4[4 * i + 2] = static_cast<double>(rng() >> 11) * 0x1.0p-53;
+    out4[4 * i + 3] = static_cast<double>(rng() >> 11) * 0x1.0p-53;
+    s += nl;
+  }
+  *neglog_sum = s;
+}
+
+// Upper bound on scheduler draws for a trajectory whose horizon is <= hb:
+// ticks <= hb/tick + 3 (t = min(t+tick, horizon) accumulation), and each tick
+// consumes min(window, |high|) - 1 <= min(window, n) - 1 draws.
+int64_t draw_bound(double hb, double tick, int window, int n) {
+  const int per = std::min(window, n) - 1;
+  if (per <= 0) return 0;
+  const double ticks = hb / tick * (1.0 + 1e-9) + 3.0;
+  const double b = ticks * per;
+  const double cap = 1ull << 28;
+  return static_cast<int64_t>(std::min(b, cap));
+}
+
+void fill_table(const saber_model& m, int max_load, double* out) {
+  out[0] = std::nan("");
+  for (int L = 1; L <= max_load; ++L) out[L] = eval_model(m, static_cast<double>(L));
+}
+
+// Picks the register-mask width for n requests.
+int nwords_for(int n) {
+  if (n <= 64) return 1;
+  if (n <= 128) return 2;
+  if (n <= 256) return 4;
+  return 8;
+}
+
+// ----------------------------------------------------------- lane scratch --
+struct Scratch {
+  DevBuf g, m, id, ledger, low;
+  int grid = 0;
+  LaneScratch view{};
+  saber_status alloc(int device, int nwords, int nmax) {
+    int grid_ = 0;
+    if (sim_occupancy_grid(nwords, 128, &grid_) != 0)
+      return fail(SABER_ECUDA, "occupancy query failed");
+    grid = grid_;
+    const size_t lanes = static_cast<size_t>(grid) * 128;
+    const size_t per = static_cast<size_t>(nmax);
+    ALLOC_TRY(g, device, lanes * per * sizeof(double));
+    ALLOC_TRY(m, device, lanes * per * sizeof(double));
+    ALLOC_TRY(id, device, lanes * per * sizeof(uint16_t));
+    ALLOC_TRY(ledger, device, lanes * per * sizeof(double));
+    ALLOC_TRY(low, device, lanes * per * sizeof(uint16_t));
+    view.slot_g = g.as<double>();
+    view.slot_m = m.as<double>();
+    view.slot_id = id.as<uint16_t>();
+    view.ledger_need = ledger.as<double>();
+    view.low_fifo = low.as<uint16_t>();
+    view.slots = nmax;
+    return SABER_OK;
+  }
+};
+
+struct Workloads {
+  DevBuf arr, dl, sla, mo, in, task, dem, hor, items, seed_base, th, tt, tl;
+  WorkloadTables view(int nmax) const {
+    WorkloadTables w;
+    w.arrival = arr.as<double>();
+    w.deadline = dl.as<double>();
+    w.sla = sla.as<double>();
+    w.max_out = mo.as<double>();
+    w.input = in.as<double>();
+    w.task = task.as<int8_t>();
+    w.demote_after = dem.as<double>();
+    w.horizon = hor.as<double>();
+    w.nmax = nmax;
+    return w;
+  }
+  saber_status alloc(int device, int64_t n_work, int nmax) {
+    const size_t cells = static_cast<size_t>(n_work) * nmax;
+    ALLOC_TRY(arr, device, cells * 8);
+    ALLOC_TRY(dl, device, cells * 8);
+    ALLOC_TRY(sla, device, cells * 8);
+    ALLOC_TRY(mo, device, cells * 8);
+    ALLOC_TRY(in, device, cells * 8);
+    ALLOC_TRY(task, device, cells);
+    ALLOC_TRY(dem, device, cells * 8);
+    ALLOC_TRY(hor, device, static_cast<size_t>(n_work) * 8);
+    return SABER_OK;
+  }
+};
+
+struct Timer {
+  cudaEvent_t a = nullptr, b = nullptr;
+  ~Timer() {
+    if (a) cudaEventDestroy(a);
+    if (b) cudaEventDestroy(b);
+  }
+  saber_status init() {
+    if (!a) CUDA_TRY(cudaEventCreate(&a));
+    if (!b) CUDA_TRY(cudaEventCreate(&b));
+    return SABER_OK;
+  }
+};
+
+saber_status validate_model(const saber_model& m, const char* what) {
+  if (!valid_family(m.family))
+    return fail(SABER_EINVAL, std::string(what) + ": unknown model family");
+  return SABER_OK;
+}
+
+}  // namespace
+
+// ============================================================== the sweep ==
+struct saber_sweep_plan {
+  saber_sweep_desc desc{};
+  std::vector<int32_t> mixes, caps;
+  std::vector<double> rps;
+  int device = 0;
+  int n = 0, R = 0, nwords = 1;
+  int64_t n_rows = 0, rows_shard = 0;
+  int n_items = 0;
+  int model_tab = -1, gt_tab = 0;
+  double ceiling = 0.0;
+  std::vector<int64_t> stream_len;
+  int64_t total_draws = 0;
+
+  Workloads wl;
+  DevBuf tables, seeds, s_off, s_len, draws, descs, rows, comp, cursor, err, caps_d;
+  DevBuf summary, best_cap, cell_scratch;
+  Scratch scratch;
+  Timer all, sim;
+  double last_ms = 0.0, sim_ms = 0.0;
+  int launches = 0;
+  bool summarized = false;
+};
+
+namespace {
+
+saber_status validate_sweep(const saber_sweep_desc& d) {
+  if (d.n_mixes < 1 || d.n_rps < 1 || (d.n_caps < 1 && !d.with_saber))
+    return fail(SABER_EINVAL, "sweep: empty grid");
+  if (d.with_saber && !d.has_model)
+    return fail(SABER_EINVAL, "sweep: saber variant requires a model");
+  for (int i = 0; i < d.n_mixes; ++i)
+    if (d.mixes[i] < 1 || d.mixes[i] > 3)
+      return fail(SABER_EINVAL, "unknown mix preset: w" + std::to_string(d.mixes[i]));
+  for (int i = 0; i < d.n_rps; ++i)
+    if (!(d.rps[i] > 0.0)) return fail(SABER_EINVAL, "rps must be > 0");
+  if (d.num_requests < 1) return fail(SABER_EINVAL, "num_requests must be >= 1");
+  if (d.num_requests > kMaxRequests)
+    return fail(SABER_EINVAL, "num_requests > " + std::to_string(kMaxRequests) +
+                                  " is not supported by the B200 engine");
+  if (d.length_jitter < 0.0 || d.length_jitter >= 1.0)
+    return fail(SABER_EINVAL, "length_jitter must be in [0, 1)");
+  if (d.window_size < 1) return fail(SABER_EINVAL, "window_size must be >= 1");
+  if (d.window_size > kMaxWindow)
+    return fail(SABER_EINVAL, "window_size > " + std::to_string(kMaxWindow) +
+                                  " is not supported by the B200 engine");
+  if (!(d.tick > 0.0)) return fail(SABER_EINVAL, "tick must be > 0");
+  for (int i = 0; i < d.n_caps; ++i)
+    if (d.caps[i] < 1) return fail(SABER_EINVAL, "static mode requires a positive batch size");
+  if (d.repeats < 1) return fail(SABER_EINVAL, "repeats must be >= 1");
+  if (d.has_horizon && !(d.horizon > 0.0)) return fail(SABER_EINVAL, "horizon must be > 0");
+  if (saber_status s = validate_model(d.ground_truth, "ground truth")) return s;
+  if (d.has_model)
+    if (saber_status s = validate_model(d.model, "model")) return s;
+  if (!(eval_model(d.ground_truth, 1.0) > 0.0))
+    return fail(SABER_EINVAL, "engine ground truth must be positive");
+  if (d.shard_count < 1 || d.shard_index < 0 || d.shard_index >= d.shard_count)
+    return fail(SABER_EINVAL, "bad shard index/count");
+  return SABER_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int64_t saber_cuda_sweep_rows(const saber_sweep_desc* d) {
+  if (!d) return 0;
+  const int64_t per_rps =
+      static_cast<int64_t>(d->n_caps) * d->repeats + (d->with_saber ? d->repeats : 0);
+  return static_cast<int64_t>(d->n_mixes) * d->n_rps * per_rps;
+}
+
+saber_status saber_cuda_sweep_plan_create(const saber_sweep_desc* desc, saber_sweep_plan** out) {
+  if (!desc || !out) return fail(SABER_EINVAL, "null argument");
+  *out = nullptr;
+  if (saber_status s = validate_sweep(*desc)) return s;
+  if (saber_status s = use_device(desc->device)) return s;
+  auto* P = new saber_sweep_plan();
+  std::unique_ptr<saber_sweep_plan> guard(P);
+  P->desc = *desc;
+  P->mixes.assign(desc->mixes, desc->mixes + desc->n_mixes);
+  P->rps.assign(desc->rps, desc->rps + desc->n_rps);
+  P->caps.assign(desc->caps, desc->caps + desc->n_caps);
+  P->desc.mixes = P->mixes.data();
+  P->desc.rps = P->rps.data();
+  P->desc.caps = P->caps.data();
+  P->device = desc->device;
+  P->n = desc->num_requests;
+  P->R = desc->repeats;
+  P->nwords = nwords_for(P->n);
+  P->n_rows = saber_cuda_sweep_rows(desc);
+  P->rows_shard = (P->n_rows - desc->shard_index + desc->shard_count - 1) / desc->shard_count;
+  if (P->rows_shard < 0) P->rows_shard = 0;
+  const int n = P->n, R = P->R, dev = P->device;
+  const int n_mixes = desc->n_mixes, n_rps = desc->n_rps;
+
+  // Host prologue: per-seed generate() draws (glibc log), F5/F8.
+  std::vector<double> base(static_cast<size_t>(R) * n * 4);
+  std::vector<double> neglog_sum(static_cast<size_t>(R));
+  for (int i = 0; i < R; ++i)
+    seed_draws(desc->seed + static_cast<uint64_t>(i), n, &base[static_cast<size_t>(i) * n * 4],
+               &neglog_sum[static_cast<size_t>(i)]);
+
+  // Predict tables: [gt | model], index L in 1..n+1.
+  const int tl = n + 2;
+  std::vector<double> tab(static_cast<size_t>(2 * tl));
+  fill_table(desc->ground_truth, n + 1, &tab[0]);
+  P->gt_tab = 0;
+  if (desc->has_model) {
+    fill_table(desc->model, n + 1, &tab[static_cast<size_t>(tl)]);
+    P->model_tab = tl;
+    P->ceiling = tab[static_cast<size_t>(tl) + 1];
+  } else {
+    P->ceiling = std::nan("");
+  }
+
+  // Workload items: (mix, rps, repeat) -> generate().
+  P->n_items = n_mixes * n_rps * R;
+  std::vector<WorkloadItem> items(static_cast<size_t>(P->n_items));
+  for (int mi = 0; mi < n_mixes; ++mi)
+    for (int ri = 0; ri < n_rps; ++ri)
+      for (int r = 0; r < R; ++r) {
+        WorkloadItem& it = items[static_cast<size_t>((mi * n_rps + ri) * R + r)];
+        it.kind = 0;
+        it.n = n;
+        it.seed_idx = r;
+        it.mix = mi;
+        it.rps = P->rps[static_cast<size_t>(ri)];
+        it.jitter = desc->length_jitter;
+        it.ceiling = desc->with_saber ? P->ceiling : std::nan("");
+      }
+  std::vector<double> th(static_cast<size_t>(n_mixes) * 4);
+  std::vector<int8_t> tt(static_cast<size_t>(n_mixes) * 4), tlast(static_cast<size_t>(n_mixes));
+  for (int mi = 0; mi < n_mixes; ++mi)
+    mix_thresholds(preset(P->mixes[static_cast<size_t>(mi)]), &th[static_cast<size_t>(mi) * 4],
+                   &tt[static_cast<size_t>(mi) * 4], &tlast[static_cast<size_t>(mi)]);
+
+  // Scheduler RNG streams, one per seed, sized by the horizon bound.
+  std::vector<uint64_t> seeds;
+  std::vector<int64_t> off;
+  if (desc->with_saber) {
+    double rmin = P->rps[0];
+    for (double r : P->rps) rmin = std::min(rmin, r);
+    for (int i = 0; i < R; ++i) {
+      const double last = neglog_sum[static_cast<size_t>(i)] / rmin * (1.0 + 1e-9) + n * 1e-6;
+      const double hb = desc->has_horizon ? desc->horizon : last + 10.0 * 12.0 + 1.0;
+      const int64_t len = draw_bound(hb, desc->tick, desc->window_size, n);
+      seeds.push_back((desc->seed + static_cast<uint64_t>(i)) ^ kSchedulerSeedSalt);
+      off.push_back(P->total_draws);
+      P->stream_len.push_back(len);
+      P->total_draws += len;
+    }
+  }
+
+  // Device buffers.
+  if (saber_status s = P->wl.alloc(dev, P->n_items, n)) return s;
+  ALLOC_TRY(P->wl.items, dev, items.size() * sizeof(WorkloadItem));
+  ALLOC_TRY(P->wl.seed_base, dev, base.size() * 8);
+  ALLOC_TRY(P->wl.th, dev, th.size() * 8);
+  ALLOC_TRY(P->wl.tt, dev, tt.size());
+  ALLOC_TRY(P->wl.tl, dev, tlast.size());
+  ALLOC_TRY(P->tables, dev, tab.size() * 8);
+  ALLOC_TRY(P->caps_d, dev, std::max<size_t>(1, P->caps.size()) * 4);
+  ALLOC_TRY(P->descs, dev, static_cast<size_t>(std::max<int64_t>(1, P->rows_shard)) * sizeof(TrajDesc));
+  ALLOC_TRY(P->rows, dev, static_cast<size_t>(P->n_rows) * sizeof(saber_traj_row));
+  ALLOC_TRY(P->comp, dev, static_cast<size_t>(P->n_rows) * n * 8);
+  ALLOC_TRY(P->cursor, dev, 16);
+  ALLOC_TRY(P->err, dev, 16);
+  ALLOC_TRY(P->summary, dev, static_cast<size_t>(n_mixes) * sizeof(saber_mix_summary));
+  ALLOC_TRY(P->best_cap, dev, static_cast<size_t>(n_mixes) * n_rps * 4);
+  ALLOC_TRY(P->cell_scratch, dev, static_cast<size_t>(n_mixes) * n_rps * 6 * 8);
+  if (desc->with_saber) {
+    ALLOC_TRY(P->seeds, dev, seeds.size() * 8);
+    ALLOC_TRY(P->s_off, dev, off.size() * 8);
+    ALLOC_TRY(P->s_len, dev, off.size() * 8);
+    ALLOC_TRY(P->draws, dev, static_cast<size_t>(std::max<int64_t>(1, P->total_draws)) * 4);
+  }
+  if (saber_status s = P->scratch.alloc(dev, P->nwords, n)) return s;
+
+  CUDA_TRY(cudaMemcpy(P->wl.items.p, items.data(), items.size() * sizeof(WorkloadItem),
+                      cudaMemcpyHostToDevice));
+  CUDA_TRY(cudaMemcpy(P->wl.seed_base.p, base.data(), base.size() * 8, cudaMemcpyHostToDevice));
+  CUDA_TRY(cudaMemcpy(P->wl.th.p, th.data(), th.size() * 8, cudaMemcpyHostToDevice));
+  CUDA_TRY(cudaMemcpy(P->wl.tt.p, tt.data(), tt.size(), cudaMemcpyHostToDevice));
+  CUDA_TRY(cudaMemcpy(P->wl.tl.p, tlast.data(), tlast.size(), cudaMemcpyHostToDevice));
+  CUDA_TRY(cudaMemcpy(P->tables.p, tab.data(), tab.size() * 8, cudaMemcpyHostToDevice));
+  if (!P->caps.empty())
+    CUDA_TRY(cudaMemcpy(P->caps_d.p, P->caps.data(), P->caps.size() * 4, cudaMemcpyHostToDevice));
+  if (desc->with_saber) {
+    CUDA_TRY(cudaMemcpy(P->seeds.p, seeds.data(), seeds.size() * 8, cudaMemcpyHostToDevice));
+    CUDA_TRY(cudaMemcpy(P->s_off.p, off.data(), off.size() * 8, cudaMemcpyHostToDevice));
+    CUDA_TRY(cudaMemcpy(P->s_len.p, P->stream_len.data(), off.size() * 8, cudaMemcpyHostToDevice));
+  }
+  if (saber_status s = P->all.init()) return s;
+  if (saber_status s = P->sim.init()) return s;
+  *out = guard.release();
+  return SABER_OK;
+}
+
+saber_status saber_cuda_sweep_plan_run(saber_sweep_plan* P, void* stream) {
+  if (!P) return fail(SABER_EINVAL, "null plan");
+  CUDA_TRY(cudaSetDevice(P->device));
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const saber_sweep_desc& d = P->desc;
+  P->launches = 0;
+  P->summarized = false;
+  CUDA_TRY(cudaEventRecord(P->all.a, s));
+  CUDA_TRY(cudaMemsetAsync(P->rows.p, 0, P->rows.bytes, s));
+  CUDA_TRY(cudaMemsetAsync(P->cursor.p, 0, 16, s));
+  CUDA_TRY(cudaMemsetAsync(P->err.p, 0, 16, s));
+  LAUNCH_TRY(launch_fill_rows(P->comp.as<double>(), P->n_rows, P->n, d.shard_index, d.shard_count, s));
+  ++P->launches;
+
+  WorkloadParams wp{};
+  wp.items = P->wl.items.as<WorkloadItem>();
+  wp.n_items = P->n_items;
+  wp.seed_base = P->wl.seed_base.as<double>();
+  wp.seed_stride = P->n;
+  wp.mix_thresh = P->wl.th.as<double>();
+  wp.mix_task = P->wl.tt.as<int8_t>();
+  wp.mix_last = P->wl.tl.as<int8_t>();
+  wp.arrival = P->wl.arr.as<double>();
+  wp.deadline = P->wl.dl.as<double>();
+  wp.sla = P->wl.sla.as<double>();
+  wp.max_out = P->wl.mo.as<double>();
+  wp.input = P->wl.in.as<double>();
+  wp.demote_after = P->wl.dem.as<double>();
+  wp.horizon = P->wl.hor.as<double>();
+  wp.task = P->wl.task.as<int8_t>();
+  wp.nmax = P->n;
+  LAUNCH_TRY(launch_workloads(wp, s));
+  ++P->launches;
+
+  if (d.with_saber) {
+    RngGenParams rg{};
+    rg.seeds = P->seeds.as<uint64_t>();
+    rg.draws = P->draws.as<uint32_t>();
+    rg.off = P->s_off.as<int64_t>();
+    rg.len = P->s_len.as<int64_t>();
+    rg.n_streams = P->R;
+    LAUNCH_TRY(launch_rng_streams(rg, s));
+    ++P->launches;
+  }
+
+  SweepDescParams dp{};
+  dp.n_mixes = d.n_mixes;
+  dp.n_rps = d.n_rps;
+  dp.n_caps = d.n_caps;
+  dp.with_saber = d.with_saber;
+  dp.repeats = d.repeats;
+  dp.n = P->n;
+  dp.caps = P->caps_d.as<int32_t>();
+  dp.window = d.window_size;
+  dp.tick = d.tick;
+  dp.prefill_rate = d.prefill_rate;
+  dp.model_tab = P->model_tab;
+  dp.gt_tab = P->gt_tab;
+  dp.has_horizon = d.has_horizon;
+  dp.horizon = d.horizon;
+  dp.shard_index = d.shard_index;
+  dp.shard_count = d.shard_count;
+  dp.out = P->descs.as<TrajDesc>();
+  dp.n_rows = P->n_rows;
+  LAUNCH_TRY(launch_sweep_descs(dp, s, P->rows_shard));
+  ++P->launches;
+
+  SimParams sp{};
+  sp.traj = P->descs.as<TrajDesc>();
+  sp.n_traj = static_cast<int32_t>(P->rows_shard);
+  sp.wl = P->wl.view(P->n);
+  sp.tables = P->tables.as<double>();
+  sp.rng.draws = P->draws.as<uint32_t>();
+  sp.rng.off = P->s_off.as<int64_t>();
+  sp.rng.len = P->s_len.as<int64_t>();
+  sp.scratch = P->scratch.view;
+  sp.out.rows = P->rows.as<saber_traj_row>();
+  sp.out.completion = P->comp.as<double>();
+  sp.out.error = P->err.as<int32_t>();
+  sp.next_traj = P->cursor.as<int32_t>();
+  CUDA_TRY(cudaEventRecord(P->sim.a, s));
+  LAUNCH_TRY(launch_sim(sp, P->nwords, P->scratch.grid, 128, s));
+  CUDA_TRY(cudaEventRecord(P->sim.b, s));
+  ++P->launches;
+
+  RowMetricsParams rm{};
+  rm.rows = P->rows.as<saber_traj_row>();
+  rm.completion = P->comp.as<double>();
+  rm.wl = sp.wl;
+  rm.traj = sp.traj;
+  rm.n_traj = sp.n_traj;
+  LAUNCH_TRY(launch_row_metrics(rm, s));
+  ++P->launches;
+  CUDA_TRY(cudaEventRecord(P->all.b, s));
+  CUDA_TRY(cudaEventSynchronize(P->all.b));
+  float ms = 0.f, ms2 = 0.f;
+  CUDA_TRY(cudaEventElapsedTime(&ms, P->all.a, P->all.b));
+  CUDA_TRY(cudaEventElapsedTime(&ms2, P->sim.a, P->sim.b));
+  P->last_ms = ms;
+  P->sim_ms = ms2;
+  int32_t err = 0;
+  CUDA_TRY(cudaMemcpy(&err, P->err.p, 4, cudaMemcpyDeviceToHost));
+  if (err == kErrRngExhausted)
+    return fail(SABER_EINTERNAL, "scheduler RNG stream exhausted (draw bound violated)");
+  if (err != 0) return fail(SABER_EINTERNAL, "trajectory kernel error " + std::to_string(err));
+  return SABER_OK;
+}
+
+saber_status saber_cuda_sweep_plan_summarize(saber_sweep_plan* P, void* stream) {
+  if (!P) return fail(SABER_EINVAL, "null plan");
+  CUDA_TRY(cudaSetDevice(P->device));
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const saber_sweep_desc& d = P->desc;
+  SummaryParams sp{};
+  sp.rows = P->rows.as<saber_traj_row>();
+  sp.completion = P->comp.as<double>();
+  sp.wl = P->wl.view(P->n);
+  sp.n_mixes = d.n_mixes;
+  sp.n_rps = d.n_rps;
+  sp.n_caps = d.n_caps;
+  sp.with_saber = d.with_saber;
+  sp.repeats = d.repeats;
+  sp.n = P->n;
+  sp.caps = P->caps_d.as<int32_t>();
+  sp.summary = P->summary.as<saber_mix_summary>();
+  sp.best_cap = P->best_cap.as<int32_t>();
+  sp.scratch = P->cell_scratch.as<double>();
+  CUDA_TRY(cudaEventRecord(P->all.a, s));
+  LAUNCH_TRY(launch_summary(sp, s));
+  CUDA_TRY(cudaEventRecord(P->all.b, s));
+  CUDA_TRY(cudaEventSynchronize(P->all.b));
+  float ms = 0.f;
+  CUDA_TRY(cudaEventElapsedTime(&ms, P->all.a, P->all.b));
+  P->last_ms += ms;
+  P->launches += 2;
+  P->summarized = true;
+  return SABER_OK;
+}
+
+saber_status saber_cuda_sweep_plan_buffers(saber_sweep_plan* P, saber_sweep_buffers* out) {
+  if (!P || !out) return fail(SABER_EINVAL, "null argument");
+  out->rows = P->rows.p;
+  out->rows_bytes = static_cast<size_t>(P->n_rows) * sizeof(saber_traj_row);
+  out->completion_times = P->comp.p;
+  out->completion_bytes = static_cast<size_t>(P->n_rows) * P->n * 8;
+  out->n_rows = P->n_rows;
+  out->rows_this_shard = P->rows_shard;
+  return SABER_OK;
+}
+
+saber_status saber_cuda_sweep_plan_fetch(saber_sweep_plan* P, saber_sweep_out* out) {
+  if (!P || !out) return fail(SABER_EINVAL, "null argument");
+  CUDA_TRY(cudaSetDevice(P->device));
+  out->n_rows = P->n_rows;
+  if (out->rows)
+    CUDA_TRY(cudaMemcpy(out->rows, P->rows.p, static_cast<size_t>(P->n_rows) * sizeof(saber_traj_row),
+                        cudaMemcpyDeviceToHost));
+  if (out->completion_times)
+    CUDA_TRY(cudaMemcpy(out->completion_times, P->comp.p, static_cast<size_t>(P->n_rows) * P->n * 8,
+                        cudaMemcpyDeviceToHost));
+  if (out->summary || out->best_cap_by_rps) {
+    if (!P->summarized) return fail(SABER_EINVAL, "summary requested before summarize");
+    if (out->summary)
+      CUDA_TRY(cudaMemcpy(out->summary, P->summary.p,
+                          static_cast<size_t>(P->desc.n_mixes) * sizeof(saber_mix_summary),
+                          cudaMemcpyDeviceToHost));
+    if (out->best_cap_by_rps)
+      CUDA_TRY(cudaMemcpy(out->best_cap_by_rps, P->best_cap.p,
+                          static_cast<size_t>(P->desc.n_mixes) * P->desc.n_rps * 4,
+                          cudaMemcpyDeviceToHost));
+  }
+  out->device_ms = P->last_ms;
+  out->kernel_launches = P->launches;
+  return SABER_OK;
+}
+
+saber_status saber_cuda_sweep_plan_stats(saber_sweep_plan* P, double* device_ms, double* sim_ms,
+                                         int32_t* launches) {
+  if (!P) return fail(SABER_EINVAL, "null plan");
+  if (device_ms) *device_ms = P->last_ms;
+  if (sim_ms) *sim_ms = P->sim_ms;
+  if (launches) *launches = P->launches;
+  return SABER_OK;
+}
+
+void saber_cuda_sweep_plan_destroy(saber_sweep_plan* P) {
+  if (!P) return;
+  cudaSetDevice(P->device);
+  delete P;
+}
+
+saber_status saber_cuda_sweep(const saber_sweep_desc* desc, saber_sweep_out* out) {
+  if (!desc || !out) return fail(SABER_EINVAL, "null argument");
+  saber_sweep_plan* P = nullptr;
+  if (saber_status s = saber_cuda_sweep_plan_create(desc, &P)) return s;
+  std::unique_ptr<saber_sweep_plan, void (*)(saber_sweep_plan*)> guard(P, saber_cuda_sweep_plan_destroy);
+  if (saber_status s = saber_cuda_sweep_plan_run(P, nullptr)) return s;
+  const double run_ms = P->last_ms;
+  if (out->summary || out->best_cap_by_rps) {
+    if (desc->shard_count != 1)
+      return fail(SABER_EINVAL, "summary of a sharded sweep needs the rows of every shard "
+                                "(all-reduce the plan buffers, then summarize)");
+    if (saber_status s = saber_cuda_sweep_plan_summarize(P, nullptr)) return s;
+  }
+  if (saber_status s = saber_cuda_sweep_plan_fetch(P, out)) return s;
+  (void)run_ms;
+  return SABER_OK;
+}
+
+const char* saber_cuda_last_error(void) { return g_err.c_str(); }
+int32_t saber_cuda_abi_version(void) { return SABER_CUDA_ABI_VERSION; }
+
+int32_t saber_cuda_device_count(void) {
+  int count = 0;
+  if (cudaGetDeviceCount(&count) != cudaSuccess) return 0;
+  int usable = 0;
+  for (int i = 0; i < count; ++i) {
+    cudaDeviceProp p;
+    if (cudaGetDeviceProperties(&p, i) == cudaSuccess && p.major == 10) ++usable;
+  }
+  return usable;
+}
+
+saber_status saber_cuda_predict_table(const saber_model* model, int32_t max_load, double* table) {
+  if (!model || !table) return fail(SABER_EINVAL, "null argument");
+  if (saber_status s = validate_model(*model, "model")) return s;
+  if (max_load < 1) return fail(SABER_EDOMAIN, "predict: load must be >= 1");
+  for (int L = 1; L <= max_load; ++L) table[L - 1] = eval_model(*model, static_cast<double>(L));
+  return SABER_OK;
+}
+
+}  // extern "C"
+
+// ============================================================== run batch ==
+namespace {
+
+saber_status validate_spec(const saber_traj_spec& s) {
+  if (s.window_size < 1) return fail(SABER_EINVAL, "window_size must be >= 1");
+  if (s.window_size > kMaxWindow)
+    return fail(SABER_EINVAL, "window_size > " + std::to_string(kMaxWindow) +
+                                  " is not supported by the B200 engine");
+  if (!(s.tick > 0.0)) return fail(SABER_EINVAL, "tick must be > 0");
+  if (s.mode != SABER_MODE_SABER && s.mode != SABER_MODE_STATIC)
+    return fail(SABER_EINVAL, "unknown scheduler mode");
+  if (s.mode == SABER_MODE_STATIC && s.static_batch_size < 1)
+    return fail(SABER_EINVAL, "static mode requires a positive batch size");
+  if (s.mode == SABER_MODE_SABER && !s.has_model)
+    return fail(SABER_EINVAL, "saber mode requires a speed model");
+  if (s.has_horizon && !(s.horizon > 0.0)) return fail(SABER_EINVAL, "horizon must be > 0");
+  if (saber_status e = validate_model(s.ground_truth, "ground truth")) return e;
+  if (s.has_model)
+    if (saber_status e = validate_model(s.model, "model")) return e;
+  if (!(eval_model(s.ground_truth, 1.0) > 0.0))
+    return fail(SABER_EINVAL, "engine ground truth must be positive");
+  if (s.num_requests < 1)
+    return fail(SABER_EINVAL, s.requests ? "run: no requests" : "num_requests must be >= 1");
+  if (s.num_requests > kMaxRequests)
+    return fail(SABER_EINVAL, "num_requests > " + std::to_string(kMaxRequests) +
+                                  " is not supported by the B200 engine");
+  if (!s.requests) {
+    if (!(s.rps > 0.0)) return fail(SABER_EINVAL, "rps must be > 0");
+    if (s.length_jitter < 0.0 || s.length_jitter >= 1.0)
+      return fail(SABER_EINVAL, "length_jitter must be in [0, 1)");
+    if (saber_status e = validate_mix(s.mix)) return e;
+  }
+  return SABER_OK;
+}
+
+}  // namespace
+
+extern "C" saber_status saber_cuda_run_batch(const saber_run_batch_desc* desc,
+                                             saber_run_batch_out* out) {
+  if (!desc || !out) return fail(SABER_EINVAL, "null argument");
+  const int T = desc->n_traj;
+  if (T < 1) return fail(SABER_EINVAL, "run_batch: no trajectories");
+  if (!out->rows) return fail(SABER_EINVAL, "run_batch: rows output required");
+  int nmax = 1;
+  for (int k = 0; k < T; ++k) {
+    if (saber_status s = validate_spec(desc->specs[k])) return s;
+    nmax = std::max(nmax, desc->specs[k].num_requests);
+  }
+  if ((out->arrival_times || out->admit_times || out->completion_times || out->demoted) &&
+      out->max_n < nmax)
+    return fail(SABER_EINVAL, "run_batch: max_n smaller than the largest trajectory");
+  if (saber_status s = use_device(desc->device)) return s;
+  const int dev = desc->device;
+
+  // Workloads (one per trajectory), tables, streams, descriptors.
+  std::vector<WorkloadItem> items(static_cast<size_t>(T));
+  std::vector<double> base(static_cast<size_t>(T) * nmax * 4, 0.0);
+  std::vector<double> th(static_cast<size_t>(T) * 4);
+  std::vector<int8_t> tt(static_cast<size_t>(T) * 4), tlast(static_cast<size_t>(T));
+  const size_t cells = static_cast<size_t>(T) * nmax;
+  std::vector<double> arr(cells, 0.0), dl(cells, 0.0), sla(cells, 1.0), mo(cells, 1.0), in(cells, 1.0);
+  std::vector<int8_t> task(cells, -1);
+  const int tl = nmax + 2;
+  std::vector<double> tab(static_cast<size_t>(T) * 2 * tl);
+  std::vector<TrajDesc> descs(static_cast<size_t>(T));
+  std::vector<uint64_t> seeds;
+  std::vector<int64_t> off, len;
+  int64_t total_draws = 0;
+  for (int k = 0; k < T; ++k) {
+    const saber_traj_spec& s = desc->specs[k];
+    const int n = s.num_requests;
+    double* gt = &tab[static_cast<size_t>(k) * 2 * tl];
+    double* mt = gt + tl;
+    fill_table(s.ground_truth, nmax + 1, gt);
+    double ceiling = std::nan("");
+    if (s.mode == SABER_MODE_SABER) {
+      fill_table(s.model, nmax + 1, mt);
+      ceiling = mt[1];
+    }
+    WorkloadItem& it = items[static_cast<size_t>(k)];
+    it.n = n;
+    it.seed_idx = k;
+    it.mix = k;
+    it.rps = s.rps;
+    it.jitter = s.length_jitter;
+    it.ceiling = ceiling;
+    double last_bound = 0.0, max_sla = 12.0;
+    if (s.requests) {
+      it.kind = 1;
+      max_sla = 0.0;
+      for (int i = 0; i < n; ++i) {
+        const saber_request& q = s.requests[i];
+        const size_t o = static_cast<size_t>(k) * nmax + i;
+        arr[o] = q.arrival_time;
+        dl[o] = q.deadline;
+        sla[o] = q.sla_seconds;
+        mo[o] = static_cast<double>(q.max_output_tokens);
+        in[o] = static_cast<double>(q.input_tokens);
+        task[o] = static_cast<int8_t>(q.task >= 0 && q.task < 4 ? q.task : -1);
+        max_sla = std::max(max_sla, q.sla_seconds);
+      }
+      last_bound = s.requests[n - 1].arrival_time;
+    } else {
+      it.kind = 0;
+      double nls = 0.0;
+      seed_draws(s.workload_seed, n, &base[static_cast<size_t>(k) * nmax * 4], &nls);
+      mix_thresholds(s.mix, &th[static_cast<size_t>(k) * 4], &tt[static_cast<size_t>(k) * 4],
+                     &tlast[static_cast<size_t>(k)]);
+      last_bound = nls / s.rps * (1.0 + 1e-9) + n * 1e-6;
+    }
+    TrajDesc& d = descs[static_cast<size_t>(k)];
+    d.workload = k;
+    d.n = n;
+    d.mode = s.mode;
+    d.cap = s.static_batch_size;
+    d.window = s.window_size;
+    d.gt_tab = k * 2 * tl;
+    d.model_tab = s.mode == SABER_MODE_SABER ? k * 2 * tl + tl : -1;
+    d.tick = s.tick;
+    d.horizon = s.has_horizon ? s.horizon : std::nan("");
+    d.prefill_rate = s.prefill_rate;
+    d.row = k;
+    d.stream = -1;
+    if (s.mode == SABER_MODE_SABER) {
+      const double hb = s.has_horizon ? s.horizon : last_bound + 10.0 * max_sla + 1.0;
+      d.stream = static_cast<int32_t>(seeds.size());
+      seeds.push_back(s.seed ^ kSchedulerSeedSalt);
+      off.push_back(total_draws);
+      const int64_t l = draw_bound(hb, s.tick, s.window_size, n);
+      len.push_back(l);
+      total_draws += l;
+    }
+  }
+
+  Workloads wl;
+  DevBuf tables, seeds_d, off_d, len_d, draws_d, descs_d, rows_d, comp_d, admit_d, demo_d, cursor_d,
+      err_d, trace_d, tcount_d;
+  Scratch scratch;
+  if (saber_status s = wl.alloc(dev, T, nmax)) return s;
+  ALLOC_TRY(wl.items, dev, items.size() * sizeof(WorkloadItem));
+  ALLOC_TRY(wl.seed_base, dev, base.size() * 8);
+  ALLOC_TRY(wl.th, dev, th.size() * 8);
+  ALLOC_TRY(wl.tt, dev, tt.size());
+  ALLOC_TRY(wl.tl, dev, tlast.size());
+  ALLOC_TRY(tables, dev, tab.size() * 8);
+  ALLOC_TRY(descs_d, dev, descs.size() * sizeof(TrajDesc));
+  ALLOC_TRY(rows_d, dev, static_cast<size_t>(T) * sizeof(saber_traj_row));
+  ALLOC_TRY(comp_d, dev, cells * 8);
+  ALLOC_TRY(cursor_d, dev, 16);
+  ALLOC_TRY(err_d, dev, 16);
+  const bool records = out->admit_times || out->demoted;
+  if (records) {
+    ALLOC_TRY(admit_d, dev, cells * 8);
+    ALLOC_TRY(demo_d, dev, cells);
+  }
+  const bool trace = out->decisions != nullptr;
+  if (trace) {
+    if (out->decision_cap < 1 || !out->n_decisions)
+      return fail(SABER_EINVAL, "run_batch: decision trace needs decision_cap and n_decisions");
+    ALLOC_TRY(trace_d, dev, static_cast<size_t>(T) * out->decision_cap * sizeof(saber_decision));
+    ALLOC_TRY(tcount_d, dev, static_cast<size_t>(T) * 8);
+  }
+  if (!seeds.empty()) {
+    ALLOC_TRY(seeds_d, dev, seeds.size() * 8);
+    ALLOC_TRY(off_d, dev, off.size() * 8);
+    ALLOC_TRY(len_d, dev, len.size() * 8);
+    ALLOC_TRY(draws_d, dev, static_cast<size_t>(std::max<int64_t>(1, total_draws)) * 4);
+  }
+  const int nwords = nwords_for(nmax);
+  if (saber_status s = scratch.alloc(dev, nwords, nmax)) return s;
+
+  CUDA_TRY(cudaMemcpy(wl.items.p, items.data(), items.size() * sizeof(WorkloadItem), cudaMemcpyHostToDevice));
+  CUDA_TRY(cudaMemcpy(wl.seed_base.p, base.data(), base.size() * 8, cudaMemcpyHostToDevice));
+  CUDA_TRY(cudaMemcpy(wl.th.p, th.data(), th.size() * 8, cudaMemcpyHostToDevice));
+  CUDA_TRY(cudaMemcpy(wl.tt.p, tt.data(), tt.size(), cudaMemcpyHostToDevice));
+  CUDA_TRY(cudaMemcpy(wl.tl.p, tlast.data(), tlast.size(), cudaMemcpyHostToDevice));
+  CUDA_TRY(cudaMemcpy(wl.arr.p, arr.data(), cells * 8, cudaMemcpyHostToDevice));
+  CUDA_TRY(cudaMemcpy(wl.dl.p, dl.data(), cells * 8, cudaMemcpyHostToDevice));
+  CUDA_TRY(cudaMemcpy(wl.sla.p, sla.data(), cells * 8, cudaMemcpyHostToDevice));
+  CUDA_TRY(cudaMemcpy(wl.mo.p, mo.data(), cells * 8, cudaMemcpyHostToDevice));
+  CUDA_TRY(cudaMemcpy(wl.in.p, in.data(), cells * 8, cudaMemcpyHostToDevice));
+  CUDA_TRY(cudaMemcpy(wl.task.p, task.data(), cells, cudaMemcpyHostToDevice));
+  CUDA_TRY(cudaMemcpy(tables.p, tab.data(), tab.size() * 8, cudaMemcpyHostToDevice));
+  CUDA_TRY(cudaMemcpy(descs_d.p, descs.data(), descs.size() * sizeof(TrajDesc), cudaMemcpyHostToDevice));
+  if (!seeds.empty()) {
+    CUDA_TRY(cudaMemcpy(seeds_d.p, seeds.data(), seeds.size() * 8, cudaMemcpyHostToDevice));
+    CUDA_TRY(cudaMemcpy(off_d.p, off.data(), off.size() * 8, cudaMemcpyHostToDevice));
+    CUDA_TRY(cudaMemcpy(len_d.p, len.data(), len.size() * 8, cudaMemcpyHostToDevice));
+  }
+
+  Timer tm;
+  if (saber_status s = tm.init()) return s;
+  cudaStream_t st = nullptr;
+  int launches = 0;
+  CUDA_TRY(cudaEventRecord(tm.a, st));
+  CUDA_TRY(cudaMemsetAsync(rows_d.p, 0, rows_d.bytes, st));
+  CUDA_TRY(cudaMemsetAsync(cursor_d.p, 0, 16, st));
+  CUDA_TRY(cudaMemsetAsync(err_d.p, 0, 16, st));
+  LAUNCH_TRY(launch_fill_rows(comp_d.as<double>(), T, nmax, 0, 1, st));
+  ++launches;
+  if (records) {
+    LAUNCH_TRY(launch_fill_rows(admit_d.as<double>(), T, nmax, 0, 1, st));
+    ++launches;
+    CUDA_TRY(cudaMemsetAsync(demo_d.p, 0, cells, st));
+  }
+  WorkloadParams wp{};
+  wp.items = wl.items.as<WorkloadItem>();
+  wp.n_items = T;
+  wp.seed_base = wl.seed_base.as<double>();
+  wp.seed_stride = nmax;
+  wp.mix_thresh = wl.th.as<double>();
+  wp.mix_task = wl.tt.as<int8_t>();
+  wp.mix_last = wl.tl.as<int8_t>();
+  wp.arrival = wl.arr.as<double>();
+  wp.deadline = wl.dl.as<double>();
+  wp.sla = wl.sla.as<double>();
+  wp.max_out = wl.mo.as<double>();
+  wp.input = wl.in.as<double>();
+  wp.demote_after = wl.dem.as<double>();
+  wp.horizon = wl.hor.as<double>();
+  wp.task = wl.task.as<int8_t>();
+  wp.nmax = nmax;
+  LAUNCH_TRY(launch_workloads(wp, st));
+  ++launches;
+  if (!seeds.empty()) {
+    RngGenParams rg{};
+    rg.seeds = seeds_d.as<uint64_t>();
+    rg.draws = draws_d.as<uint32_t>();
+    rg.off = off_d.as<int64_t>();
+    rg.len = len_d.as<int64_t>();
+    rg.n_streams = static_cast<int32_t>(seeds.size());
+    LAUNCH_TRY(launch_rng_streams(rg, st));
+    ++launches;
+  }
+  SimParams sp{};
+  sp.traj = descs_d.as<TrajDesc>();
+  sp.n_traj = T;
+  sp.wl = wl.view(nmax);
+  sp.tables = tables.as<double>();
+  sp.rng.draws = draws_d.as<uint32_t>();
+  sp.rng.off = off_d.as<int64_t>();
+  sp.rng.len = len_d.as<int64_t>();
+  sp.scratch = scratch.view;
+  sp.out.rows = rows_d.as<saber_traj_row>();
+  sp.out.completion = comp_d.as<double>();
+  sp.out.admit = records ? admit_d.as<double>() : nullptr;
+  sp.out.demoted = records ? demo_d.as<uint8_t>() : nullptr;
+  sp.out.trace = trace ? trace_d.as<saber_decision>() : nullptr;
+  sp.out.trace_count = trace ? tcount_d.as<int64_t>() : nullptr;
+  sp.out.trace_cap = trace ? out->decision_cap : 0;
+  sp.out.error = err_d.as<int32_t>();
+  sp.next_traj = cursor_d.as<int32_t>();
+  LAUNCH_TRY(launch_sim(sp, nwords, scratch.grid, 128, st));
+  ++launches;
+  RowMetricsParams rm{};
+  rm.rows = rows_d.as<saber_traj_row>();
+  rm.completion = comp_d.as<double>();
+  rm.wl = sp.wl;
+  rm.traj = sp.traj;
+  rm.n_traj = T;
+  LAUNCH_TRY(launch_row_metrics(rm, st));
+  ++launches;
+  CUDA_TRY(cudaEventRecord(tm.b, st));
+  CUDA_TRY(cudaEventSynchronize(tm.b));
+  float ms = 0.f;
+  CUDA_TRY(cudaEventElapsedTime(&ms, tm.a, tm.b));
+  int32_t err = 0;
+  CUDA_TRY(cudaMemcpy(&err, err_d.p, 4, cudaMemcpyDeviceToHost));
+
+  CUDA_TRY(cudaMemcpy(out->rows, rows_d.p, static_cast<size_t>(T) * sizeof(saber_traj_row),
+                      cudaMemcpyDeviceToHost));
+  auto copy_rows = [&](void* dst, const DevBuf& src, size_t elem) -> saber_status {
+    if (!dst) return SABER_OK;
+    std::vector<uint8_t> h(cells * elem);
+    CUDA_TRY(cudaMemcpy(h.data(), src.p, cells * elem, cudaMemcpyDeviceToHost));
+    for (int k = 0; k < T; ++k)
+      std::memcpy(static_cast<uint8_t*>(dst) + static_cast<size_t>(k) * out->max_n * elem,
+                  h.data() + static_cast<size_t>(k) * nmax * elem, static_cast<size_t>(nmax) * elem);
+    return SABER_OK;
+  };
+  if (saber_status s = copy_rows(out->completion_times, comp_d, 8)) return s;
+  if (saber_status s = copy_rows(out->arrival_times, wl.arr, 8)) return s;
+  if (records) {
+    if (saber_status s = copy_rows(out->admit_times, admit_d, 8)) return s;
+    if (saber_status s = copy_rows(out->demoted, demo_d, 1)) return s;
+  }
+  if (trace) {
+    CUDA_TRY(cudaMemcpy(out->n_decisions, tcount_d.p, static_cast<size_t>(T) * 8, cudaMemcpyDeviceToHost));
+    CUDA_TRY(cudaMemcpy(out->decisions, trace_d.p,
+                        static_cast<size_t>(T) * out->decision_cap * sizeof(saber_decision),
+                        cudaMemcpyDeviceToHost));
+  }
+  out->device_ms = ms;
+  out->kernel_launches = launches;
+  if (err == kErrTraceOverflow) return fail(SABER_ECAPACITY, "decision trace capacity exceeded");
+  if (err == kErrRngExhausted)
+    return fail(SABER_EINTERNAL, "scheduler RNG stream exhausted (draw bound violated)");
+  if (err != 0) return fail(SABER_EINTERNAL, "trajectory kernel error " + std::to_string(err));
+  return SABER_OK;
+}
+
+extern "C" saber_status saber_cuda_fp64_peak(int32_t device, double* tflops) {
+  if (!tflops) return fail(SABER_EINVAL, "null argument");
+  if (saber_status s = use_device(device)) return s;
+  if (fp64_peak(device, tflops) != 0) return fail(SABER_ECUDA, "fp64 microbenchmark failed");
+  return SABER_OK;
+}
+
+extern "C" saber_status saber_cuda_fit_batch(const saber_fit_desc* desc, saber_fit_out* out) {
+  (void)desc;
+  (void)out;
+  return fail(SABER_EINTERNAL, "fit_batch: not built yet");
+}

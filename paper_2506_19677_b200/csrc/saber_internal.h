@@ -1,0 +1,209 @@
+// saber_internal.h — device data layout shared by the host orchestration
+// (host.cpp) and the sm_100a kernels (*.cu).  See DESIGN.md §2 for the HBM map.
+#pragma once
+
+#include <cstddef>
+#include <cstdint>
+
+#include "../../include/saber_cuda.h"
+
+namespace saberb200 {
+
+// Largest request count the register-bitmask trajectory kernel supports
+// (8 x 64-bit words of per-request tier masks).  Larger n is rejected with
+// SABER_EINVAL.
+constexpr int kMaxRequests = 512;
+// Largest admission window the register Fisher-Yates supports (4-bit nibbles
+// in one u64).  The reference default is 8 (types.hpp:80).
+constexpr int kMaxWindow = 16;
+// Lanes per warp; per-lane scratch is interleaved with this stride.
+constexpr int kWarp = 32;
+
+// One workload = one request list (generate() output or a replayed trace),
+// stored SoA with row stride `nmax`.
+struct WorkloadTables {
+  const double* arrival;   // [W][nmax]
+  const double* deadline;  // [W][nmax]
+  const double* sla;       // [W][nmax]
+  const double* max_out;   // [W][nmax]  (double: compared against fluid progress)
+  const double* input;     // [W][nmax]
+  const int8_t* task;      // [W][nmax]  catalog index or -1
+  const double* demote_after;  // [W][nmax] safe lower bound on demotion time
+  const double* horizon;   // [W]  last arrival + 10 * max sla (simloop.cpp:60-63)
+  int32_t nmax;
+};
+
+// One trajectory to simulate (a SimConfig bound to a workload).
+struct TrajDesc {
+  int32_t workload;
+  int32_t n;
+  int32_t mode;       // SABER_MODE_*
+  int32_t cap;        // static_batch_size
+  int32_t window;
+  int32_t model_tab;  // offset (doubles) of the scheduler model's predict table, -1 none
+  int32_t gt_tab;     // offset of the ground-truth table
+  int32_t stream;     // scheduler RNG stream index, -1 none
+  double tick;
+  double horizon;     // NaN => use the workload's default horizon
+  double prefill_rate;
+  int64_t row;        // output row
+};
+
+// Scheduler RNG streams: stream s holds draws [off[s], off[s] + len[s]).
+// Each draw is mt19937_64() % 720720 (= lcm(1..16)), exact for every
+// `% (i+1)` with i+1 <= 16 the Fisher-Yates needs.
+struct RngStreams {
+  const uint32_t* draws;
+  const int64_t* off;
+  const int64_t* len;
+};
+
+constexpr uint32_t kDrawModulus = 720720u;  // lcm(1..16)
+
+// Per-lane scratch (global memory, lane-interleaved).
+struct LaneScratch {
+  double* slot_g;      // [lanes/32][S][32] generated (>=0) or -prefill_left (<0)
+  double* slot_m;      // [lanes/32][S][32] max_output_tokens
+  uint16_t* slot_id;   // [lanes/32][S][32]
+  double* ledger_need; // [lanes/32][nmax][32]
+  uint16_t* low_fifo;  // [lanes/32][nmax][32]
+  int32_t slots;       // S (= nmax)
+};
+
+// Outputs of the trajectory kernel.
+struct SimOutputs {
+  saber_traj_row* rows;       // [rows]
+  double* completion;         // [rows][nmax]   pre-filled NaN by the caller
+  double* admit;              // [rows][nmax] or null
+  uint8_t* demoted;           // [rows][nmax] or null
+  saber_decision* trace;      // [trace_rows][trace_cap] or null
+  int64_t* trace_count;       // [rows] or null
+  int64_t trace_cap;
+  int32_t* error;             // [1] first error code (0 = none)
+};
+
+struct SimParams {
+  const TrajDesc* traj;
+  int32_t n_traj;
+  WorkloadTables wl;
+  const double* tables;       // predict tables, table[L] at model_tab + L
+  RngStreams rng;
+  LaneScratch scratch;
+  SimOutputs out;
+  int32_t* next_traj;         // work-queue cursor (device)
+};
+
+// Error codes written to SimOutputs::error.
+enum : int32_t {
+  kErrNone = 0,
+  kErrRngExhausted = 1,   // scheduler stream too short (host bound violated)
+  kErrTraceOverflow = 2,  // decision trace capacity exceeded
+  kErrBadDesc = 3,
+};
+
+// Kernel launchers (defined in the .cu files).
+int launch_sim(const SimParams& p, int nwords, int grid, int block, void* stream);
+int sim_occupancy_grid(int nwords, int block, int* grid);
+
+struct RngGenParams {
+  const uint64_t* seeds;  // [n_streams] already xor-salted
+  uint32_t* draws;
+  const int64_t* off;
+  const int64_t* len;
+  int32_t n_streams;
+};
+int launch_rng_streams(const RngGenParams& p, void* stream);
+
+// Workload expansion.  Item kind 0 = generate() from per-seed draws
+// (seed_base row seed_idx, mix thresholds `mix`, rate rps); kind 1 = replayed
+// requests already written into the tables.  Both get demotion bounds for
+// `ceiling` (the SABER model's max_speed; NaN/<=0 disables the bound) and the
+// default horizon.
+struct WorkloadItem {
+  int32_t kind;
+  int32_t n;
+  int32_t seed_idx;
+  int32_t mix;
+  double rps;
+  double jitter;
+  double ceiling;
+};
+struct WorkloadParams {
+  const WorkloadItem* items;
+  int32_t n_items;
+  const double* seed_base;   // [seeds][seed_stride][4]: -log(1-u_gap) (glibc), u_task, u_in, u_out
+  int32_t seed_stride;
+  const double* mix_thresh;  // [mixes][4] cumulative thresholds, alphabetical order
+  const int8_t* mix_task;    // [mixes][4] task at each threshold slot (-1 unused)
+  const int8_t* mix_last;    // [mixes] fallback task (last map entry)
+  double *arrival, *deadline, *sla, *max_out, *input, *demote_after, *horizon;
+  int8_t* task;
+  int32_t nmax;
+};
+int launch_workloads(const WorkloadParams& p, void* stream);
+
+// Sweep trajectory descriptors (grid order) for this shard.
+struct SweepDescParams {
+  int32_t n_mixes, n_rps, n_caps, with_saber, repeats, n;
+  const int32_t* caps;
+  int32_t window;
+  double tick, prefill_rate;
+  int32_t model_tab, gt_tab;
+  int32_t has_horizon;
+  double horizon;
+  int32_t shard_index, shard_count;
+  TrajDesc* out;          // [rows_this_shard]
+  int64_t n_rows;
+};
+int launch_sweep_descs(const SweepDescParams& p, void* stream, int64_t rows_this_shard);
+
+// Fill completion rows: NaN for rows in this shard, 0 for others.
+int launch_fill_rows(double* comp, int64_t n_rows, int32_t nmax, int32_t shard_index,
+                     int32_t shard_count, void* stream);
+
+// Per-row metrics epilogue (metrics.cpp:17-140) over rows of this shard.
+struct RowMetricsParams {
+  saber_traj_row* rows;
+  const double* completion;
+  WorkloadTables wl;
+  const TrajDesc* traj;
+  int32_t n_traj;
+};
+int launch_row_metrics(const RowMetricsParams& p, void* stream);
+
+// Sweep summary (simloop.cpp:206-275).
+struct SummaryParams {
+  const saber_traj_row* rows;
+  const double* completion;
+  WorkloadTables wl;
+  int32_t n_mixes, n_rps, n_caps, with_saber, repeats, n;
+  const int32_t* caps;
+  saber_mix_summary* summary;   // [n_mixes]
+  int32_t* best_cap;            // [n_mixes][n_rps]
+  double* scratch;              // [n_mixes][n_rps][4] cell-level means/counts
+};
+int launch_summary(const SummaryParams& p, void* stream);
+
+// Fitting.
+struct FitParams {
+  const int32_t* loads;
+  const double* speeds;
+  const int64_t* offsets;
+  int32_t n_curves;
+  int32_t family_mask;
+  int32_t calibrate;
+  double* params;      // [3*n_curves][3]
+  double* r2;          // [3*n_curves]
+  int32_t* status;     // [3*n_curves]
+  int32_t* best_family;// [n_curves]
+  int32_t* iterations; // [3*n_curves]
+  double* lm_scratch;  // [3*n_curves*5][4]: per-start (p0,p1,p2,sse)
+  int32_t* lm_conv;    // [3*n_curves*5]
+  int32_t* lm_iters;   // [3*n_curves*5]
+  int32_t* cursor;     // work queue
+};
+int launch_fit(const FitParams& p, void* stream, int* launches);
+
+int fp64_peak(int device, double* tflops);
+
+}  // namespace saberb200
