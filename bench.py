@@ -1,0 +1,410 @@
+#!/usr/bin/env python3
+"""bench.py — BASELINE config 2 on the B200 engine (and the reference arm).
+
+Workload (BASELINE.json configs[1]): W1-W3 x RPS 1..20 x (static caps
+10..100:10 + SABER-USL) x 64 seeds, n = 100 requests per trajectory, default
+engine (usl(100, 0.05, 0.001), prefill 2000 tok/s), window 8, tick 0.01 s.
+One step = one full sweep = 42,240 trajectories (per GPU; weak scaling: at N
+GPUs the job is the same sweep over 64*N seeds, rows strided across ranks,
+then the NCCL all-reduce that gathers every row for the summary).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl engine|reference]
+
+Prints ONE JSON line (rank 0).  `value` = trajectories/s with inputs resident
+in HBM (CUDA events, L2 flushed between steps, max over ranks); `e2e` = the
+same metric through the one-shot C-ABI call with host buffers.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+# calibrate(profile(EngineConfig{}, {w3, n=1000, seed 42}, 50)).best
+CAL_USL = (99.999999999997357, 0.049999999999992085, 0.0010000000000001078)
+RPS = [float(r) for r in range(1, 21)]
+CAPS = list(range(10, 101, 10))
+MIXES = ["w1", "w2", "w3"]
+N_REQ = 100
+SEEDS_PER_GPU = 64
+BASE_SEED = 42
+WORKLOAD = ("config2: W1-W3 x RPS 1-20 x (static caps 10..100:10 + SABER-USL) x 64 seeds/GPU, "
+            "n=100 requests, default engine usl(100,0.05,0.001), prefill 2000, window 8, tick 0.01")
+METRIC = "simulated admission decisions/sec and sweep trajectories/sec vs CPU ref, same goodput"
+
+
+def env_int(k, d):
+    try:
+        return int(os.environ.get(k, d))
+    except ValueError:
+        return d
+
+
+# ------------------------------------------------------------------ clocks --
+class ClockSampler:
+    QUERY = ("index,clocks.sm,clocks.max.sm,power.draw,utilization.gpu,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device = device
+        self.proc = None
+        self.path = None
+
+    def start(self):
+        fd, self.path = tempfile.mkstemp(prefix="clocks_", suffix=".csv")
+        os.close(fd)
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.QUERY}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except OSError:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        sm, mx, util, reasons = [], [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in open(self.path):
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                s, m, u = float(f[1]), float(f[2]), float(f[4])
+            except ValueError:
+                continue
+            sm.append(s)
+            mx.append(m)
+            util.append(u)
+            for name, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(name)
+        os.unlink(self.path)
+        loaded = [s for s, u in zip(sm, util) if u > 0] or sm
+        return {"sm_mhz": statistics.median(loaded) if loaded else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# -------------------------------------------------------------- reference --
+def reference_sample(seeds, jobs=0):
+    """Time oracle/_ref (the unmodified reference compiled from its sources)
+    running saber::sweep on `seeds` seeds of the same grid, all host cores."""
+    import oracle as O  # noqa: E402  (CPU-baseline / reference arm only)
+    ref = O.Oracle("reference")
+    base = O.make_config(mix="w3", n=N_REQ, seed=BASE_SEED,
+                         model=(O.USL, CAL_USL), gt=O.DEFAULT_GT)
+    base.has_model = 1
+    t0 = time.perf_counter()
+    r = ref.sweep(base, MIXES, RPS, CAPS, True, seeds, jobs=jobs)
+    dt = time.perf_counter() - t0
+    return r, dt
+
+
+def reference_arm(args):
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    rank = env_int("RANK", 0)
+    if rank != 0:
+        return 0
+    cores = os.cpu_count() or 1
+    rows_per_seed = len(MIXES) * len(RPS) * (len(CAPS) + 1)
+    # size the per-step sample: ~3 s of all-core CPU work per step
+    _, t1 = reference_sample(1)
+    seeds = int(max(1, min(SEEDS_PER_GPU, round(3.0 / max(t1, 1e-3)))))
+    for _ in range(args.warmup):
+        reference_sample(seeds)
+    times = []
+    for _ in range(args.steps):
+        _, dt = reference_sample(seeds)
+        times.append(dt)
+    rows = rows_per_seed * seeds
+    value = rows * args.steps / sum(times)
+    sample = (f"{seeds} seed(s) x {rows_per_seed} cells = {rows} trajectories per step "
+              f"(saber::sweep jobs=0 -> {cores} threads)")
+    line = {"metric": METRIC, "value": value, "unit": "traj/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * sum(times) / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (reference generate(): mt19937_64 Poisson arrivals)",
+            "config": {"workload": WORKLOAD, "trajectories_per_step": rows, "l2": "n/a (CPU)"},
+            "impl": "reference",
+            "cpu_baseline": {"value": value, "unit": "traj/s", "cores": cores, "kind": "reference",
+                             "sample": sample},
+            "e2e": {"value": value, "unit": "traj/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ------------------------------------------------------------------ engine --
+def algorithmic_fp64_ops(rows):
+    """SURVEY §8(d) W_traj summed over rows: per pass 3 + 11 per decode slot +
+    4 per prefill slot; per tick 1 + 6 per high-tier entry + 6 per gate
+    candidate + 1 per ledger entry scanned."""
+    r = rows
+    return float(np.sum(3 * r["passes"] + 11 * r["decode_updates"] + 4 * r["prefill_updates"] +
+                        r["ticks"] + 6 * r["refresh_entries"] + 6 * r["gate_candidates"] +
+                        r["ledger_scanned"]))
+
+
+def load_profile_traffic():
+    p = os.path.join(ROOT, "profiles", "sim_kernel_traffic.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return d.get("dram_bytes_per_launch"), d
+    except (OSError, ValueError):
+        return None, None
+
+
+def engine_arm(args):
+    import torch
+    import paper_2506_19677_b200 as S
+
+    world = env_int("WORLD_SIZE", 1)
+    rank = env_int("RANK", 0)
+    local = env_int("LOCAL_RANK", 0)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist  # noqa: F811
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(local)
+    device = torch.cuda.current_device()
+    stream = torch.cuda.current_stream()
+
+    grid = S.SweepGrid(MIXES, RPS, CAPS, True)
+    base = S.SimConfig()
+    base.workload.num_requests = N_REQ
+    base.model = S.SpeedModel(S.ModelFamily.Usl, CAL_USL)
+    base.repeats = SEEDS_PER_GPU * world
+    base.seed = BASE_SEED
+    plan = S.SweepPlan(grid, base, device=device, shard_index=rank, shard_count=world)
+    bufs = plan.buffers()
+    rows_t = comp_t = None
+    if world > 1:
+        # zero-copy int64 views of the plan's row/completion buffers for NCCL
+        rows_t = torch.as_tensor(_CudaView(bufs.rows, bufs.rows_bytes), device=f"cuda:{device}")
+        comp_t = torch.as_tensor(_CudaView(bufs.completion_times, bufs.completion_bytes),
+                                 device=f"cuda:{device}")
+
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.int32, device=device)
+
+    def step():
+        plan.run(stream.cuda_stream)
+        if world > 1:
+            # NCCL final statistics reduce: shards are disjoint (other ranks'
+            # rows are 0), so an integer sum of the raw bits is an exact gather
+            dist.all_reduce(rows_t)
+            dist.all_reduce(comp_t)
+        plan.summarize(stream.cuda_stream)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+
+    clocks = ClockSampler(device)
+    clocks.start()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(args.steps)]
+    sim_ms = []
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    for k in range(args.steps):
+        flush.fill_(k)  # evict L2 (256 MB > 126 MB) between timed steps
+        ev[k][0].record(stream)
+        step()
+        ev[k][1].record(stream)
+        sim_ms.append(plan.stats()[1])
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    clk = clocks.stop()
+    total_ms = sum(a.elapsed_time(b) for a, b in ev)
+    if dist:
+        t = torch.tensor([total_ms], dtype=torch.float64, device=device)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    launches_per_step = plan.stats()[2]
+
+    rows, _, summ, best = plan.fetch(completion=False, summary=True)
+    total_rows = plan.n_rows
+    value = total_rows * args.steps / (total_ms / 1e3)
+    decisions = float(rows["decisions"].sum())
+    mine = rows[rows["n"] > 0] if world > 1 else rows
+    fp64_ops = algorithmic_fp64_ops(rows[np.arange(len(rows)) % world == rank])
+    sim_avg_ms = float(np.mean(sim_ms))
+
+    # e2e: the one-shot C-ABI call with host buffers (host prologue, H2D, all
+    # kernels, D2H of rows + summary) per step.
+    e2e_times = []
+    h2d = d2h = 0
+    if world == 1:
+        for k in range(args.warmup + args.steps):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            out = _one_shot(S, grid, base, device)
+            torch.cuda.synchronize()
+            if k >= args.warmup:
+                e2e_times.append(time.perf_counter() - t0)
+            h2d, d2h = out
+        e2e_value = total_rows * len(e2e_times) / sum(e2e_times)
+    else:
+        e2e_value = None
+
+    peak = S.fp64_peak_tflops(device)
+    achieved = fp64_ops / (sim_avg_ms / 1e3) / 1e12
+    traffic, prof = load_profile_traffic()
+
+    line = None
+    if rank == 0:
+        cpu = None
+        if world == 1 and not args.no_cpu_baseline:
+            cpu = cpu_baseline(rows, grid, base)
+        line = {
+            "metric": METRIC, "value": value, "unit": "traj/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (generate(): mt19937_64 Poisson arrivals, task/length draws; "
+                    f"seeds {BASE_SEED}..{BASE_SEED + base.repeats - 1})",
+            "config": {"workload": WORKLOAD, "trajectories_per_step": total_rows,
+                       "seeds": base.repeats, "l2": "flushed between steps (256 MB write)",
+                       "parallelism": f"rows strided over {world} GPU(s)"},
+            "decisions_per_s": decisions * args.steps / (total_ms / 1e3),
+            "decisions_per_step": decisions,
+            "e2e": {"value": e2e_value, "unit": "traj/s", "h2d_bytes_per_step": h2d,
+                    "d2h_bytes_per_step": d2h},
+            "gpu_launches": launches_per_step * args.steps,
+            "roofline": {"bound": "fp64", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                         "frac": achieved / peak if peak else None, "traffic": traffic,
+                         "kernel": "sim_kernel (K1)", "kernel_ms": sim_avg_ms,
+                         "share_of_step": sim_avg_ms / (total_ms / args.steps),
+                         "algorithmic_fp64_ops_per_launch": fp64_ops,
+                         "peak_source": "measured live: DFMA microbenchmark (saber_cuda_fp64_peak)",
+                         "note": "K1 is issue/latency-bound (DESIGN.md §4); FP64 pipe is the "
+                                 "algorithmic roofline SURVEY §8(d) names"},
+            "clocks": clk,
+            "summary": {m: {"delta": summ[i].delta, "saber_mean_goodput": summ[i].saber_mean_goodput,
+                            "best_static_mean_goodput": summ[i].best_static_mean_goodput}
+                        for i, m in enumerate(MIXES)},
+        }
+        if cpu is not None:
+            line["cpu_baseline"] = cpu
+    plan.close()
+    if line is not None:
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
+    return 0
+
+
+def _one_shot(S, grid, base, device):
+    """One saber_cuda_sweep call: host buffers in and out."""
+    import ctypes as C
+    N = S._native
+    p = S.SweepPlan.__new__(S.SweepPlan)
+    # build the descriptor exactly as SweepPlan does, without creating a plan
+    mix_ids = (C.c_int32 * len(grid.mixes))(*[int(m[1:]) for m in grid.mixes])
+    rps = (C.c_double * len(grid.rps_list))(*grid.rps_list)
+    caps = (C.c_int32 * len(grid.caps))(*grid.caps)
+    d = N.saber_sweep_desc()
+    d.mixes, d.n_mixes = mix_ids, len(grid.mixes)
+    d.rps, d.n_rps = rps, len(grid.rps_list)
+    d.caps, d.n_caps = caps, len(grid.caps)
+    d.with_saber = 1
+    d.num_requests = base.workload.num_requests
+    d.length_jitter = base.workload.length_jitter
+    d.window_size = base.scheduler.window_size
+    d.tick = base.scheduler.tick
+    d.has_model = 1
+    d.model = S.api._model(base.model)
+    d.ground_truth = S.api._model(base.engine.ground_truth)
+    d.prefill_rate = base.engine.prefill_rate
+    d.repeats = base.repeats
+    d.seed = base.seed
+    d.device = device
+    d.shard_index, d.shard_count = 0, 1
+    n_rows = int(N.lib().saber_cuda_sweep_rows(C.byref(d)))
+    rows = np.empty(n_rows, dtype=S.ROW_DTYPE)
+    summ = (N.saber_mix_summary * len(grid.mixes))()
+    best = np.empty((len(grid.mixes), len(grid.rps_list)), dtype=np.int32)
+    o = N.saber_sweep_out()
+    o.rows = rows.ctypes.data_as(C.POINTER(N.saber_traj_row))
+    o.summary = summ
+    o.best_cap_by_rps = best.ctypes.data_as(C.POINTER(C.c_int32))
+    S.api._check(N.lib().saber_cuda_sweep(C.byref(d), C.byref(o)))
+    del p
+    return int(o.h2d_bytes), int(o.d2h_bytes)
+
+
+class _CudaView:
+    """__cuda_array_interface__ over a raw device allocation (int64 words)."""
+
+    def __init__(self, ptr, nbytes):
+        self.__cuda_array_interface__ = {"shape": (nbytes // 8,), "typestr": "<i8",
+                                         "data": (int(ptr), False), "version": 3, "strides": None}
+
+
+def cpu_baseline(gpu_rows, grid, base):
+    """The reference on the host cores, on a bounded sample of the same
+    workload; also checks the sample's goodputs equal the GPU's rows."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    try:
+        import oracle as O  # noqa: F401
+        if not O.reference_available():
+            return None
+    except ImportError:
+        return None
+    cores = os.cpu_count() or 1
+    _, t1 = reference_sample(1)
+    seeds = int(max(1, min(SEEDS_PER_GPU, round(15.0 / max(t1, 1e-3)))))
+    r, dt = reference_sample(seeds)
+    rows_per_seed = len(MIXES) * len(RPS) * (len(CAPS) + 1)
+    n = rows_per_seed * seeds
+    # GPU rows for the same (mix, rps, variant, seed) keys
+    R = base.repeats
+    per_cell = len(CAPS) + 1
+    idx = []
+    for c in range(len(MIXES) * len(RPS) * per_cell):
+        for s in range(seeds):
+            idx.append(c * R + s)
+    same = bool(np.array_equal(gpu_rows["goodput"][np.array(idx)], r["goodput"]))
+    return {"value": n / dt, "unit": "traj/s", "cores": cores, "kind": "reference",
+            "sample": f"saber::sweep over seeds {BASE_SEED}..{BASE_SEED + seeds - 1} of the same grid "
+                      f"({n} trajectories, {dt:.1f} s, jobs=0)",
+            "same_goodput_rows": n, "same_goodput": same}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="engine", choices=["engine", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return reference_arm(args)
+    return engine_arm(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

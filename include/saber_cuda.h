@@ -161,6 +161,8 @@ typedef struct {
   int64_t n_rows;
   double device_ms;                /* CUDA-event time of the device work */
   int32_t kernel_launches;
+  int64_t h2d_bytes;               /* host->device bytes of the inputs (plan create) */
+  int64_t d2h_bytes;               /* device->host bytes of the results (fetch) */
 } saber_sweep_out;
 
 /* Number of rows a sweep produces (= SweepResult::rows.size()). */

@@ -72,6 +72,7 @@ class saber_sweep_out(C.Structure):
         ("rows", C.POINTER(saber_traj_row)), ("completion_times", C.POINTER(C.c_double)),
         ("summary", C.POINTER(saber_mix_summary)), ("best_cap_by_rps", C.POINTER(C.c_int32)),
         ("n_rows", C.c_int64), ("device_ms", C.c_double), ("kernel_launches", C.c_int32),
+        ("h2d_bytes", C.c_int64), ("d2h_bytes", C.c_int64),
     ]
 
 

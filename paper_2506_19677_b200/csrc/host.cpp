@@ -15,6 +15,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -259,29 +260,34 @@ int nwords_for(int n) {
   return 8;
 }
 
-// ----------------------------------------------------------- lane scratch --
+// ---------------------------------------------------------- group scratch --
+// Lanes per trajectory.  SABER_GROUP overrides for tuning.
+int group_size() {
+  const char* e = std::getenv("SABER_GROUP");
+  if (e) {
+    const int g = std::atoi(e);
+    if (g == 1 || g == 2 || g == 4 || g == 8) return g;
+  }
+  return 4;
+}
+
 struct Scratch {
-  DevBuf g, m, id, ledger, low;
-  int grid = 0;
-  LaneScratch view{};
-  saber_status alloc(int device, int nwords, int nmax) {
-    int grid_ = 0;
-    if (sim_occupancy_grid(nwords, 128, &grid_) != 0)
-      return fail(SABER_ECUDA, "occupancy query failed");
-    grid = grid_;
-    const size_t lanes = static_cast<size_t>(grid) * 128;
+  DevBuf ledger, low;
+  SimLaunch launch{};
+  GroupScratch view{};
+  saber_status alloc(int device, int nmax) {
+    const int rc = plan_sim(nmax, group_size(), &launch);
+    if (rc != 0)
+      return fail(SABER_ECUDA, "trajectory kernel configuration failed (" + std::to_string(rc) +
+                                   "): " + cudaGetErrorString(cudaGetLastError()));
+    const int64_t groups =
+        static_cast<int64_t>(launch.grid) * (kSimBlock / kWarp) * (kWarp / launch.group);
     const size_t per = static_cast<size_t>(nmax);
-    ALLOC_TRY(g, device, lanes * per * sizeof(double));
-    ALLOC_TRY(m, device, lanes * per * sizeof(double));
-    ALLOC_TRY(id, device, lanes * per * sizeof(uint16_t));
-    ALLOC_TRY(ledger, device, lanes * per * sizeof(double));
-    ALLOC_TRY(low, device, lanes * per * sizeof(uint16_t));
-    view.slot_g = g.as<double>();
-    view.slot_m = m.as<double>();
-    view.slot_id = id.as<uint16_t>();
+    ALLOC_TRY(ledger, device, static_cast<size_t>(groups) * per * sizeof(double));
+    ALLOC_TRY(low, device, static_cast<size_t>(groups) * per * sizeof(uint16_t));
     view.ledger_need = ledger.as<double>();
     view.low_fifo = low.as<uint16_t>();
-    view.slots = nmax;
+    view.groups = groups;
     return SABER_OK;
   }
 };
@@ -352,12 +358,13 @@ struct saber_sweep_plan {
 
   Workloads wl;
   DevBuf tables, seeds, s_off, s_len, draws, descs, rows, comp, cursor, err, caps_d;
-  DevBuf summary, best_cap, cell_scratch;
+  DevBuf summary, best_cap, cell_scratch, ratios;
   Scratch scratch;
   Timer all, sim;
   double last_ms = 0.0, sim_ms = 0.0;
   int launches = 0;
   bool summarized = false;
+  int64_t h2d_bytes = 0;
 };
 
 namespace {
@@ -507,13 +514,14 @@ saber_status saber_cuda_sweep_plan_create(const saber_sweep_desc* desc, saber_sw
   ALLOC_TRY(P->summary, dev, static_cast<size_t>(n_mixes) * sizeof(saber_mix_summary));
   ALLOC_TRY(P->best_cap, dev, static_cast<size_t>(n_mixes) * n_rps * 4);
   ALLOC_TRY(P->cell_scratch, dev, static_cast<size_t>(n_mixes) * n_rps * 6 * 8);
+  ALLOC_TRY(P->ratios, dev, static_cast<size_t>(P->n_rows) * n * 8);
   if (desc->with_saber) {
     ALLOC_TRY(P->seeds, dev, seeds.size() * 8);
     ALLOC_TRY(P->s_off, dev, off.size() * 8);
     ALLOC_TRY(P->s_len, dev, off.size() * 8);
     ALLOC_TRY(P->draws, dev, static_cast<size_t>(std::max<int64_t>(1, P->total_draws)) * 4);
   }
-  if (saber_status s = P->scratch.alloc(dev, P->nwords, n)) return s;
+  if (saber_status s = P->scratch.alloc(dev, n)) return s;
 
   CUDA_TRY(cudaMemcpy(P->wl.items.p, items.data(), items.size() * sizeof(WorkloadItem),
                       cudaMemcpyHostToDevice));
@@ -529,6 +537,9 @@ saber_status saber_cuda_sweep_plan_create(const saber_sweep_desc* desc, saber_sw
     CUDA_TRY(cudaMemcpy(P->s_off.p, off.data(), off.size() * 8, cudaMemcpyHostToDevice));
     CUDA_TRY(cudaMemcpy(P->s_len.p, P->stream_len.data(), off.size() * 8, cudaMemcpyHostToDevice));
   }
+  P->h2d_bytes = static_cast<int64_t>(items.size() * sizeof(WorkloadItem) + base.size() * 8 +
+                                      th.size() * 8 + tt.size() + tlast.size() + tab.size() * 8 +
+                                      P->caps.size() * 4 + seeds.size() * 8 + off.size() * 16);
   if (saber_status s = P->all.init()) return s;
   if (saber_status s = P->sim.init()) return s;
   *out = guard.release();
@@ -611,12 +622,13 @@ saber_status saber_cuda_sweep_plan_run(saber_sweep_plan* P, void* stream) {
   sp.rng.off = P->s_off.as<int64_t>();
   sp.rng.len = P->s_len.as<int64_t>();
   sp.scratch = P->scratch.view;
+  sp.slot_rows = P->scratch.launch.slot_rows;
   sp.out.rows = P->rows.as<saber_traj_row>();
   sp.out.completion = P->comp.as<double>();
   sp.out.error = P->err.as<int32_t>();
   sp.next_traj = P->cursor.as<int32_t>();
   CUDA_TRY(cudaEventRecord(P->sim.a, s));
-  LAUNCH_TRY(launch_sim(sp, P->nwords, P->scratch.grid, 128, s));
+  LAUNCH_TRY(launch_sim(sp, P->scratch.launch, s));
   CUDA_TRY(cudaEventRecord(P->sim.b, s));
   ++P->launches;
 
@@ -662,6 +674,7 @@ saber_status saber_cuda_sweep_plan_summarize(saber_sweep_plan* P, void* stream) 
   sp.summary = P->summary.as<saber_mix_summary>();
   sp.best_cap = P->best_cap.as<int32_t>();
   sp.scratch = P->cell_scratch.as<double>();
+  sp.ratios = P->ratios.as<double>();
   CUDA_TRY(cudaEventRecord(P->all.a, s));
   LAUNCH_TRY(launch_summary(sp, s));
   CUDA_TRY(cudaEventRecord(P->all.b, s));
@@ -669,7 +682,7 @@ saber_status saber_cuda_sweep_plan_summarize(saber_sweep_plan* P, void* stream) 
   float ms = 0.f;
   CUDA_TRY(cudaEventElapsedTime(&ms, P->all.a, P->all.b));
   P->last_ms += ms;
-  P->launches += 2;
+  P->launches += 3;
   P->summarized = true;
   return SABER_OK;
 }
@@ -689,6 +702,12 @@ saber_status saber_cuda_sweep_plan_fetch(saber_sweep_plan* P, saber_sweep_out* o
   if (!P || !out) return fail(SABER_EINVAL, "null argument");
   CUDA_TRY(cudaSetDevice(P->device));
   out->n_rows = P->n_rows;
+  out->h2d_bytes = P->h2d_bytes;
+  out->d2h_bytes = 0;
+  if (out->rows) out->d2h_bytes += static_cast<int64_t>(P->n_rows) * sizeof(saber_traj_row);
+  if (out->completion_times) out->d2h_bytes += static_cast<int64_t>(P->n_rows) * P->n * 8;
+  if (out->summary) out->d2h_bytes += P->desc.n_mixes * static_cast<int64_t>(sizeof(saber_mix_summary));
+  if (out->best_cap_by_rps) out->d2h_bytes += static_cast<int64_t>(P->desc.n_mixes) * P->desc.n_rps * 4;
   if (out->rows)
     CUDA_TRY(cudaMemcpy(out->rows, P->rows.p, static_cast<size_t>(P->n_rows) * sizeof(saber_traj_row),
                         cudaMemcpyDeviceToHost));
@@ -936,8 +955,7 @@ extern "C" saber_status saber_cuda_run_batch(const saber_run_batch_desc* desc,
     ALLOC_TRY(len_d, dev, len.size() * 8);
     ALLOC_TRY(draws_d, dev, static_cast<size_t>(std::max<int64_t>(1, total_draws)) * 4);
   }
-  const int nwords = nwords_for(nmax);
-  if (saber_status s = scratch.alloc(dev, nwords, nmax)) return s;
+  if (saber_status s = scratch.alloc(dev, nmax)) return s;
 
   CUDA_TRY(cudaMemcpy(wl.items.p, items.data(), items.size() * sizeof(WorkloadItem), cudaMemcpyHostToDevice));
   CUDA_TRY(cudaMemcpy(wl.seed_base.p, base.data(), base.size() * 8, cudaMemcpyHostToDevice));
@@ -1011,6 +1029,7 @@ extern "C" saber_status saber_cuda_run_batch(const saber_run_batch_desc* desc,
   sp.rng.off = off_d.as<int64_t>();
   sp.rng.len = len_d.as<int64_t>();
   sp.scratch = scratch.view;
+  sp.slot_rows = scratch.launch.slot_rows;
   sp.out.rows = rows_d.as<saber_traj_row>();
   sp.out.completion = comp_d.as<double>();
   sp.out.admit = records ? admit_d.as<double>() : nullptr;
@@ -1020,7 +1039,7 @@ extern "C" saber_status saber_cuda_run_batch(const saber_run_batch_desc* desc,
   sp.out.trace_cap = trace ? out->decision_cap : 0;
   sp.out.error = err_d.as<int32_t>();
   sp.next_traj = cursor_d.as<int32_t>();
-  LAUNCH_TRY(launch_sim(sp, nwords, scratch.grid, 128, st));
+  LAUNCH_TRY(launch_sim(sp, scratch.launch, st));
   ++launches;
   RowMetricsParams rm{};
   rm.rows = rows_d.as<saber_traj_row>();

@@ -60,14 +60,13 @@ struct RngStreams {
 
 constexpr uint32_t kDrawModulus = 720720u;  // lcm(1..16)
 
-// Per-lane scratch (global memory, lane-interleaved).
-struct LaneScratch {
-  double* slot_g;      // [lanes/32][S][32] generated (>=0) or -prefill_left (<0)
-  double* slot_m;      // [lanes/32][S][32] max_output_tokens
-  uint16_t* slot_id;   // [lanes/32][S][32]
-  double* ledger_need; // [lanes/32][nmax][32]
-  uint16_t* low_fifo;  // [lanes/32][nmax][32]
-  int32_t slots;       // S (= nmax)
+// Per-group scratch in global memory for the rarely touched queues
+// (DESIGN.md §2): the ledger's frozen requirements and the low-tier FIFO.
+// The hot per-slot state lives in shared memory (sim_kernel.cu).
+struct GroupScratch {
+  double* ledger_need;  // [groups][nmax]
+  uint16_t* low_fifo;   // [groups][nmax]
+  int64_t groups;
 };
 
 // Outputs of the trajectory kernel.
@@ -88,7 +87,8 @@ struct SimParams {
   WorkloadTables wl;
   const double* tables;       // predict tables, table[L] at model_tab + L
   RngStreams rng;
-  LaneScratch scratch;
+  GroupScratch scratch;
+  int32_t slot_rows;          // ceil(nmax / G): shared-memory slot rows per warp
   SimOutputs out;
   int32_t* next_traj;         // work-queue cursor (device)
 };
@@ -102,8 +102,17 @@ enum : int32_t {
 };
 
 // Kernel launchers (defined in the .cu files).
-int launch_sim(const SimParams& p, int nwords, int grid, int block, void* stream);
-int sim_occupancy_grid(int nwords, int block, int* grid);
+// Trajectory kernel configuration: G lanes per trajectory, 4 warps per block.
+struct SimLaunch {
+  int nwords;     // 64-bit mask words (n <= 64 * nwords)
+  int group;      // lanes per trajectory
+  int grid;       // persistent blocks
+  int slot_rows;  // ceil(nmax / group)
+  size_t smem;    // dynamic shared memory per block
+};
+constexpr int kSimBlock = 128;
+int plan_sim(int nmax, int group, SimLaunch* out);
+int launch_sim(const SimParams& p, const SimLaunch& l, void* stream);
 
 struct RngGenParams {
   const uint64_t* seeds;  // [n_streams] already xor-salted
@@ -180,7 +189,8 @@ struct SummaryParams {
   const int32_t* caps;
   saber_mix_summary* summary;   // [n_mixes]
   int32_t* best_cap;            // [n_mixes][n_rps]
-  double* scratch;              // [n_mixes][n_rps][4] cell-level means/counts
+  double* scratch;              // [n_mixes][n_rps][6] cell-level means/flags
+  double* ratios;               // [n_rows][n] latency/SLA ratios (NaN = never completed)
 };
 int launch_summary(const SummaryParams& p, void* stream);
 

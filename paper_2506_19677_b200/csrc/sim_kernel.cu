@@ -1,32 +1,39 @@
 // sim_kernel.cu — the trajectory engine (K1) and its per-row metrics epilogue
 // (K2) for sm_100a.
 //
-// One LANE owns one trajectory: a persistent grid pulls
-// trajectory indices from a warp-aggregated atomic work queue, and each lane
-// runs the reference's tick loop (simloop.cpp:78-101) for its trajectory:
+// A GROUP of G lanes owns one trajectory.  A persistent grid
+// pulls trajectory indices from an atomic work queue; every lane of the group
+// carries an identical copy of the trajectory's scalar state (clock, tiers as
+// register bitmasks, ledger, RNG cursor, decision hash) and runs the
+// reference's tick loop (simloop.cpp:78-101):
 //   arrivals -> refresh_tiers -> admission_step | static_step  (scheduler.cpp)
 //   -> Engine::advance_to (engine.cpp:51-127) -> completions.
-// 32 trajectories share a warp's instruction stream, so per-tick scheduler
-// logic costs ~1/32 of an issue slot per trajectory instead of a whole warp.
+// The engine's per-slot work — the only part that scales with the batch — is
+// split across the group: slot k is updated by lane k % G, with the slot
+// state (fluid progress / prefill debt, max_out | id) held in shared memory in
+// a lane-interleaved layout (conflict-free 64-bit accesses), and the
+// next-event minima combined with REDUX.MIN over the group.
 //
 // Bit-exactness with the reference: compiled with --fmad=false
 // (the reference has no FMA); every floating-point expression keeps
 // the reference's operand order; predict() comes from host-built tables
 // (SURVEY F6); the scheduler RNG from precomputed mt19937_64 streams
-// (SURVEY F2).  Two exact algebraic rewrites remove per-slot divides:
+// (SURVEY F2).  Three exact rewrites remove work without changing any result:
 //   * min_i fl(rem_i / speed) == fl(min_i rem_i / speed), because correctly
 //     rounded division by a positive constant is monotone;
+//   * that one divide is skipped when min_rem >= speed*dt*(1+1e-12), which
+//     proves fl(min_rem / speed) >= dt, i.e. the boundary cannot bind;
 //   * a high-tier request cannot demote before demote_after[i], a safe lower
 //     bound (prologue.cu), so refresh only scans when one might.
-#include <cooperative_groups.h>
+// Slot order inside the engine never affects a result (min is order-free,
+// completions of one pass share the clock), so completed slots are removed by
+// swap-with-last instead of the reference's order-preserving erase.
 #include <cuda_runtime.h>
 
 #include <cmath>
 #include <cstdint>
 
 #include "saber_internal.h"
-
-namespace cg = cooperative_groups;
 
 namespace saberb200 {
 namespace {
@@ -35,7 +42,8 @@ constexpr double kInf = __builtin_huge_val();
 constexpr double kOnePlusTol = 1.0 + 1e-12;  // engine.cpp:17,76 (kGroupTol)
 constexpr uint64_t kHashSeed = 0x243F6A8885A308D3ULL;
 constexpr uint64_t kAbsent = 0xFFF8000000000001ULL;
-constexpr int kBlock = 128;
+constexpr uint64_t kDoneMark = 0xFFF0DEAD0000DEADULL;  // a NaN the engine never produces
+constexpr uint64_t kIdMask = 0xFFFFull;
 
 __device__ __forceinline__ uint64_t hstep(uint64_t h, uint64_t x) {
   h ^= x;
@@ -49,6 +57,10 @@ __device__ __forceinline__ uint64_t rotl64(uint64_t x, int r) {
 __device__ __forceinline__ uint64_t dbits(double v) {
   return static_cast<uint64_t>(__double_as_longlong(v));
 }
+__device__ __forceinline__ double bitsd(uint64_t b) {
+  return __longlong_as_double(static_cast<long long>(b));
+}
+__device__ __forceinline__ double dmin(double a, double b) { return (b < a) ? b : a; }
 
 // required_speed (types.cpp:82-88) for a queued request: generated == 0.
 __device__ __forceinline__ double queued_need(double max_out, double deadline,
@@ -59,67 +71,75 @@ __device__ __forceinline__ double queued_need(double max_out, double deadline,
   return remaining / (deadline - now);
 }
 
-// Per-request tier membership as an NW x 64-bit register bitmask.  All word
-// indices are resolved through unrolled selects so nothing spills to local
-// memory.
-template <int NW>
+// Group minimum of a non-negative double (IEEE order == unsigned bit order).
+template <int G>
+__device__ __forceinline__ double group_min_pos(double v, unsigned gmask) {
+  if (G == 1) return v;
+  const uint64_t b = dbits(v);
+  const unsigned hi = static_cast<unsigned>(b >> 32);
+  const unsigned lo = static_cast<unsigned>(b);
+  const unsigned mhi = __reduce_min_sync(gmask, hi);
+  const unsigned mlo = __reduce_min_sync(gmask, hi == mhi ? lo : 0xFFFFFFFFu);
+  return bitsd((static_cast<uint64_t>(mhi) << 32) | mlo);
+}
+template <int G>
+__device__ __forceinline__ unsigned group_sum(unsigned v, unsigned gmask) {
+  if (G == 1) return v;
+  return __reduce_add_sync(gmask, v);
+}
+
+// Per-request tier membership as an NW x 64-bit register bitmask.  Built as a
+// recursive struct of scalar words (no array), so a runtime word index can
+// never turn into a local-memory access.
+template <int NW, int B = 0>
 struct Mask {
-  uint64_t w[NW];
-  __device__ __forceinline__ void clear() {
-#pragma unroll
-    for (int i = 0; i < NW; ++i) w[i] = 0;
-  }
+  uint64_t w;
+  Mask<NW - 1, B + 1> r;
+  __device__ __forceinline__ void clear() { w = 0; r.clear(); }
   __device__ __forceinline__ void set(int id) {
-#pragma unroll
-    for (int i = 0; i < NW; ++i)
-      if (i == (id >> 6)) w[i] |= 1ull << (id & 63);
+    if ((id >> 6) == B) w |= 1ull << (id & 63);
+    else r.set(id);
   }
   __device__ __forceinline__ void reset(int id) {
-#pragma unroll
-    for (int i = 0; i < NW; ++i)
-      if (i == (id >> 6)) w[i] &= ~(1ull << (id & 63));
+    if ((id >> 6) == B) w &= ~(1ull << (id & 63));
+    else r.reset(id);
   }
   __device__ __forceinline__ bool test(int id) const {
-    bool r = false;
-#pragma unroll
-    for (int i = 0; i < NW; ++i)
-      if (i == (id >> 6)) r = (w[i] >> (id & 63)) & 1ull;
-    return r;
+    return (id >> 6) == B ? ((w >> (id & 63)) & 1ull) != 0 : r.test(id);
   }
-  __device__ __forceinline__ bool any() const {
-    uint64_t a = 0;
-#pragma unroll
-    for (int i = 0; i < NW; ++i) a |= w[i];
-    return a != 0;
+  __device__ __forceinline__ uint64_t word(int i) const { return i == B ? w : r.word(i); }
+  __device__ __forceinline__ void andnot(int i, uint64_t m) {
+    if (i == B) w &= ~m;
+    else r.andnot(i, m);
   }
-  __device__ __forceinline__ int count() const {
-    int c = 0;
-#pragma unroll
-    for (int i = 0; i < NW; ++i) c += __popcll(w[i]);
-    return c;
-  }
+  __device__ __forceinline__ bool any() const { return w != 0 || r.any(); }
+  __device__ __forceinline__ int count() const { return __popcll(w) + r.count(); }
   __device__ __forceinline__ int lowest() const {
-    int r = -1;
-#pragma unroll
-    for (int i = NW - 1; i >= 0; --i)
-      if (w[i]) r = i * 64 + __ffsll(static_cast<long long>(w[i])) - 1;
-    return r;
+    return w ? B * 64 + __ffsll(static_cast<long long>(w)) - 1 : r.lowest();
   }
   // k-th set bit in ascending id order (0-based); k < count().
   __device__ __forceinline__ int select(int k) const {
-    int r = -1;
-#pragma unroll
-    for (int i = 0; i < NW; ++i) {
-      const int c = __popcll(w[i]);
-      if (r < 0 && k < c) {
-        uint64_t x = w[i];
-        for (int j = 0; j < k; ++j) x &= x - 1;
-        r = i * 64 + __ffsll(static_cast<long long>(x)) - 1;
-      }
-      if (r < 0) k -= c;
+    const int c = __popcll(w);
+    if (k < c) {
+      uint64_t x = w;
+      for (int j = 0; j < k; ++j) x &= x - 1;
+      return B * 64 + __ffsll(static_cast<long long>(x)) - 1;
     }
-    return r;
+    return r.select(k - c);
   }
+};
+template <int B>
+struct Mask<0, B> {
+  __device__ __forceinline__ void clear() {}
+  __device__ __forceinline__ void set(int) {}
+  __device__ __forceinline__ void reset(int) {}
+  __device__ __forceinline__ bool test(int) const { return false; }
+  __device__ __forceinline__ uint64_t word(int) const { return 0; }
+  __device__ __forceinline__ void andnot(int, uint64_t) {}
+  __device__ __forceinline__ bool any() const { return false; }
+  __device__ __forceinline__ int count() const { return 0; }
+  __device__ __forceinline__ int lowest() const { return -1; }
+  __device__ __forceinline__ int select(int) const { return -1; }
 };
 
 struct DecisionLog {
@@ -132,13 +152,13 @@ template <bool kTrace>
 __device__ __forceinline__ void push_decision(DecisionLog& L, double t, int id,
                                               int kind, int load, uint64_t pb,
                                               uint64_t rb, saber_decision* tr,
-                                              int64_t cap, int32_t* err) {
+                                              int64_t cap, int32_t* err, bool writer) {
   const uint64_t w = static_cast<uint64_t>(static_cast<uint32_t>(id)) |
                      (static_cast<uint64_t>(kind) << 32) |
                      (static_cast<uint64_t>(static_cast<uint32_t>(load)) << 40);
   L.h = hstep(L.h, dbits(t));
   L.h = hstep(L.h, w ^ rotl64(pb, 17) ^ rotl64(rb, 43));
-  if (kTrace && tr != nullptr) {
+  if (kTrace && tr != nullptr && writer) {
     if (L.n < cap) {
       saber_decision& d = tr[L.n];
       d.time = t;
@@ -147,8 +167,8 @@ __device__ __forceinline__ void push_decision(DecisionLog& L, double t, int id,
       d.load_before = load;
       d.has_pred = pb != kAbsent;
       d.has_req = rb != kAbsent;
-      d.pred_speed = pb != kAbsent ? __longlong_as_double(static_cast<long long>(pb)) : nan("");
-      d.req_speed = rb != kAbsent ? __longlong_as_double(static_cast<long long>(rb)) : nan("");
+      d.pred_speed = pb != kAbsent ? bitsd(pb) : nan("");
+      d.req_speed = rb != kAbsent ? bitsd(rb) : nan("");
     } else {
       atomicCAS(err, kErrNone, kErrTraceOverflow);
     }
@@ -161,13 +181,21 @@ __device__ __forceinline__ void push_decision(DecisionLog& L, double t, int id,
   L.k4 += kind == 4;
 }
 
-// Simulates trajectory `ti` on this lane.  G/M/SID are the lane's slot arrays
-// (stride 32), LNEED/LOW its ledger and low-tier FIFO (stride 32).
-template <int NW, bool kTrace, bool kRecords>
-__device__ __forceinline__ void simulate_one(const SimParams& P, int ti,
-                                             double* __restrict__ G,
-                                             double* __restrict__ M,
-                                             uint16_t* __restrict__ SID,
+// Shared-memory slot arrays of one group: slot k lives at row k / G, column
+// grp * G + k % G of the warp's [rows][32] tile (so lane k % G of the group
+// always touches its own column: 32 lanes hit 32 consecutive 8-byte words).
+template <int G>
+struct Slots {
+  double* g;     // fluid progress (>= 0) or -prefill_left (< 0); kDoneMark when done
+  uint64_t* m;   // bits(max_output_tokens) | request id (low 16 bits are free)
+  int col0;      // grp * G
+  __device__ __forceinline__ int idx(int k) const { return (k / G) * kWarp + col0 + (k % G); }
+};
+
+// Simulates trajectory `ti` on this group.
+template <int NW, int G, bool kTrace, bool kRecords>
+__device__ __forceinline__ void simulate_one(const SimParams& P, int ti, const Slots<G>& S,
+                                             int sub, unsigned gmask,
                                              double* __restrict__ LNEED,
                                              uint16_t* __restrict__ LOW) {
   const TrajDesc d = P.traj[ti];
@@ -193,6 +221,7 @@ __device__ __forceinline__ void simulate_one(const SimParams& P, int ti,
   double* __restrict__ ADM = kRecords && P.out.admit ? P.out.admit + d.row * nmax : nullptr;
   uint8_t* __restrict__ DEMO =
       kRecords && P.out.demoted ? P.out.demoted + d.row * nmax : nullptr;
+  const bool leader = sub == 0;
   saber_decision* tr = kTrace && P.out.trace ? P.out.trace + d.row * P.out.trace_cap : nullptr;
 
   Mask<NW> high, ledger;
@@ -217,29 +246,30 @@ __device__ __forceinline__ void simulate_one(const SimParams& P, int ti,
   int32_t ticks = 0, passes = 0, decode_updates = 0, prefill_updates = 0;
   int32_t refresh_entries = 0, cands = 0, ledger_scanned = 0, rng_draws = 0;
 
-  // Engine::admit (engine.cpp:26-49), slot appended in admit order.
+  // Engine::admit (engine.cpp:26-49): append slot A.  Every lane of the group
+  // writes the same values, so the owning lane reads back its own write.
   auto admit = [&](int id, double now) {
     const double pl = pr > 0.0 ? IN[id] / pr : 0.0;
     const double m = MO[id];
+    const int s = S.idx(A);
     if (pl == 0.0) {
-      G[A * kWarp] = 0.0;  // decode starts at admission
-      min_rem = fmin(min_rem, m - 0.0);
+      S.g[s] = 0.0;  // decode starts at admission
+      min_rem = dmin(min_rem, m - 0.0);
     } else {
-      G[A * kWarp] = -pl;
-      min_pf = fmin(min_pf, pl);
+      S.g[s] = -pl;
+      min_pf = dmin(min_pf, pl);
     }
-    M[A * kWarp] = m;
-    SID[A * kWarp] = static_cast<uint16_t>(id);
+    S.m[s] = dbits(m) | static_cast<uint64_t>(id);
     ++A;
-    if (kRecords && ADM) ADM[id] = now;
+    if (kRecords && ADM && leader) ADM[id] = now;
   };
 
   double t = 0.0;
   for (;;) {
-    // Arrivals due at t (simloop.cpp:79-85): arrival times strictly increase.
+    // Arrivals due at t (simloop.cpp:79-85).
     while (na_t <= t) {
       high.set(next);
-      if (saber) min_td = fmin(min_td, DEM[next]);
+      if (saber) min_td = dmin(min_td, DEM[next]);
       ++next;
       na_t = next < n ? ARR[next] : kInf;
     }
@@ -252,9 +282,8 @@ __device__ __forceinline__ void simulate_one(const SimParams& P, int ti,
       // when some entry may have crossed its demotion bound.
       if (hc > 0 && t >= min_td) {
         double nm = kInf;
-#pragma unroll
         for (int i = 0; i < NW; ++i) {
-          uint64_t b = high.w[i];
+          uint64_t b = high.word(i);
           while (b) {
             const int bit = __ffsll(static_cast<long long>(b)) - 1;
             b &= b - 1;
@@ -265,15 +294,15 @@ __device__ __forceinline__ void simulate_one(const SimParams& P, int ti,
               const double need = queued_need(MO[id], DL[id], t);
               if (need > ceiling) {
                 demote = true;
-                high.w[i] &= ~(1ull << bit);
-                LOW[low_tail * kWarp] = static_cast<uint16_t>(id);
+                high.andnot(i, 1ull << bit);
+                LOW[low_tail] = static_cast<uint16_t>(id);
                 ++low_tail;
-                push_decision<kTrace>(L, t, id, SABER_DEMOTE, load, dbits(ceiling),
-                                      dbits(need), tr, P.out.trace_cap, P.out.error);
-                if (kRecords && DEMO) DEMO[id] = 1;
+                push_decision<kTrace>(L, t, id, SABER_DEMOTE, load, dbits(ceiling), dbits(need),
+                                      tr, P.out.trace_cap, P.out.error, leader);
+                if (kRecords && DEMO && leader) DEMO[id] = 1;
               }
             }
-            if (!demote) nm = fmin(nm, T);
+            if (!demote) nm = dmin(nm, T);
           }
         }
         min_td = nm;
@@ -283,22 +312,21 @@ __device__ __forceinline__ void simulate_one(const SimParams& P, int ti,
         const int hcount = high.count();
         const int w = d.window < hcount ? d.window : hcount;
         uint64_t ord = 0xFEDCBA9876543210ull;  // window positions as nibbles
+        if (draw_pos + (w - 1) > draw_len) {
+          failed = true;
+          break;
+        }
 #pragma unroll
         for (int i = kMaxWindow - 1; i >= 1; --i) {
           if (i < w) {
-            if (draw_pos >= draw_len) {
-              failed = true;
-            } else {
-              const uint32_t x = draws[draw_pos++];
-              const uint32_t j = x % static_cast<uint32_t>(i + 1);  // rng() % (i+1)
-              const uint64_t a = (ord >> (4 * i)) & 15ull;
-              const uint64_t bb = (ord >> (4 * j)) & 15ull;
-              const uint64_t x2 = a ^ bb;
-              ord ^= (x2 << (4 * i)) | (x2 << (4 * j));
-            }
+            const uint32_t x = draws[draw_pos++];
+            const uint32_t j = x % static_cast<uint32_t>(i + 1);  // rng() % (i+1)
+            const uint64_t a = (ord >> (4 * i)) & 15ull;
+            const uint64_t bb = (ord >> (4 * j)) & 15ull;
+            const uint64_t x2 = a ^ bb;
+            ord ^= (x2 << (4 * i)) | (x2 << (4 * j));
           }
         }
-        if (failed) break;
         rng_draws += w - 1;
         const double pred = MT[load + 1];
         const bool violates = pred < ledger_max;  // ActiveLedger::violates
@@ -309,33 +337,33 @@ __device__ __forceinline__ void simulate_one(const SimParams& P, int ti,
           ++cands;
           const double need = queued_need(MO[id], DL[id], t);
           if (pred < need) {
-            push_decision<kTrace>(L, t, id, SABER_REJECT_OWN, load, dbits(pred),
-                                  dbits(need), tr, P.out.trace_cap, P.out.error);
+            push_decision<kTrace>(L, t, id, SABER_REJECT_OWN, load, dbits(pred), dbits(need),
+                                  tr, P.out.trace_cap, P.out.error, leader);
             continue;
           }
           if (violates) {
-            push_decision<kTrace>(L, t, id, SABER_REJECT_ACTIVE, load, dbits(pred),
-                                  dbits(need), tr, P.out.trace_cap, P.out.error);
+            push_decision<kTrace>(L, t, id, SABER_REJECT_ACTIVE, load, dbits(pred), dbits(need),
+                                  tr, P.out.trace_cap, P.out.error, leader);
             continue;
           }
           admit(id, t);
           ledger.set(id);
           ++ledger_size;
-          LNEED[id * kWarp] = need;
+          LNEED[id] = need;
           ledger_max = (ledger_max < need) ? need : ledger_max;
           high.reset(id);
-          push_decision<kTrace>(L, t, id, SABER_ADMIT_HIGH, load, dbits(pred),
-                                dbits(need), tr, P.out.trace_cap, P.out.error);
+          push_decision<kTrace>(L, t, id, SABER_ADMIT_HIGH, load, dbits(pred), dbits(need), tr,
+                                P.out.trace_cap, P.out.error, leader);
           break;
         }
       } else if (low_head < low_tail) {
         // admission_step, low tier (scheduler.cpp:97-108).
-        const int id = LOW[low_head * kWarp];
+        const int id = LOW[low_head];
         ++low_head;
         const double need = queued_need(MO[id], DL[id], t);
         admit(id, t);
-        push_decision<kTrace>(L, t, id, SABER_ADMIT_LOW, load, kAbsent, dbits(need),
-                              tr, P.out.trace_cap, P.out.error);
+        push_decision<kTrace>(L, t, id, SABER_ADMIT_LOW, load, kAbsent, dbits(need), tr,
+                              P.out.trace_cap, P.out.error, leader);
       }
     } else {
       // StaticScheduler::static_step (scheduler.cpp:129-144).
@@ -344,8 +372,8 @@ __device__ __forceinline__ void simulate_one(const SimParams& P, int ti,
         high.reset(id);
         const int before = A;
         admit(id, t);
-        push_decision<kTrace>(L, t, id, SABER_ADMIT_HIGH, before, kAbsent, kAbsent,
-                              tr, P.out.trace_cap, P.out.error);
+        push_decision<kTrace>(L, t, id, SABER_ADMIT_HIGH, before, kAbsent, kAbsent, tr,
+                              P.out.trace_cap, P.out.error, leader);
       }
     }
 
@@ -353,7 +381,6 @@ __device__ __forceinline__ void simulate_one(const SimParams& P, int ti,
     const double nt = (horizon < t + tick) ? horizon : t + tick;
 
     // Engine::advance_to(nt) (engine.cpp:51-127).
-    bool ledger_dirty = false;
     while (clock < nt) {
       if (A == 0) {
         clock = nt;
@@ -363,27 +390,32 @@ __device__ __forceinline__ void simulate_one(const SimParams& P, int ti,
       const double speed = GT[A];
       double dt = nt - clock;
       if (min_pf < dt) dt = min_pf;
-      const double bnd = min_rem / speed;
-      if (bnd < dt) dt = bnd;
+      // dt = min(dt, fl(min_rem / speed)); the divide can only bind when
+      // min_rem < speed * dt * (1 + 1e-12) (see header).
+      if (min_rem < speed * dt * kOnePlusTol) {
+        const double bnd = min_rem / speed;
+        if (bnd < dt) dt = bnd;
+      }
       const double group = dt * kOnePlusTol;
       const double sdt = speed * dt;
       const double sgd = speed * (group - dt);
       const double nclock = clock + dt;
       double npf = kInf, nrem = kInf;
-      int j = 0;
-      decode_updates += A;
-      for (int k = 0; k < A; ++k) {
-        double g = G[k * kWarp];
-        const double m = M[k * kWarp];
+      unsigned pf_count = 0, done_count = 0;
+      for (int k = sub; k < A; k += G) {
+        const int s = S.idx(k);
+        double g = S.g[s];
+        const uint64_t mb = S.m[s];
+        const double m = bitsd(mb & ~kIdMask);
         bool done;
         if (g < 0.0) {  // prefill slot: g = -prefill_left
-          ++prefill_updates;
+          ++pf_count;
           if (-g <= group) {
             g = 0.0;  // decode starts at nclock
             done = g + sgd >= m;
           } else {
             g = g + dt;  // == -(prefill_left - dt), exactly
-            npf = fmin(npf, -g);
+            npf = dmin(npf, -g);
             done = false;
           }
         } else {
@@ -391,94 +423,124 @@ __device__ __forceinline__ void simulate_one(const SimParams& P, int ti,
           done = g + sgd >= m;
         }
         if (!done) {
-          if (g >= 0.0) nrem = fmin(nrem, m - g);
-          G[j * kWarp] = g;
-          if (j != k) {
-            M[j * kWarp] = m;
-            SID[j * kWarp] = SID[k * kWarp];
-          }
-          ++j;
+          if (g >= 0.0) nrem = dmin(nrem, m - g);
+          S.g[s] = g;
         } else {
-          const int id = SID[k * kWarp];
-          COMP[id] = nclock;
-          ++completed;
+          S.g[s] = bitsd(kDoneMark);
+          COMP[static_cast<int>(mb & kIdMask)] = nclock;
+          ++done_count;
+        }
+      }
+      min_pf = group_min_pos<G>(npf, gmask);
+      min_rem = group_min_pos<G>(nrem, gmask);
+      prefill_updates += static_cast<int32_t>(group_sum<G>(pf_count, gmask));
+      decode_updates += A;
+      const unsigned ndone = group_sum<G>(done_count, gmask);
+      if (ndone) {
+        // Rare path (once per completion event): every lane replays the
+        // completions for the replicated scheduler state, then the leader
+        // compacts the slot array by swap-with-last.
+        __syncwarp(gmask);
+        bool dirty = false;
+        for (int k = 0; k < A; ++k) {
+          const int s = S.idx(k);
+          if (dbits(S.g[s]) != kDoneMark) continue;
+          const int id = static_cast<int>(S.m[s] & kIdMask);
           if (saber && ledger.test(id)) {
             ledger.reset(id);
             --ledger_size;
-            ledger_dirty = true;
+            dirty = true;
           }
         }
-      }
-      A = j;
-      clock = nclock;
-      min_pf = npf;
-      min_rem = nrem;
-    }
-    if (ledger_dirty) {
-      double mx = -kInf;
-#pragma unroll
-      for (int i = 0; i < NW; ++i) {
-        uint64_t b = ledger.w[i];
-        while (b) {
-          const int id = i * 64 + __ffsll(static_cast<long long>(b)) - 1;
-          b &= b - 1;
-          const double v = LNEED[id * kWarp];
-          mx = (mx < v) ? v : mx;
+        __syncwarp(gmask);
+        if (leader) {
+          int a = A;
+          for (int k = 0; k < a;) {
+            const int s = S.idx(k);
+            if (dbits(S.g[s]) != kDoneMark) {
+              ++k;
+              continue;
+            }
+            const int last = S.idx(a - 1);
+            S.g[s] = S.g[last];
+            S.m[s] = S.m[last];
+            --a;
+          }
+        }
+        __syncwarp(gmask);
+        A -= static_cast<int>(ndone);
+        completed += static_cast<int>(ndone);
+        if (dirty) {
+          double mx = -kInf;
+          for (int i = 0; i < NW; ++i) {
+            uint64_t b = ledger.word(i);
+            while (b) {
+              const int id = i * 64 + __ffsll(static_cast<long long>(b)) - 1;
+              b &= b - 1;
+              const double v = LNEED[id];
+              mx = (mx < v) ? v : mx;
+            }
+          }
+          ledger_max = mx;
         }
       }
-      ledger_max = mx;
+      clock = nclock;
     }
     t = nt;
     if (completed == n) break;
   }
   decode_updates -= prefill_updates;
 
-  if (failed) atomicCAS(P.out.error, kErrNone, kErrRngExhausted);
-  saber_traj_row* R = P.out.rows + d.row;
-  R->n = n;
-  R->decisions = L.n;
-  R->n_kind[0] = L.k0;
-  R->n_kind[1] = L.k1;
-  R->n_kind[2] = L.k2;
-  R->n_kind[3] = L.k3;
-  R->n_kind[4] = L.k4;
-  R->decision_hash = L.h;
-  R->ticks = ticks;
-  R->passes = passes;
-  R->decode_updates = decode_updates;
-  R->prefill_updates = prefill_updates;
-  R->refresh_entries = refresh_entries;
-  R->gate_candidates = cands;
-  R->ledger_scanned = ledger_scanned;
-  R->rng_draws = rng_draws;
-  R->last_arrival = n > 0 ? ARR[n - 1] : 0.0;
-  R->horizon = horizon;
-  if (kTrace && P.out.trace_count) P.out.trace_count[d.row] = L.n;
+  if (failed && leader) atomicCAS(P.out.error, kErrNone, kErrRngExhausted);
+  if (leader) {
+    saber_traj_row* R = P.out.rows + d.row;
+    R->n = n;
+    R->decisions = L.n;
+    R->n_kind[0] = L.k0;
+    R->n_kind[1] = L.k1;
+    R->n_kind[2] = L.k2;
+    R->n_kind[3] = L.k3;
+    R->n_kind[4] = L.k4;
+    R->decision_hash = L.h;
+    R->ticks = ticks;
+    R->passes = passes;
+    R->decode_updates = decode_updates;
+    R->prefill_updates = prefill_updates;
+    R->refresh_entries = refresh_entries;
+    R->gate_candidates = cands;
+    R->ledger_scanned = ledger_scanned;
+    R->rng_draws = rng_draws;
+    R->last_arrival = n > 0 ? ARR[n - 1] : 0.0;
+    R->horizon = horizon;
+    if (kTrace && P.out.trace_count) P.out.trace_count[d.row] = L.n;
+  }
 }
 
-template <int NW, bool kTrace, bool kRecords>
-__global__ void __launch_bounds__(kBlock) sim_kernel(const SimParams P) {
+template <int NW, int G, bool kTrace, bool kRecords>
+__global__ void __launch_bounds__(kSimBlock) sim_kernel(const SimParams P) {
+  extern __shared__ __align__(16) uint64_t smem[];
   const int lane = threadIdx.x & 31;
-  const int64_t warp_global = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-  const int64_t S = P.scratch.slots;
-  const int64_t sb = warp_global * S * kWarp + lane;
-  const int64_t nb = warp_global * static_cast<int64_t>(P.wl.nmax) * kWarp + lane;
-  double* G = P.scratch.slot_g + sb;
-  double* M = P.scratch.slot_m + sb;
-  uint16_t* SID = P.scratch.slot_id + sb;
-  double* LNEED = P.scratch.ledger_need + nb;
-  uint16_t* LOW = P.scratch.low_fifo + nb;
+  const int warp = threadIdx.x >> 5;
+  const int grp = lane / G;
+  const int sub = lane % G;
+  const unsigned gmask = (G == 32 ? 0xFFFFFFFFu : ((1u << G) - 1u)) << (grp * G);
+  const int rows = P.slot_rows;
+  uint64_t* tile = smem + static_cast<size_t>(warp) * rows * kWarp * 2;
+  Slots<G> S;
+  S.g = reinterpret_cast<double*>(tile);
+  S.m = tile + static_cast<size_t>(rows) * kWarp;
+  S.col0 = grp * G;
+  const int64_t group_id =
+      (static_cast<int64_t>(blockIdx.x) * (kSimBlock / kWarp) + warp) * (kWarp / G) + grp;
+  double* LNEED = P.scratch.ledger_need + group_id * P.wl.nmax;
+  uint16_t* LOW = P.scratch.low_fifo + group_id * P.wl.nmax;
   for (;;) {
-    int ti;
-    {
-      cg::coalesced_group g = cg::coalesced_threads();
-      int base = 0;
-      if (g.thread_rank() == 0) base = atomicAdd(P.next_traj, static_cast<int>(g.size()));
-      base = g.shfl(base, 0);
-      ti = base + static_cast<int>(g.thread_rank());
-    }
+    int ti = 0;
+    if (sub == 0) ti = atomicAdd(P.next_traj, 1);
+    ti = __shfl_sync(gmask, ti, grp * G);
     if (ti >= P.n_traj) break;
-    simulate_one<NW, kTrace, kRecords>(P, ti, G, M, SID, LNEED, LOW);
+    simulate_one<NW, G, kTrace, kRecords>(P, ti, S, sub, gmask, LNEED, LOW);
+    __syncwarp(gmask);
   }
 }
 
@@ -536,56 +598,79 @@ __global__ void __launch_bounds__(128) row_metrics_kernel(const RowMetricsParams
   R->cv = mean == 0.0 ? nan("") : R->ratio_std / mean;
 }
 
-template <int NW>
-int launch_nw(const SimParams& p, bool trace, bool records, int grid, cudaStream_t s) {
-  if (trace)
-    sim_kernel<NW, true, true><<<grid, kBlock, 0, s>>>(p);
-  else if (records)
-    sim_kernel<NW, false, true><<<grid, kBlock, 0, s>>>(p);
-  else
-    sim_kernel<NW, false, false><<<grid, kBlock, 0, s>>>(p);
-  return cudaGetLastError() == cudaSuccess ? 0 : 1;
+template <int NW, int G, bool kTrace, bool kRecords>
+void* kernel_ptr() {
+  return reinterpret_cast<void*>(&sim_kernel<NW, G, kTrace, kRecords>);
+}
+
+using KernelGetter = void* (*)();
+
+template <int NW, int G>
+void* pick_tr(bool trace, bool records) {
+  if (trace) return kernel_ptr<NW, G, true, true>();
+  if (records) return kernel_ptr<NW, G, false, true>();
+  return kernel_ptr<NW, G, false, false>();
 }
 
 template <int NW>
-int occ_nw(int* blocks) {
-  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks, sim_kernel<NW, false, false>,
-                                                       kBlock, 0) == cudaSuccess
-             ? 0
-             : 1;
+void* pick_g(int g, bool trace, bool records) {
+  switch (g) {
+    case 1: return pick_tr<NW, 1>(trace, records);
+    case 2: return pick_tr<NW, 2>(trace, records);
+    case 4: return pick_tr<NW, 4>(trace, records);
+    case 8: return pick_tr<NW, 8>(trace, records);
+  }
+  return nullptr;
+}
+
+void* pick_kernel(int nw, int g, bool trace, bool records) {
+  switch (nw) {
+    case 1: return pick_g<1>(g, trace, records);
+    case 2: return pick_g<2>(g, trace, records);
+    case 4: return pick_g<4>(g, trace, records);
+    case 8: return pick_g<8>(g, trace, records);
+  }
+  return nullptr;
 }
 
 }  // namespace
 
-int sim_occupancy_grid(int nwords, int block, int* grid) {
-  (void)block;
+int plan_sim(int nmax, int group, SimLaunch* out) {
+  SimLaunch l{};
+  l.nwords = nmax <= 64 ? 1 : nmax <= 128 ? 2 : nmax <= 256 ? 4 : 8;
+  l.group = group;
+  l.slot_rows = (nmax + group - 1) / group;
+  l.smem = static_cast<size_t>(kSimBlock / kWarp) * l.slot_rows * kWarp * 16;
+  void* k = pick_kernel(l.nwords, group, false, false);
+  if (!k) return 1;
   int dev = 0, sms = 0, per_sm = 0;
   if (cudaGetDevice(&dev) != cudaSuccess) return 1;
   if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) return 1;
-  int rc = 1;
-  switch (nwords) {
-    case 1: rc = occ_nw<1>(&per_sm); break;
-    case 2: rc = occ_nw<2>(&per_sm); break;
-    case 4: rc = occ_nw<4>(&per_sm); break;
-    case 8: rc = occ_nw<8>(&per_sm); break;
-  }
-  if (rc) return rc;
-  *grid = sms * (per_sm > 0 ? per_sm : 1);
+  for (int tr = 0; tr < 2; ++tr)
+    for (int rec = 0; rec < 2; ++rec) {
+      void* kk = pick_kernel(l.nwords, group, tr != 0, rec != 0);
+      if (cudaFuncSetAttribute(kk, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               static_cast<int>(l.smem)) != cudaSuccess)
+        return 2;
+    }
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, kSimBlock, l.smem) != cudaSuccess)
+    return 1;
+  if (per_sm < 1) return 3;
+  l.grid = sms * per_sm;
+  *out = l;
   return 0;
 }
 
-int launch_sim(const SimParams& p, int nwords, int grid, int block, void* stream) {
-  (void)block;
+int launch_sim(const SimParams& p, const SimLaunch& l, void* stream) {
   const bool trace = p.out.trace != nullptr;
   const bool records = p.out.admit != nullptr || p.out.demoted != nullptr;
-  cudaStream_t s = static_cast<cudaStream_t>(stream);
-  switch (nwords) {
-    case 1: return launch_nw<1>(p, trace, records, grid, s);
-    case 2: return launch_nw<2>(p, trace, records, grid, s);
-    case 4: return launch_nw<4>(p, trace, records, grid, s);
-    case 8: return launch_nw<8>(p, trace, records, grid, s);
-  }
-  return 1;
+  void* k = pick_kernel(l.nwords, l.group, trace, records);
+  if (!k) return 1;
+  void* args[] = {const_cast<SimParams*>(&p)};
+  return cudaLaunchKernel(k, dim3(l.grid), dim3(kSimBlock), args, l.smem,
+                          static_cast<cudaStream_t>(stream)) == cudaSuccess
+             ? 0
+             : 1;
 }
 
 int launch_row_metrics(const RowMetricsParams& p, void* stream) {

@@ -1,14 +1,17 @@
 // summary.cu — sweep summary on the device (simloop.cpp:206-275).
 //
-// S1 (thread per (mix, rps)): per-cell mean goodput over repeats, the static
+// S0 (grid-parallel): ratio[row][q] = (completion - arrival) / sla, NaN when
+//    the request never completed (ratio_to_sla, metrics.cpp:39-47).
+// S1 (warp per (mix, rps)): per-cell mean goodput over repeats, the static
 //    argmax over caps in ascending order with ties to the smaller cap, and the
 //    per-cell latency-ratio means.
-// S2 (block per mix): means over the rps grid, pooled CVs over every ratio of
-//    the chosen cells, and CVs of the per-rps ratio means.
-// Every sum runs sequentially in the reference's order (rows in grid order,
-// ratios in request-id order), so the summary is bit-identical to
-// saber::sweep's.  Ratios are recomputed from completion times exactly like
-// ratio_to_sla (metrics.cpp:39-47).
+// S2 (warp per (mix, variant)): means over the rps grid, pooled CVs over every
+//    ratio of the chosen cells, and CVs of the per-rps ratio means.
+// The reference's sums are sequential left-to-right double additions, so the
+// summary is bit-identical only if the device adds in the same order.  The
+// sums therefore stay sequential, but a whole warp streams the contiguous
+// ratio blocks (coalesced 256-byte loads) and hands the values to the
+// dependent add chain through shuffles, so the chain never waits on memory.
 #include <cuda_runtime.h>
 
 #include <climits>
@@ -20,51 +23,64 @@ namespace saberb200 {
 namespace {
 
 constexpr int kCellScratch = 6;
+constexpr unsigned kFull = 0xFFFFFFFFu;
 
-struct RowView {
-  const double* comp;
-  const double* arr;
-  const double* sla;
-  int n;
-};
-
-__device__ __forceinline__ RowView row_view(const SummaryParams& p, int mi, int ri, int64_t row,
-                                            int rep) {
-  const int64_t w = (static_cast<int64_t>(mi) * p.n_rps + ri) * p.repeats + rep;
-  RowView v;
-  v.comp = p.completion + row * p.wl.nmax;
-  v.arr = p.wl.arrival + w * p.wl.nmax;
-  v.sla = p.wl.sla + w * p.wl.nmax;
-  v.n = p.n;
-  return v;
-}
-
-// Adds this row's ratios (id order) to (sum, count).
-__device__ __forceinline__ void add_ratios(const RowView& v, double& sum, int64_t& cnt) {
-  for (int q = 0; q < v.n; ++q) {
-    const double c = v.comp[q];
-    if (isnan(c)) continue;
-    sum += (c - v.arr[q]) / v.sla[q];
-    ++cnt;
+__global__ void ratios_kernel(const SummaryParams p) {
+  const int64_t total = static_cast<int64_t>(p.n_mixes) * p.n_rps *
+                        (static_cast<int64_t>(p.n_caps) * p.repeats + (p.with_saber ? p.repeats : 0)) *
+                        p.n;
+  const int per_rps = p.n_caps * p.repeats + (p.with_saber ? p.repeats : 0);
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < total;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t row = i / p.n;
+    const int q = static_cast<int>(i % p.n);
+    const int64_t cell = row / per_rps;
+    const int rem = static_cast<int>(row % per_rps);
+    const int rep = rem < p.n_caps * p.repeats ? rem % p.repeats : rem - p.n_caps * p.repeats;
+    const int64_t w = cell * p.repeats + rep;  // workload (mix, rps, seed)
+    const double c = p.completion[row * p.wl.nmax + q];
+    const int64_t o = w * p.wl.nmax + q;
+    p.ratios[i] = isnan(c) ? nan("") : (c - p.wl.arrival[o]) / p.wl.sla[o];
   }
 }
-__device__ __forceinline__ void add_sq(const RowView& v, double mean, double& acc) {
-  for (int q = 0; q < v.n; ++q) {
-    const double c = v.comp[q];
-    if (isnan(c)) continue;
-    const double x = (c - v.arr[q]) / v.sla[q];
-    acc += (x - mean) * (x - mean);
+
+// Sequential sum over `len` contiguous values (NaN = absent), in order.
+__device__ __forceinline__ void warp_seq_sum(const double* v, int64_t len, double& sum,
+                                             int64_t& cnt) {
+  const int lane = threadIdx.x & 31;
+  for (int64_t base = 0; base < len; base += 32) {
+    const double x = base + lane < len ? v[base + lane] : nan("");
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+      const double y = __shfl_sync(kFull, x, j);
+      if (!isnan(y)) {
+        sum += y;
+        ++cnt;
+      }
+    }
+  }
+}
+__device__ __forceinline__ void warp_seq_sq(const double* v, int64_t len, double mean,
+                                            double& acc) {
+  const int lane = threadIdx.x & 31;
+  for (int64_t base = 0; base < len; base += 32) {
+    const double x = base + lane < len ? v[base + lane] : nan("");
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+      const double y = __shfl_sync(kFull, x, j);
+      if (!isnan(y)) acc += (y - mean) * (y - mean);
+    }
   }
 }
 
 __global__ void summary_cells_kernel(const SummaryParams p) {
-  const int cell = blockIdx.x * blockDim.x + threadIdx.x;
+  const int cell = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (cell >= p.n_mixes * p.n_rps) return;
-  const int mi = cell / p.n_rps, ri = cell % p.n_rps;
+  const int lane = threadIdx.x & 31;
   const int R = p.repeats;
   const int per_rps = p.n_caps * R + (p.with_saber ? R : 0);
   const int64_t base = static_cast<int64_t>(cell) * per_rps;
-  double* out = p.scratch + static_cast<int64_t>(cell) * kCellScratch;
+  double out[kCellScratch];
   const double nanv = nan("");
   out[0] = out[1] = out[2] = out[3] = nanv;
   out[4] = out[5] = 0.0;
@@ -98,15 +114,14 @@ __global__ void summary_cells_kernel(const SummaryParams p) {
     int64_t c = 0;
     for (int w = 0; w < p.n_caps; ++w) {
       if (p.caps[w] != best_cap) continue;
-      for (int i = 0; i < R; ++i)
-        add_ratios(row_view(p, mi, ri, base + static_cast<int64_t>(w) * R + i, i), s, c);
+      warp_seq_sum(p.ratios + (base + static_cast<int64_t>(w) * R) * p.n,
+                   static_cast<int64_t>(R) * p.n, s, c);
     }
     if (c > 0) {
       out[3] = s / static_cast<double>(c);
       out[5] = 1.0;
     }
   }
-  p.best_cap[cell] = best_cap;
   if (p.with_saber) {
     const int64_t sb = base + static_cast<int64_t>(p.n_caps) * R;
     double g = 0.0;
@@ -114,11 +129,15 @@ __global__ void summary_cells_kernel(const SummaryParams p) {
     out[0] = g / static_cast<double>(R);
     double s = 0.0;
     int64_t c = 0;
-    for (int i = 0; i < R; ++i) add_ratios(row_view(p, mi, ri, sb + i, i), s, c);
+    warp_seq_sum(p.ratios + sb * p.n, static_cast<int64_t>(R) * p.n, s, c);
     if (c > 0) {
       out[2] = s / static_cast<double>(c);
       out[4] = 1.0;
     }
+  }
+  if (lane == 0) {
+    p.best_cap[cell] = best_cap;
+    for (int k = 0; k < kCellScratch; ++k) p.scratch[static_cast<int64_t>(cell) * kCellScratch + k] = out[k];
   }
 }
 
@@ -144,10 +163,11 @@ __device__ double cv_cells(const double* sc, int n_rps, int col, int flag) {
   return sqrt(var) / mean;
 }
 
+// One warp per (mix, variant); variant 0 = saber, 1 = best static.
 __global__ void summary_mix_kernel(const SummaryParams p) {
   const int mi = blockIdx.x;
-  const int variant = threadIdx.x;  // 0 = saber, 1 = best static
-  if (mi >= p.n_mixes || variant > 1) return;
+  const int variant = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
   __shared__ double means[2];
   const double* sc = p.scratch + static_cast<int64_t>(mi) * p.n_rps * kCellScratch;
   const int R = p.repeats;
@@ -155,6 +175,7 @@ __global__ void summary_mix_kernel(const SummaryParams p) {
   const bool present = variant == 0 ? p.with_saber != 0 : p.n_caps > 0;
   const double nanv = nan("");
   double mean_goodput = nanv, pooled = nanv, rps_cv = nanv;
+  const int64_t block = static_cast<int64_t>(R) * p.n;
   if (present) {
     double s = 0.0;
     for (int ri = 0; ri < p.n_rps; ++ri) s += sc[ri * kCellScratch + (variant == 0 ? 0 : 1)];
@@ -162,37 +183,42 @@ __global__ void summary_mix_kernel(const SummaryParams p) {
     // pooled ratios: rps in grid order, the chosen cell's rows, ids in order
     double sum = 0.0;
     int64_t cnt = 0;
-    for (int pass = 0; pass < 2; ++pass) {
-      const double mean = pass == 0 ? 0.0 : sum / static_cast<double>(cnt);
-      if (pass == 1 && (cnt == 0 || mean == 0.0)) break;
-      double acc = 0.0;
-      for (int ri = 0; ri < p.n_rps; ++ri) {
-        const int64_t base = (static_cast<int64_t>(mi) * p.n_rps + ri) * per_rps;
-        if (variant == 0) {
-          const int64_t sb = base + static_cast<int64_t>(p.n_caps) * R;
-          for (int i = 0; i < R; ++i) {
-            const RowView v = row_view(p, mi, ri, sb + i, i);
-            if (pass == 0) add_ratios(v, sum, cnt);
-            else add_sq(v, mean, acc);
-          }
-        } else {
-          const int bc = p.best_cap[mi * p.n_rps + ri];
-          for (int w = 0; w < p.n_caps; ++w) {
-            if (p.caps[w] != bc) continue;
-            for (int i = 0; i < R; ++i) {
-              const RowView v = row_view(p, mi, ri, base + static_cast<int64_t>(w) * R + i, i);
-              if (pass == 0) add_ratios(v, sum, cnt);
-              else add_sq(v, mean, acc);
-            }
+    for (int ri = 0; ri < p.n_rps; ++ri) {
+      const int64_t base = (static_cast<int64_t>(mi) * p.n_rps + ri) * per_rps;
+      if (variant == 0) {
+        warp_seq_sum(p.ratios + (base + static_cast<int64_t>(p.n_caps) * R) * p.n, block, sum, cnt);
+      } else {
+        const int bc = p.best_cap[mi * p.n_rps + ri];
+        for (int w = 0; w < p.n_caps; ++w)
+          if (p.caps[w] == bc)
+            warp_seq_sum(p.ratios + (base + static_cast<int64_t>(w) * R) * p.n, block, sum, cnt);
+      }
+    }
+    if (cnt > 0) {
+      const double mean = sum / static_cast<double>(cnt);
+      if (mean != 0.0) {
+        double acc = 0.0;
+        for (int ri = 0; ri < p.n_rps; ++ri) {
+          const int64_t base = (static_cast<int64_t>(mi) * p.n_rps + ri) * per_rps;
+          if (variant == 0) {
+            warp_seq_sq(p.ratios + (base + static_cast<int64_t>(p.n_caps) * R) * p.n, block, mean,
+                        acc);
+          } else {
+            const int bc = p.best_cap[mi * p.n_rps + ri];
+            for (int w = 0; w < p.n_caps; ++w)
+              if (p.caps[w] == bc)
+                warp_seq_sq(p.ratios + (base + static_cast<int64_t>(w) * R) * p.n, block, mean,
+                            acc);
           }
         }
+        pooled = sqrt(acc / static_cast<double>(cnt)) / mean;
       }
-      if (pass == 1) pooled = sqrt(acc / static_cast<double>(cnt)) / mean;
     }
     rps_cv = cv_cells(sc, p.n_rps, variant == 0 ? 2 : 3, variant == 0 ? 4 : 5);
   }
-  means[variant] = mean_goodput;
+  if (lane == 0) means[variant] = mean_goodput;
   __syncthreads();
+  if (lane != 0) return;
   saber_mix_summary* out = p.summary + mi;
   if (variant == 0) {
     out->saber_mean_goodput = mean_goodput;
@@ -212,8 +238,9 @@ int launch_summary(const SummaryParams& p, void* stream) {
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const int cells = p.n_mixes * p.n_rps;
   if (cells == 0) return 0;
-  summary_cells_kernel<<<(cells + 63) / 64, 64, 0, s>>>(p);
-  summary_mix_kernel<<<p.n_mixes, 2, 0, s>>>(p);
+  ratios_kernel<<<1184, 256, 0, s>>>(p);
+  summary_cells_kernel<<<(cells * 32 + 127) / 128, 128, 0, s>>>(p);
+  summary_mix_kernel<<<p.n_mixes, 64, 0, s>>>(p);
   return cudaGetLastError() == cudaSuccess ? 0 : 1;
 }
 
