@@ -197,7 +197,8 @@ template <int NW, int G, bool kTrace, bool kRecords>
 __device__ __forceinline__ void simulate_one(const SimParams& P, int ti, const Slots<G>& S,
                                              int sub, unsigned gmask,
                                              double* __restrict__ LNEED,
-                                             uint16_t* __restrict__ LOW) {
+                                             uint16_t* __restrict__ LOW,
+                                             const uint32_t* __restrict__ INV) {
   const TrajDesc d = P.traj[ti];
   const int n = d.n;
   const int nmax = P.wl.nmax;
@@ -232,9 +233,13 @@ __device__ __forceinline__ void simulate_one(const SimParams& P, int ti, const S
   double min_td = kInf;  // lower bound on the earliest possible demotion
   int low_head = 0, low_tail = 0;
 
-  int A = 0;  // |active|
+  int A = 0;         // |active|
+  int npre = 0;      // active slots still in prefill
   double clock = 0.0;
-  double min_pf = kInf, min_rem = kInf;
+  double min_pf = kInf;   // exact min prefill_left over prefill slots
+  double rem_lb = kInf;   // lower bound on min (max_out - generated) over decode slots
+  bool rem_exact = true;  // rem_lb is the exact minimum
+  double m_hi = 0.0;      // >= max_output_tokens of every active slot
 
   int next = 0;
   double na_t = n > 0 ? ARR[0] : kInf;
@@ -254,11 +259,13 @@ __device__ __forceinline__ void simulate_one(const SimParams& P, int ti, const S
     const int s = S.idx(A);
     if (pl == 0.0) {
       S.g[s] = 0.0;  // decode starts at admission
-      min_rem = dmin(min_rem, m - 0.0);
+      rem_lb = dmin(rem_lb, m - 0.0);
     } else {
       S.g[s] = -pl;
       min_pf = dmin(min_pf, pl);
+      ++npre;
     }
+    m_hi = (m_hi < m) ? m : m_hi;
     S.m[s] = dbits(m) | static_cast<uint64_t>(id);
     ++A;
     if (kRecords && ADM && leader) ADM[id] = now;
@@ -316,16 +323,17 @@ __device__ __forceinline__ void simulate_one(const SimParams& P, int ti, const S
           failed = true;
           break;
         }
-#pragma unroll
-        for (int i = kMaxWindow - 1; i >= 1; --i) {
-          if (i < w) {
-            const uint32_t x = draws[draw_pos++];
-            const uint32_t j = x % static_cast<uint32_t>(i + 1);  // rng() % (i+1)
-            const uint64_t a = (ord >> (4 * i)) & 15ull;
-            const uint64_t bb = (ord >> (4 * j)) & 15ull;
-            const uint64_t x2 = a ^ bb;
-            ord ^= (x2 << (4 * i)) | (x2 << (4 * j));
-          }
+        // Fisher-Yates over the window: j = rng() % (i+1) for i = w-1..1.
+        // Draws are stored mod lcm(1..16); x % d is exact via the reciprocal
+        // table (x < 2^20).
+        for (int i = w - 1; i >= 1; --i) {
+          const uint32_t x = draws[draw_pos++];
+          const uint32_t d1 = static_cast<uint32_t>(i + 1);
+          const uint32_t j = x - __umulhi(x, INV[d1]) * d1;
+          const uint64_t a = (ord >> (4 * i)) & 15ull;
+          const uint64_t bb = (ord >> (4 * j)) & 15ull;
+          const uint64_t x2 = a ^ bb;
+          ord ^= (x2 << (4 * i)) | (x2 << (4 * j));
         }
         rng_draws += w - 1;
         const double pred = MT[load + 1];
@@ -390,10 +398,42 @@ __device__ __forceinline__ void simulate_one(const SimParams& P, int ti, const S
       const double speed = GT[A];
       double dt = nt - clock;
       if (min_pf < dt) dt = min_pf;
+      // Quiet pass: no prefill ends (min_pf is exact) and the
+      // lower bound on min(max_out - generated) proves both that the decode
+      // boundary cannot bind and that no slot can satisfy the completion
+      // test.  Every slot then just advances, and the new minima follow from
+      // the scalars: min fl(pl - dt) == fl(min_pf - dt) (monotone rounding).
+      const double sdt0 = speed * dt;
+      const bool quiet = !(min_pf <= dt * kOnePlusTol) &&
+                         rem_lb >= sdt0 * (1.0 + 1e-9) + 1e-15 * (m_hi + sdt0 + 1.0);
+      if (quiet) {
+        const double sdt = sdt0;
+        for (int k = sub, s = S.idx(sub); k < A; k += G, s += kWarp) {
+          const double g = S.g[s];
+          S.g[s] = g < 0.0 ? g + dt : g + sdt;
+        }
+        min_pf = min_pf - dt;  // == min over prefill slots of fl(pl - dt)
+        rem_lb = (rem_lb - sdt) - 1e-15 * (m_hi + sdt + fabs(rem_lb));
+        rem_exact = false;
+        prefill_updates += npre;
+        decode_updates += A - npre;
+        clock = clock + dt;
+        continue;
+      }
+      // Exact pass.  First make the decode minimum exact if it is a bound.
+      if (!rem_exact) {
+        double r = kInf;
+        for (int k = sub, s = S.idx(sub); k < A; k += G, s += kWarp) {
+          const double g = S.g[s];
+          if (g >= 0.0) r = dmin(r, bitsd(S.m[s] & ~kIdMask) - g);
+        }
+        rem_lb = group_min_pos<G>(r, gmask);
+        rem_exact = true;
+      }
       // dt = min(dt, fl(min_rem / speed)); the divide can only bind when
       // min_rem < speed * dt * (1 + 1e-12) (see header).
-      if (min_rem < speed * dt * kOnePlusTol) {
-        const double bnd = min_rem / speed;
+      if (rem_lb < speed * dt * kOnePlusTol) {
+        const double bnd = rem_lb / speed;
         if (bnd < dt) dt = bnd;
       }
       const double group = dt * kOnePlusTol;
@@ -401,21 +441,20 @@ __device__ __forceinline__ void simulate_one(const SimParams& P, int ti, const S
       const double sgd = speed * (group - dt);
       const double nclock = clock + dt;
       double npf = kInf, nrem = kInf;
-      unsigned pf_count = 0, done_count = 0;
-      for (int k = sub; k < A; k += G) {
-        const int s = S.idx(k);
+      unsigned counts = 0;  // (done << 16) | still-in-prefill
+      for (int k = sub, s = S.idx(sub); k < A; k += G, s += kWarp) {
         double g = S.g[s];
         const uint64_t mb = S.m[s];
         const double m = bitsd(mb & ~kIdMask);
         bool done;
         if (g < 0.0) {  // prefill slot: g = -prefill_left
-          ++pf_count;
           if (-g <= group) {
             g = 0.0;  // decode starts at nclock
             done = g + sgd >= m;
           } else {
             g = g + dt;  // == -(prefill_left - dt), exactly
             npf = dmin(npf, -g);
+            ++counts;
             done = false;
           }
         } else {
@@ -428,14 +467,16 @@ __device__ __forceinline__ void simulate_one(const SimParams& P, int ti, const S
         } else {
           S.g[s] = bitsd(kDoneMark);
           COMP[static_cast<int>(mb & kIdMask)] = nclock;
-          ++done_count;
+          counts += 1u << 16;
         }
       }
+      prefill_updates += npre;
+      decode_updates += A - npre;
       min_pf = group_min_pos<G>(npf, gmask);
-      min_rem = group_min_pos<G>(nrem, gmask);
-      prefill_updates += static_cast<int32_t>(group_sum<G>(pf_count, gmask));
-      decode_updates += A;
-      const unsigned ndone = group_sum<G>(done_count, gmask);
+      rem_lb = group_min_pos<G>(nrem, gmask);
+      const unsigned tot = group_sum<G>(counts, gmask);
+      npre = static_cast<int>(tot & 0xFFFFu);
+      const unsigned ndone = tot >> 16;
       if (ndone) {
         // Rare path (once per completion event): every lane replays the
         // completions for the replicated scheduler state, then the leader
@@ -489,7 +530,6 @@ __device__ __forceinline__ void simulate_one(const SimParams& P, int ti, const S
     t = nt;
     if (completed == n) break;
   }
-  decode_updates -= prefill_updates;
 
   if (failed && leader) atomicCAS(P.out.error, kErrNone, kErrRngExhausted);
   if (leader) {
@@ -519,6 +559,10 @@ __device__ __forceinline__ void simulate_one(const SimParams& P, int ti, const S
 template <int NW, int G, bool kTrace, bool kRecords>
 __global__ void __launch_bounds__(kSimBlock) sim_kernel(const SimParams P) {
   extern __shared__ __align__(16) uint64_t smem[];
+  __shared__ uint32_t inv[kMaxWindow + 1];  // ceil(2^32 / d) for d = 2..16
+  if (threadIdx.x >= 2 && threadIdx.x <= kMaxWindow)
+    inv[threadIdx.x] = static_cast<uint32_t>((0x100000000ull + threadIdx.x - 1) / threadIdx.x);
+  __syncthreads();
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
   const int grp = lane / G;
@@ -539,7 +583,7 @@ __global__ void __launch_bounds__(kSimBlock) sim_kernel(const SimParams P) {
     if (sub == 0) ti = atomicAdd(P.next_traj, 1);
     ti = __shfl_sync(gmask, ti, grp * G);
     if (ti >= P.n_traj) break;
-    simulate_one<NW, G, kTrace, kRecords>(P, ti, S, sub, gmask, LNEED, LOW);
+    simulate_one<NW, G, kTrace, kRecords>(P, ti, S, sub, gmask, LNEED, LOW, inv);
     __syncwarp(gmask);
   }
 }

@@ -53,10 +53,9 @@ __device__ __forceinline__ void warp_seq_sum(const double* v, int64_t len, doubl
 #pragma unroll
     for (int j = 0; j < 32; ++j) {
       const double y = __shfl_sync(kFull, x, j);
-      if (!isnan(y)) {
-        sum += y;
-        ++cnt;
-      }
+      const bool ok = !isnan(y);
+      sum += ok ? y : 0.0;  // sum >= +0 and y >= 0: adding +0.0 is exact
+      cnt += ok;
     }
   }
 }
@@ -68,7 +67,8 @@ __device__ __forceinline__ void warp_seq_sq(const double* v, int64_t len, double
 #pragma unroll
     for (int j = 0; j < 32; ++j) {
       const double y = __shfl_sync(kFull, x, j);
-      if (!isnan(y)) acc += (y - mean) * (y - mean);
+      const double d = isnan(y) ? 0.0 : (y - mean) * (y - mean);
+      acc += d;  // acc >= +0: adding +0.0 is exact
     }
   }
 }
