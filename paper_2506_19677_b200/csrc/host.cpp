@@ -266,9 +266,9 @@ int group_size() {
   const char* e = std::getenv("SABER_GROUP");
   if (e) {
     const int g = std::atoi(e);
-    if (g == 1 || g == 2 || g == 4 || g == 8) return g;
+    if (g == 1 || g == 2 || g == 4 || g == 8 || g == 16) return g;
   }
-  return 4;
+  return 8;
 }
 
 struct Scratch {

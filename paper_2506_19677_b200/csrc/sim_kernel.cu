@@ -189,7 +189,10 @@ struct Slots {
   double* g;     // fluid progress (>= 0) or -prefill_left (< 0); kDoneMark when done
   uint64_t* m;   // bits(max_output_tokens) | request id (low 16 bits are free)
   int col0;      // grp * G
-  __device__ __forceinline__ int idx(int k) const { return (k / G) * kWarp + col0 + (k % G); }
+  static_assert((G & (G - 1)) == 0, "G must be a power of two");
+  __device__ __forceinline__ int idx(int k) const {
+    return ((k / G) << 5) + col0 + (k & (G - 1));
+  }
 };
 
 // Simulates trajectory `ti` on this group.
@@ -408,6 +411,7 @@ __device__ __forceinline__ void simulate_one(const SimParams& P, int ti, const S
                          rem_lb >= sdt0 * (1.0 + 1e-9) + 1e-15 * (m_hi + sdt0 + 1.0);
       if (quiet) {
         const double sdt = sdt0;
+#pragma unroll 4
         for (int k = sub, s = S.idx(sub); k < A; k += G, s += kWarp) {
           const double g = S.g[s];
           S.g[s] = g < 0.0 ? g + dt : g + sdt;
@@ -442,6 +446,7 @@ __device__ __forceinline__ void simulate_one(const SimParams& P, int ti, const S
       const double nclock = clock + dt;
       double npf = kInf, nrem = kInf;
       unsigned counts = 0;  // (done << 16) | still-in-prefill
+      int done_k = -1, done_id = -1;  // this lane's last completed slot / request
       for (int k = sub, s = S.idx(sub); k < A; k += G, s += kWarp) {
         double g = S.g[s];
         const uint64_t mb = S.m[s];
@@ -466,7 +471,9 @@ __device__ __forceinline__ void simulate_one(const SimParams& P, int ti, const S
           S.g[s] = g;
         } else {
           S.g[s] = bitsd(kDoneMark);
-          COMP[static_cast<int>(mb & kIdMask)] = nclock;
+          done_id = static_cast<int>(mb & kIdMask);
+          done_k = k;
+          COMP[done_id] = nclock;
           counts += 1u << 16;
         }
       }
@@ -477,9 +484,42 @@ __device__ __forceinline__ void simulate_one(const SimParams& P, int ti, const S
       const unsigned tot = group_sum<G>(counts, gmask);
       npre = static_cast<int>(tot & 0xFFFFu);
       const unsigned ndone = tot >> 16;
-      if (ndone) {
-        // Rare path (once per completion event): every lane replays the
-        // completions for the replicated scheduler state, then the leader
+      if (ndone == 1) {
+        // One completion (the common event): fetch it from its owner lane,
+        // update the replicated ledger, and swap the last slot into its place.
+        unsigned owner = 0;
+        if (G > 1) owner = __ffs(__ballot_sync(gmask, done_k >= 0)) - 1;
+        const int k = G > 1 ? __shfl_sync(gmask, done_k, owner) : done_k;
+        const int id = G > 1 ? __shfl_sync(gmask, done_id, owner) : done_id;
+        if (saber && ledger.test(id)) {
+          ledger.reset(id);
+          --ledger_size;
+          double mx = -kInf;
+          for (int i = 0; i < NW; ++i) {
+            uint64_t b = ledger.word(i);
+            while (b) {
+              const int q = i * 64 + __ffsll(static_cast<long long>(b)) - 1;
+              b &= b - 1;
+              const double v = LNEED[q];
+              mx = (mx < v) ? v : mx;
+            }
+          }
+          ledger_max = mx;
+        }
+        if (k != A - 1) {
+          const int dst = S.idx(k), src = S.idx(A - 1);
+          __syncwarp(gmask);
+          if (leader) {
+            S.g[dst] = S.g[src];
+            S.m[dst] = S.m[src];
+          }
+          __syncwarp(gmask);
+        }
+        A -= 1;
+        completed += 1;
+      } else if (ndone) {
+        // Several completions in one pass (lockstep bursts): every lane
+        // replays them for the replicated scheduler state, then the leader
         // compacts the slot array by swap-with-last.
         __syncwarp(gmask);
         bool dirty = false;
@@ -663,6 +703,7 @@ void* pick_g(int g, bool trace, bool records) {
     case 2: return pick_tr<NW, 2>(trace, records);
     case 4: return pick_tr<NW, 4>(trace, records);
     case 8: return pick_tr<NW, 8>(trace, records);
+    case 16: return pick_tr<NW, 16>(trace, records);
   }
   return nullptr;
 }
@@ -682,9 +723,15 @@ void* pick_kernel(int nw, int g, bool trace, bool records) {
 int plan_sim(int nmax, int group, SimLaunch* out) {
   SimLaunch l{};
   l.nwords = nmax <= 64 ? 1 : nmax <= 128 ? 2 : nmax <= 256 ? 4 : 8;
-  l.group = group;
-  l.slot_rows = (nmax + group - 1) / group;
-  l.smem = static_cast<size_t>(kSimBlock / kWarp) * l.slot_rows * kWarp * 16;
+  // Widen the group until two blocks' slot tiles fit in shared memory.
+  constexpr size_t kTileBudget = 100 * 1024;
+  for (;;) {
+    l.group = group;
+    l.slot_rows = (nmax + group - 1) / group;
+    l.smem = static_cast<size_t>(kSimBlock / kWarp) * l.slot_rows * kWarp * 16;
+    if (l.smem <= kTileBudget || group >= 16) break;
+    group *= 2;
+  }
   void* k = pick_kernel(l.nwords, group, false, false);
   if (!k) return 1;
   int dev = 0, sms = 0, per_sm = 0;

@@ -44,33 +44,50 @@ __global__ void ratios_kernel(const SummaryParams p) {
   }
 }
 
-// Sequential sum over `len` contiguous values (NaN = absent), in order.
+// Sequential sums over `len` contiguous values (NaN = absent), in order.  The
+// warp loads 8 x 32 values per lane-batch and prefetches the next batch while
+// the dependent add chain consumes the current one through shuffles.
+constexpr int kBatch = 8;
+
+template <class F>
+__device__ __forceinline__ void warp_stream(const double* v, int64_t len, F&& consume) {
+  const int lane = threadIdx.x & 31;
+  double cur[kBatch], nxt[kBatch];
+#pragma unroll
+  for (int c = 0; c < kBatch; ++c) {
+    const int64_t i = c * 32 + lane;
+    cur[c] = i < len ? v[i] : nan("");
+  }
+  for (int64_t base = 0; base < len; base += 32 * kBatch) {
+#pragma unroll
+    for (int c = 0; c < kBatch; ++c) {
+      const int64_t i = base + 32 * kBatch + c * 32 + lane;
+      nxt[c] = i < len ? v[i] : nan("");
+    }
+#pragma unroll
+    for (int c = 0; c < kBatch; ++c) {
+#pragma unroll
+      for (int j = 0; j < 32; ++j) consume(__shfl_sync(kFull, cur[c], j));
+    }
+#pragma unroll
+    for (int c = 0; c < kBatch; ++c) cur[c] = nxt[c];
+  }
+}
+
 __device__ __forceinline__ void warp_seq_sum(const double* v, int64_t len, double& sum,
                                              int64_t& cnt) {
-  const int lane = threadIdx.x & 31;
-  for (int64_t base = 0; base < len; base += 32) {
-    const double x = base + lane < len ? v[base + lane] : nan("");
-#pragma unroll
-    for (int j = 0; j < 32; ++j) {
-      const double y = __shfl_sync(kFull, x, j);
-      const bool ok = !isnan(y);
-      sum += ok ? y : 0.0;  // sum >= +0 and y >= 0: adding +0.0 is exact
-      cnt += ok;
-    }
-  }
+  warp_stream(v, len, [&](double y) {
+    const bool ok = !isnan(y);
+    sum += ok ? y : 0.0;  // sum >= +0 and y >= 0: adding +0.0 is exact
+    cnt += ok;
+  });
 }
 __device__ __forceinline__ void warp_seq_sq(const double* v, int64_t len, double mean,
                                             double& acc) {
-  const int lane = threadIdx.x & 31;
-  for (int64_t base = 0; base < len; base += 32) {
-    const double x = base + lane < len ? v[base + lane] : nan("");
-#pragma unroll
-    for (int j = 0; j < 32; ++j) {
-      const double y = __shfl_sync(kFull, x, j);
-      const double d = isnan(y) ? 0.0 : (y - mean) * (y - mean);
-      acc += d;  // acc >= +0: adding +0.0 is exact
-    }
-  }
+  warp_stream(v, len, [&](double y) {
+    const double d = isnan(y) ? 0.0 : (y - mean) * (y - mean);
+    acc += d;  // acc >= +0: adding +0.0 is exact
+  });
 }
 
 __global__ void summary_cells_kernel(const SummaryParams p) {
