@@ -1,0 +1,261 @@
+// saber_cuda_adapter.hpp — the reference-side binding (header only).
+//
+// A SaberSim user includes this next to the reference's own headers and links
+// libsaber_b200.so; the functions below take and return the reference's types
+// (proj/core/include/saber/*.hpp) and throw the reference's exception types,
+// so switching a call site is a namespace change:
+//
+//     saber::sweep(grid, base, jobs)   ->  saber::cuda::sweep(grid, base, jobs)
+//     saber::run(cfg)                  ->  saber::cuda::run(cfg)
+//     saber::run_with_requests(cfg, r) ->  saber::cuda::run_with_requests(cfg, r)
+//
+// Only this header depends on the reference; the engine itself (the C ABI in
+// saber_cuda.h) does not.
+#pragma once
+
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <optional>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "saber/calibration.hpp"
+#include "saber/estimator.hpp"
+#include "saber/metrics.hpp"
+#include "saber/scheduler.hpp"
+#include "saber/simloop.hpp"
+#include "saber/types.hpp"
+#include "saber/workload.hpp"
+#include "saber_cuda.h"
+
+namespace saber::cuda {
+
+namespace detail {
+
+inline const char* kTask[4] = {"code_qna", "code_generation", "code_summary", "code_translation"};
+
+inline int task_index(const std::string& name) {
+  for (int t = 0; t < 4; ++t)
+    if (name == kTask[t]) return t;
+  return SABER_TASK_CUSTOM;
+}
+
+inline void check(saber_status s) {
+  if (s == SABER_OK) return;
+  const std::string msg = saber_cuda_last_error();
+  switch (s) {
+    case SABER_EINVAL: throw std::invalid_argument(msg);
+    case SABER_EDOMAIN: throw std::domain_error(msg);
+    case SABER_EINTERNAL: throw std::logic_error(msg);
+    default: throw std::runtime_error(msg);
+  }
+}
+
+inline saber_model model_of(const SpeedModel& m) {
+  saber_model x{};
+  x.family = static_cast<int32_t>(m.family);
+  for (int k = 0; k < 3; ++k) x.params[k] = m.params[static_cast<size_t>(k)];
+  return x;
+}
+
+inline saber_mix mix_of(const WorkloadMix& m) {
+  saber_mix x{};
+  for (const auto& [name, frac] : m.proportions) {
+    const int t = task_index(name);
+    if (t < 0) throw std::invalid_argument("mix references unknown task: " + name);
+    x.frac[t] = frac;
+    x.present[t] = 1;
+  }
+  return x;
+}
+
+inline saber_traj_spec spec_of(const SimConfig& c) {
+  saber_traj_spec s{};
+  s.mix = mix_of(c.workload.mix);
+  s.rps = c.workload.rps;
+  s.num_requests = c.workload.num_requests;
+  s.workload_seed = c.workload.seed;
+  s.length_jitter = c.workload.length_jitter;
+  s.mode = c.scheduler.mode == SchedulerMode::Saber ? SABER_MODE_SABER : SABER_MODE_STATIC;
+  s.window_size = c.scheduler.window_size;
+  s.tick = c.scheduler.tick;
+  s.static_batch_size = c.scheduler.static_batch_size;
+  s.has_model = c.model.has_value();
+  if (c.model) s.model = model_of(*c.model);
+  s.ground_truth = model_of(c.engine.ground_truth);
+  s.prefill_rate = c.engine.prefill_rate;
+  s.has_horizon = c.horizon.has_value();
+  s.horizon = c.horizon.value_or(0.0);
+  s.seed = c.seed;
+  return s;
+}
+
+inline RunOutput run_one(const SimConfig& cfg, std::vector<Request> requests, bool replay) {
+  saber_traj_spec spec = spec_of(cfg);
+  std::vector<saber_request> rq;
+  if (replay) {
+    if (requests.empty()) throw std::invalid_argument("run: no requests");
+    rq.resize(requests.size());
+    for (size_t i = 0; i < requests.size(); ++i) {
+      if (requests[i].id != i) throw std::invalid_argument("run: request ids must be 0..n-1");
+      rq[i].arrival_time = requests[i].arrival_time;
+      rq[i].sla_seconds = requests[i].sla_seconds;
+      rq[i].deadline = requests[i].deadline;
+      rq[i].input_tokens = requests[i].input_tokens;
+      rq[i].max_output_tokens = requests[i].max_output_tokens;
+      rq[i].task = task_index(requests[i].task);
+    }
+    spec.requests = rq.data();
+    spec.num_requests = static_cast<int32_t>(rq.size());
+  } else {
+    requests = generate(cfg.workload);  // reference generator, for the Request records
+  }
+  const int n = static_cast<int>(requests.size());
+  saber_run_batch_desc d{&spec, 1, 0};
+  saber_traj_row row{};
+  std::vector<double> arr(n), adm(n), comp(n);
+  std::vector<uint8_t> dem(n);
+  const int64_t cap = 1 << 22;
+  std::vector<saber_decision> decs(static_cast<size_t>(cap));
+  int64_t n_dec = 0;
+  saber_run_batch_out o{};
+  o.rows = &row;
+  o.arrival_times = arr.data();
+  o.admit_times = adm.data();
+  o.completion_times = comp.data();
+  o.demoted = dem.data();
+  o.max_n = n;
+  o.decisions = decs.data();
+  o.decision_cap = cap;
+  o.n_decisions = &n_dec;
+  check(saber_cuda_run_batch(&d, &o));
+  RunOutput out;
+  for (int i = 0; i < n; ++i) {
+    Request& r = requests[static_cast<size_t>(i)];
+    if (!std::isnan(adm[i])) r.admit_time = adm[i];
+    if (!std::isnan(comp[i])) {
+      r.completion_time = comp[i];
+      r.generated_tokens = r.max_output_tokens;
+      r.state = RequestState::Completed;
+    } else if (!std::isnan(adm[i])) {
+      r.state = RequestState::Executing;
+    } else {
+      r.state = dem[i] ? RequestState::QueuedLow : RequestState::QueuedHigh;
+    }
+    r.demoted = dem[i] != 0;
+    out.records.push_back(make_record(r));
+  }
+  for (int64_t k = 0; k < n_dec; ++k) {
+    const saber_decision& x = decs[static_cast<size_t>(k)];
+    Decision dd;
+    dd.time = x.time;
+    dd.request_id = x.request_id;
+    dd.kind = static_cast<DecisionKind>(x.kind);
+    dd.load_before = x.load_before;
+    if (x.has_pred) dd.pred_speed = x.pred_speed;
+    if (x.has_req) dd.req_speed = x.req_speed;
+    out.decisions.push_back(dd);
+  }
+  out.metrics = compute_metrics(out.records);
+  out.requests = std::move(requests);
+  return out;
+}
+
+}  // namespace detail
+
+// simloop.hpp:49
+inline RunOutput run(const SimConfig& config) { return detail::run_one(config, {}, false); }
+
+// simloop.hpp:53-54
+inline RunOutput run_with_requests(const SimConfig& config, std::vector<Request> requests) {
+  return detail::run_one(config, std::move(requests), true);
+}
+
+// simloop.hpp:96-99.  `jobs` is accepted for signature parity; the device
+// decides its own parallelism and the output never depends on it.
+inline SweepResult sweep(const SweepGrid& grid, const SimConfig& base, int jobs = 0,
+                         int device = 0) {
+  (void)jobs;
+  std::vector<int32_t> mixes;
+  for (const auto& m : grid.mixes) {
+    if (m != "w1" && m != "w2" && m != "w3")
+      throw std::invalid_argument("unknown mix preset: " + m);
+    mixes.push_back(m[1] - '0');
+  }
+  std::vector<double> rps(grid.rps_list.begin(), grid.rps_list.end());
+  std::vector<int32_t> caps(grid.caps.begin(), grid.caps.end());
+  saber_sweep_desc d{};
+  d.mixes = mixes.data();
+  d.n_mixes = static_cast<int32_t>(mixes.size());
+  d.rps = rps.data();
+  d.n_rps = static_cast<int32_t>(rps.size());
+  d.caps = caps.data();
+  d.n_caps = static_cast<int32_t>(caps.size());
+  d.with_saber = grid.with_saber;
+  d.num_requests = base.workload.num_requests;
+  d.length_jitter = base.workload.length_jitter;
+  d.window_size = base.scheduler.window_size;
+  d.tick = base.scheduler.tick;
+  d.has_model = base.model.has_value();
+  if (base.model) d.model = detail::model_of(*base.model);
+  d.ground_truth = detail::model_of(base.engine.ground_truth);
+  d.prefill_rate = base.engine.prefill_rate;
+  d.has_horizon = base.horizon.has_value();
+  d.horizon = base.horizon.value_or(0.0);
+  d.repeats = base.repeats;
+  d.seed = base.seed;
+  d.device = device;
+  d.shard_index = 0;
+  d.shard_count = 1;
+  const int64_t n_rows = saber_cuda_sweep_rows(&d);
+  std::vector<saber_traj_row> rows(static_cast<size_t>(n_rows > 0 ? n_rows : 0));
+  std::vector<saber_mix_summary> summ(mixes.size());
+  std::vector<int32_t> best(mixes.size() * rps.size());
+  saber_sweep_out o{};
+  o.rows = rows.data();
+  o.summary = summ.data();
+  o.best_cap_by_rps = best.data();
+  detail::check(saber_cuda_sweep(&d, &o));
+  SweepResult res;
+  size_t k = 0;
+  for (const auto& m : grid.mixes)
+    for (const double r : grid.rps_list) {
+      auto push = [&](SchedulerMode mode, int cap, int i) {
+        SweepRow row;
+        row.mix = m;
+        row.rps = r;
+        row.scheduler = mode;
+        row.static_cap = cap;
+        row.repeat_seed = base.seed + static_cast<std::uint64_t>(i);
+        row.goodput = rows[k].goodput;
+        row.ratio_mean = rows[k].ratio_mean;
+        row.ratio_std = rows[k].ratio_std;
+        row.cv = rows[k].cv;
+        res.rows.push_back(row);
+        ++k;
+      };
+      for (const int cap : grid.caps)
+        for (int i = 0; i < base.repeats; ++i) push(SchedulerMode::Static, cap, i);
+      if (grid.with_saber)
+        for (int i = 0; i < base.repeats; ++i) push(SchedulerMode::Saber, 0, i);
+    }
+  for (size_t mi = 0; mi < grid.mixes.size(); ++mi) {
+    MixSummary s;
+    s.saber_mean_goodput = summ[mi].saber_mean_goodput;
+    s.best_static_mean_goodput = summ[mi].best_static_mean_goodput;
+    s.delta = summ[mi].delta;
+    s.saber_pooled_cv = summ[mi].saber_pooled_cv;
+    s.best_static_pooled_cv = summ[mi].best_static_pooled_cv;
+    s.saber_rps_mean_cv = summ[mi].saber_rps_mean_cv;
+    s.best_static_rps_mean_cv = summ[mi].best_static_rps_mean_cv;
+    if (!grid.caps.empty())
+      for (size_t ri = 0; ri < grid.rps_list.size(); ++ri)
+        s.best_cap_by_rps[grid.rps_list[ri]] = best[mi * grid.rps_list.size() + ri];
+    res.summary[grid.mixes[mi]] = s;
+  }
+  return res;
+}
+
+}  // namespace saber::cuda

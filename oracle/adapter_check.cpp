@@ -1,0 +1,104 @@
+// adapter_check.cpp — TEST INFRASTRUCTURE ONLY.
+//
+// Drives the reference's own API and the drop-in adapter
+// (include/saber_cuda_adapter.hpp -> libsaber_b200.so) on the same inputs and
+// compares the results field by field:
+//   saber::sweep(grid, base)      vs saber::cuda::sweep(grid, base)
+//   saber::run(cfg)               vs saber::cuda::run(cfg)
+//   saber::run_with_requests(...) vs saber::cuda::run_with_requests(...)
+// Built by oracle/Makefile into oracle/_ref/adapter_check (it links the
+// compiled reference); tests/test_adapter.py runs it.
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <exception>
+#include <string>
+
+#include "saber_cuda_adapter.hpp"
+
+namespace {
+
+int failures = 0;
+
+bool same(double a, double b) { return (std::isnan(a) && std::isnan(b)) || a == b; }
+
+void expect(bool ok, const std::string& what) {
+  if (!ok) {
+    ++failures;
+    std::printf("MISMATCH %s\n", what.c_str());
+  }
+}
+
+saber::SpeedModel calibrated_usl() {
+  return {saber::ModelFamily::Usl,
+          {99.999999999997357, 0.049999999999992085, 0.0010000000000001078}, {}};
+}
+
+void compare_runs(const saber::RunOutput& a, const saber::RunOutput& b, const std::string& tag) {
+  expect(a.decisions.size() == b.decisions.size(), tag + " decision count");
+  for (size_t i = 0; i < a.decisions.size() && i < b.decisions.size(); ++i) {
+    const auto& x = a.decisions[i];
+    const auto& y = b.decisions[i];
+    const bool ok = x.time == y.time && x.request_id == y.request_id && x.kind == y.kind &&
+                    x.load_before == y.load_before && x.pred_speed == y.pred_speed &&
+                    x.req_speed == y.req_speed;
+    if (!ok) {
+      expect(false, tag + " decision " + std::to_string(i));
+      break;
+    }
+  }
+  expect(saber::decisions_to_csv(a.decisions) == saber::decisions_to_csv(b.decisions),
+         tag + " decisions.csv");
+  expect(saber::records_to_csv(a.records) == saber::records_to_csv(b.records), tag + " records.csv");
+  expect(saber::to_json(a.metrics) == saber::to_json(b.metrics), tag + " metrics.json");
+}
+
+}  // namespace
+
+int main() {
+  try {
+    // BASELINE config 1 through run().
+    saber::SimConfig cfg;
+    cfg.workload.mix = saber::preset_mix("w1");
+    cfg.workload.rps = 4.0;
+    cfg.workload.num_requests = 100;
+    cfg.workload.seed = 42;
+    cfg.seed = 42;
+    cfg.model = calibrated_usl();
+    compare_runs(saber::run(cfg), saber::cuda::run(cfg), "config1");
+
+    // A static trajectory and a replayed workload.
+    saber::SimConfig st = cfg;
+    st.scheduler.mode = saber::SchedulerMode::Static;
+    st.scheduler.static_batch_size = 30;
+    st.model.reset();
+    st.workload.mix = saber::preset_mix("w3");
+    st.workload.rps = 8.0;
+    compare_runs(saber::run(st), saber::cuda::run(st), "static");
+    auto reqs = saber::generate(cfg.workload);
+    compare_runs(saber::run_with_requests(cfg, reqs), saber::cuda::run_with_requests(cfg, reqs),
+                 "replay");
+
+    // A config-2 shaped sweep.
+    saber::SweepGrid grid;
+    grid.mixes = {"w1", "w2", "w3"};
+    grid.rps_list = {2.0, 9.0, 20.0};
+    grid.caps = {10, 40, 70};
+    grid.with_saber = true;
+    saber::SimConfig base;
+    base.workload.num_requests = 60;
+    base.model = calibrated_usl();
+    base.repeats = 3;
+    base.seed = 7;
+    const saber::SweepResult a = saber::sweep(grid, base, 0);
+    const saber::SweepResult b = saber::cuda::sweep(grid, base, 0);
+    expect(saber::results_to_csv(a.rows) == saber::results_to_csv(b.rows), "sweep results.csv");
+    expect(saber::summary_to_json(a) == saber::summary_to_json(b), "sweep summary.json");
+  } catch (const std::exception& e) {
+    std::printf("EXCEPTION %s\n", e.what());
+    return 2;
+  }
+  if (failures) return 1;
+  std::printf("ADAPTER OK\n");
+  return 0;
+}
