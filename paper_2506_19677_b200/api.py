@@ -594,3 +594,102 @@ def fp64_peak_tflops(device: int = 0) -> float:
     v = C.c_double()
     _check(N.lib().saber_cuda_fp64_peak(device, C.byref(v)))
     return v.value
+
+
+# ------------------------------------------------------------------ fitting
+@dataclass
+class LoadSpeedSample:
+    load: int
+    speed: float
+
+
+@dataclass
+class FamilyFit:
+    family: int
+    ok: bool
+    model: Optional[SpeedModel]
+    error: str = ""
+
+
+@dataclass
+class CalibrationReport:
+    best: SpeedModel
+    fits: List[FamilyFit]
+
+
+@dataclass
+class FitBatchResult:
+    params: np.ndarray       # [3 families][n_curves][3]
+    r2: np.ndarray           # [3][n_curves] fit_r2, or FitError best_sse
+    status: np.ndarray       # [3][n_curves] 0 ok, 1 FitError, -1 not fitted
+    best_family: Optional[np.ndarray]  # [n_curves] (calibrate): -2 too few loads, -1 none
+    iterations: np.ndarray   # [3][n_curves] LM iterations over the 5 starts
+    device_ms: float
+    kernel_launches: int
+
+
+def fit_batch(loads, speeds, offsets, family_mask: int = 0x7, calibrate: bool = False,
+              device: int = 0) -> FitBatchResult:
+    """Many independent fit()/calibrate() calls in one launch (SoA curves:
+    curve c owns samples [offsets[c], offsets[c+1]))."""
+    loads = np.ascontiguousarray(loads, dtype=np.int32)
+    speeds = np.ascontiguousarray(speeds, dtype=np.float64)
+    offsets = np.ascontiguousarray(offsets, dtype=np.int64)
+    n = len(offsets) - 1
+    params = np.zeros((3, n, 3))
+    r2 = np.zeros((3, n))
+    status = np.zeros((3, n), dtype=np.int32)
+    best = np.zeros(n, dtype=np.int32) if calibrate else None
+    iters = np.zeros((3, n), dtype=np.int32)
+    d = N.saber_fit_desc()
+    P = C.POINTER
+    d.loads = loads.ctypes.data_as(P(C.c_int32))
+    d.speeds = speeds.ctypes.data_as(P(C.c_double))
+    d.offsets = offsets.ctypes.data_as(P(C.c_int64))
+    d.n_curves = n
+    d.family_mask = family_mask
+    d.calibrate = 1 if calibrate else 0
+    d.device = device
+    o = N.saber_fit_out()
+    o.params = params.ctypes.data_as(P(C.c_double))
+    o.r2 = r2.ctypes.data_as(P(C.c_double))
+    o.status = status.ctypes.data_as(P(C.c_int32))
+    if calibrate:
+        o.best_family = best.ctypes.data_as(P(C.c_int32))
+    o.iterations = iters.ctypes.data_as(P(C.c_int32))
+    _check(N.lib().saber_cuda_fit_batch(C.byref(d), C.byref(o)))
+    return FitBatchResult(params, r2, status, best, iters, o.device_ms, o.kernel_launches)
+
+
+def _samples_arrays(samples):
+    loads = np.array([s.load if isinstance(s, LoadSpeedSample) else s[0] for s in samples], np.int32)
+    speeds = np.array([s.speed if isinstance(s, LoadSpeedSample) else s[1] for s in samples], np.float64)
+    return loads, speeds
+
+
+def fit(samples, family: int, device: int = 0) -> SpeedModel:
+    """estimator.cpp:241-346 on the GPU; raises FitError like the reference."""
+    loads, speeds = _samples_arrays(samples)
+    res = fit_batch(loads, speeds, [0, len(loads)], family_mask=1 << family, device=device)
+    p = res.params[family, 0]
+    if res.status[family, 0] != 0:
+        raise FitError(f"fit failed for {FAMILIES[family]}", family, p, res.r2[family, 0])
+    return SpeedModel(family, tuple(float(x) for x in p), float(res.r2[family, 0]))
+
+
+def calibrate(samples, device: int = 0) -> CalibrationReport:
+    """calibration.cpp:137-168 on the GPU."""
+    loads, speeds = _samples_arrays(samples)
+    res = fit_batch(loads, speeds, [0, len(loads)], calibrate=True, device=device)
+    b = int(res.best_family[0])
+    if b == -2:
+        raise CalibrationError("calibrate: insufficient distinct loads")
+    if b == -1:
+        raise CalibrationError("calibrate: no model family produced a fit")
+    fits = []
+    for f in range(3):
+        ok = res.status[f, 0] == 0
+        fits.append(FamilyFit(f, bool(ok), SpeedModel(f, tuple(float(x) for x in res.params[f, 0]),
+                                                      float(res.r2[f, 0])) if ok else None,
+                              "" if ok else f"fit failed for {FAMILIES[f]}"))
+    return CalibrationReport(fits[b].model, fits)

@@ -1096,7 +1096,80 @@ extern "C" saber_status saber_cuda_fp64_peak(int32_t device, double* tflops) {
 }
 
 extern "C" saber_status saber_cuda_fit_batch(const saber_fit_desc* desc, saber_fit_out* out) {
-  (void)desc;
-  (void)out;
-  return fail(SABER_EINTERNAL, "fit_batch: not built yet");
+  if (!desc || !out) return fail(SABER_EINVAL, "null argument");
+  const int N = desc->n_curves;
+  if (N < 1) return fail(SABER_EINVAL, "fit_batch: no curves");
+  if (!desc->loads || !desc->speeds || !desc->offsets)
+    return fail(SABER_EINVAL, "fit_batch: loads, speeds and offsets are required");
+  if (!out->params || !out->r2 || !out->status)
+    return fail(SABER_EINVAL, "fit_batch: params, r2 and status outputs are required");
+  if (desc->calibrate && !out->best_family)
+    return fail(SABER_EINVAL, "fit_batch: calibrate needs best_family");
+  int mask = desc->family_mask & 7;
+  if (desc->calibrate) mask = 7;  // calibrate() fits all three families
+  if (mask == 0) return fail(SABER_EINVAL, "fit_batch: empty family mask");
+  if (desc->offsets[0] != 0) return fail(SABER_EINVAL, "fit_batch: offsets[0] must be 0");
+  for (int c = 0; c < N; ++c)
+    if (desc->offsets[c + 1] < desc->offsets[c])
+      return fail(SABER_EINVAL, "fit_batch: offsets must be non-decreasing");
+  const int64_t M = desc->offsets[N];
+  for (int64_t i = 0; i < M; ++i)
+    if (desc->loads[i] < 1) return fail(SABER_EDOMAIN, "predict: load must be >= 1");
+  if (saber_status s = use_device(desc->device)) return s;
+  const int dev = desc->device;
+  DevBuf loads, speeds, offs, scratch, conv, iters, params, r2, status, best, itc, cursor;
+  ALLOC_TRY(loads, dev, static_cast<size_t>(std::max<int64_t>(1, M)) * 4);
+  ALLOC_TRY(speeds, dev, static_cast<size_t>(std::max<int64_t>(1, M)) * 8);
+  ALLOC_TRY(offs, dev, static_cast<size_t>(N + 1) * 8);
+  ALLOC_TRY(scratch, dev, static_cast<size_t>(2) * N * 5 * 4 * 8);
+  ALLOC_TRY(conv, dev, static_cast<size_t>(2) * N * 5 * 4);
+  ALLOC_TRY(iters, dev, static_cast<size_t>(2) * N * 5 * 4);
+  ALLOC_TRY(params, dev, static_cast<size_t>(3) * N * 3 * 8);
+  ALLOC_TRY(r2, dev, static_cast<size_t>(3) * N * 8);
+  ALLOC_TRY(status, dev, static_cast<size_t>(3) * N * 4);
+  ALLOC_TRY(best, dev, static_cast<size_t>(N) * 4);
+  ALLOC_TRY(itc, dev, static_cast<size_t>(3) * N * 4);
+  ALLOC_TRY(cursor, dev, 16);
+  Timer tm;
+  if (saber_status s = tm.init()) return s;
+  cudaStream_t st = nullptr;
+  CUDA_TRY(cudaEventRecord(tm.a, st));
+  if (M > 0) {
+    CUDA_TRY(cudaMemcpyAsync(loads.p, desc->loads, static_cast<size_t>(M) * 4, cudaMemcpyHostToDevice, st));
+    CUDA_TRY(cudaMemcpyAsync(speeds.p, desc->speeds, static_cast<size_t>(M) * 8, cudaMemcpyHostToDevice, st));
+  }
+  CUDA_TRY(cudaMemcpyAsync(offs.p, desc->offsets, static_cast<size_t>(N + 1) * 8, cudaMemcpyHostToDevice, st));
+  CUDA_TRY(cudaMemsetAsync(cursor.p, 0, 16, st));
+  FitParams fp{};
+  fp.loads = loads.as<int32_t>();
+  fp.speeds = speeds.as<double>();
+  fp.offsets = offs.as<int64_t>();
+  fp.n_curves = N;
+  fp.family_mask = mask;
+  fp.calibrate = desc->calibrate;
+  fp.params = params.as<double>();
+  fp.r2 = r2.as<double>();
+  fp.status = status.as<int32_t>();
+  fp.best_family = best.as<int32_t>();
+  fp.iterations = itc.as<int32_t>();
+  fp.lm_scratch = scratch.as<double>();
+  fp.lm_conv = conv.as<int32_t>();
+  fp.lm_iters = iters.as<int32_t>();
+  fp.cursor = cursor.as<int32_t>();
+  int launches = 0;
+  LAUNCH_TRY(launch_fit(fp, st, &launches));
+  CUDA_TRY(cudaMemcpyAsync(out->params, params.p, static_cast<size_t>(3) * N * 3 * 8, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaMemcpyAsync(out->r2, r2.p, static_cast<size_t>(3) * N * 8, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaMemcpyAsync(out->status, status.p, static_cast<size_t>(3) * N * 4, cudaMemcpyDeviceToHost, st));
+  if (desc->calibrate)
+    CUDA_TRY(cudaMemcpyAsync(out->best_family, best.p, static_cast<size_t>(N) * 4, cudaMemcpyDeviceToHost, st));
+  if (out->iterations)
+    CUDA_TRY(cudaMemcpyAsync(out->iterations, itc.p, static_cast<size_t>(3) * N * 4, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaEventRecord(tm.b, st));
+  CUDA_TRY(cudaEventSynchronize(tm.b));
+  float ms = 0.f;
+  CUDA_TRY(cudaEventElapsedTime(&ms, tm.a, tm.b));
+  out->device_ms = ms;
+  out->kernel_launches = launches;
+  return SABER_OK;
 }
