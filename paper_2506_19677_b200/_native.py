@@ -11,7 +11,7 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libsaber_b200.so")
+LIB_PATH = os.environ.get("SABER_LIB", os.path.join(HERE, "libsaber_b200.so"))
 
 SABER_OK, SABER_EINVAL, SABER_EDOMAIN, SABER_EFIT, SABER_ECUDA, SABER_ECAPACITY, SABER_EINTERNAL = range(7)
 STATUS_NAMES = ["SABER_OK", "SABER_EINVAL", "SABER_EDOMAIN", "SABER_EFIT", "SABER_ECUDA",

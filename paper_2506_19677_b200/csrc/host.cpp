@@ -275,13 +275,21 @@ struct Scratch {
   DevBuf ledger, low;
   SimLaunch launch{};
   GroupScratch view{};
-  saber_status alloc(int device, int nmax) {
-    const int rc = plan_sim(nmax, group_size(), &launch);
+  // Kernel choice: the G-lane group kernel; SABER_KERNEL=lane
+  // selects the lane-per-trajectory lockstep kernel when the trajectory fits
+  // it (n <= 128, max_output_tokens < 2^23).  Measured slower on config 2
+  // (DESIGN.md §4), kept as a parity-tested alternative.
+  saber_status alloc(int device, int nmax, bool lane_ok = true) {
+    const char* e = std::getenv("SABER_KERNEL");
+    const bool lane = lane_ok && nmax <= kLaneMaxRequests && e && std::string(e) == "lane";
+    int rc = lane ? plan_sim_lane(nmax, &launch) : plan_sim(nmax, group_size(), &launch);
+    if (rc != 0 && lane) rc = plan_sim(nmax, group_size(), &launch);
     if (rc != 0)
       return fail(SABER_ECUDA, "trajectory kernel configuration failed (" + std::to_string(rc) +
                                    "): " + cudaGetErrorString(cudaGetLastError()));
-    const int64_t groups =
-        static_cast<int64_t>(launch.grid) * (kSimBlock / kWarp) * (kWarp / launch.group);
+    const int64_t groups = launch.lane ? static_cast<int64_t>(launch.grid) * launch.block
+                                       : static_cast<int64_t>(launch.grid) * (kSimBlock / kWarp) *
+                                             (kWarp / launch.group);
     const size_t per = static_cast<size_t>(nmax);
     ALLOC_TRY(ledger, device, static_cast<size_t>(groups) * per * sizeof(double));
     ALLOC_TRY(low, device, static_cast<size_t>(groups) * per * sizeof(uint16_t));
@@ -955,7 +963,10 @@ extern "C" saber_status saber_cuda_run_batch(const saber_run_batch_desc* desc,
     ALLOC_TRY(len_d, dev, len.size() * 8);
     ALLOC_TRY(draws_d, dev, static_cast<size_t>(std::max<int64_t>(1, total_draws)) * 4);
   }
-  if (saber_status s = scratch.alloc(dev, nmax)) return s;
+  bool lane_ok = true;
+  for (size_t i = 0; i < cells; ++i)
+    if (!(mo[i] <= kLaneMaxOutput)) lane_ok = false;
+  if (saber_status s = scratch.alloc(dev, nmax, lane_ok)) return s;
 
   CUDA_TRY(cudaMemcpy(wl.items.p, items.data(), items.size() * sizeof(WorkloadItem), cudaMemcpyHostToDevice));
   CUDA_TRY(cudaMemcpy(wl.seed_base.p, base.data(), base.size() * 8, cudaMemcpyHostToDevice));

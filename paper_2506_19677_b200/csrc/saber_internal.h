@@ -106,13 +106,20 @@ enum : int32_t {
 struct SimLaunch {
   int nwords;     // 64-bit mask words (n <= 64 * nwords)
   int group;      // lanes per trajectory
+  int lane;       // 1 = lane-per-trajectory lockstep kernel (sim_lane.cu)
+  int block;      // threads per block
   int grid;       // persistent blocks
-  int slot_rows;  // ceil(nmax / group)
+  int slot_rows;  // group kernel: ceil(nmax / group); lane kernel: nmax
   size_t smem;    // dynamic shared memory per block
 };
 constexpr int kSimBlock = 128;
 int plan_sim(int nmax, int group, SimLaunch* out);
 int launch_sim(const SimParams& p, const SimLaunch& l, void* stream);
+// Lane-per-trajectory lockstep kernel: n <= 128, max_output_tokens < 2^23.
+constexpr int kLaneMaxRequests = 128;
+constexpr double kLaneMaxOutput = 8388607.0;
+int plan_sim_lane(int nmax, SimLaunch* out);
+int launch_sim_lane(const SimParams& p, const SimLaunch& l, void* stream);
 
 struct RngGenParams {
   const uint64_t* seeds;  // [n_streams] already xor-salted

@@ -34,152 +34,17 @@
 #include <cstdint>
 
 #include "saber_internal.h"
+#include "sim_common.cuh"
 
 namespace saberb200 {
 namespace {
 
-constexpr double kInf = __builtin_huge_val();
-constexpr double kOnePlusTol = 1.0 + 1e-12;  // engine.cpp:17,76 (kGroupTol)
-constexpr uint64_t kHashSeed = 0x243F6A8885A308D3ULL;
-constexpr uint64_t kAbsent = 0xFFF8000000000001ULL;
-constexpr uint64_t kDoneMark = 0xFFF0DEAD0000DEADULL;  // a NaN the engine never produces
-constexpr uint64_t kIdMask = 0xFFFFull;
+using namespace simdev;
 
-__device__ __forceinline__ uint64_t hstep(uint64_t h, uint64_t x) {
-  h ^= x;
-  h *= 0x9E3779B97F4A7C15ULL;
-  h ^= h >> 32;
-  return h;
-}
-__device__ __forceinline__ uint64_t rotl64(uint64_t x, int r) {
-  return (x << r) | (x >> (64 - r));
-}
-__device__ __forceinline__ uint64_t dbits(double v) {
-  return static_cast<uint64_t>(__double_as_longlong(v));
-}
-__device__ __forceinline__ double bitsd(uint64_t b) {
-  return __longlong_as_double(static_cast<long long>(b));
-}
-__device__ __forceinline__ double dmin(double a, double b) { return (b < a) ? b : a; }
+#ifndef SABER_SIM_MIN_BLOCKS
+#define SABER_SIM_MIN_BLOCKS 4
+#endif
 
-// required_speed (types.cpp:82-88) for a queued request: generated == 0.
-__device__ __forceinline__ double queued_need(double max_out, double deadline,
-                                              double now) {
-  if (now >= deadline) return kInf;
-  const double remaining = max_out - 0.0;
-  if (remaining <= 0.0) return 0.0;
-  return remaining / (deadline - now);
-}
-
-// Group minimum of a non-negative double (IEEE order == unsigned bit order).
-template <int G>
-__device__ __forceinline__ double group_min_pos(double v, unsigned gmask) {
-  if (G == 1) return v;
-  const uint64_t b = dbits(v);
-  const unsigned hi = static_cast<unsigned>(b >> 32);
-  const unsigned lo = static_cast<unsigned>(b);
-  const unsigned mhi = __reduce_min_sync(gmask, hi);
-  const unsigned mlo = __reduce_min_sync(gmask, hi == mhi ? lo : 0xFFFFFFFFu);
-  return bitsd((static_cast<uint64_t>(mhi) << 32) | mlo);
-}
-template <int G>
-__device__ __forceinline__ unsigned group_sum(unsigned v, unsigned gmask) {
-  if (G == 1) return v;
-  return __reduce_add_sync(gmask, v);
-}
-
-// Per-request tier membership as an NW x 64-bit register bitmask.  Built as a
-// recursive struct of scalar words (no array), so a runtime word index can
-// never turn into a local-memory access.
-template <int NW, int B = 0>
-struct Mask {
-  uint64_t w;
-  Mask<NW - 1, B + 1> r;
-  __device__ __forceinline__ void clear() { w = 0; r.clear(); }
-  __device__ __forceinline__ void set(int id) {
-    if ((id >> 6) == B) w |= 1ull << (id & 63);
-    else r.set(id);
-  }
-  __device__ __forceinline__ void reset(int id) {
-    if ((id >> 6) == B) w &= ~(1ull << (id & 63));
-    else r.reset(id);
-  }
-  __device__ __forceinline__ bool test(int id) const {
-    return (id >> 6) == B ? ((w >> (id & 63)) & 1ull) != 0 : r.test(id);
-  }
-  __device__ __forceinline__ uint64_t word(int i) const { return i == B ? w : r.word(i); }
-  __device__ __forceinline__ void andnot(int i, uint64_t m) {
-    if (i == B) w &= ~m;
-    else r.andnot(i, m);
-  }
-  __device__ __forceinline__ bool any() const { return w != 0 || r.any(); }
-  __device__ __forceinline__ int count() const { return __popcll(w) + r.count(); }
-  __device__ __forceinline__ int lowest() const {
-    return w ? B * 64 + __ffsll(static_cast<long long>(w)) - 1 : r.lowest();
-  }
-  // k-th set bit in ascending id order (0-based); k < count().
-  __device__ __forceinline__ int select(int k) const {
-    const int c = __popcll(w);
-    if (k < c) {
-      uint64_t x = w;
-      for (int j = 0; j < k; ++j) x &= x - 1;
-      return B * 64 + __ffsll(static_cast<long long>(x)) - 1;
-    }
-    return r.select(k - c);
-  }
-};
-template <int B>
-struct Mask<0, B> {
-  __device__ __forceinline__ void clear() {}
-  __device__ __forceinline__ void set(int) {}
-  __device__ __forceinline__ void reset(int) {}
-  __device__ __forceinline__ bool test(int) const { return false; }
-  __device__ __forceinline__ uint64_t word(int) const { return 0; }
-  __device__ __forceinline__ void andnot(int, uint64_t) {}
-  __device__ __forceinline__ bool any() const { return false; }
-  __device__ __forceinline__ int count() const { return 0; }
-  __device__ __forceinline__ int lowest() const { return -1; }
-  __device__ __forceinline__ int select(int) const { return -1; }
-};
-
-struct DecisionLog {
-  uint64_t h;
-  int32_t n;
-  int32_t k0, k1, k2, k3, k4;
-};
-
-template <bool kTrace>
-__device__ __forceinline__ void push_decision(DecisionLog& L, double t, int id,
-                                              int kind, int load, uint64_t pb,
-                                              uint64_t rb, saber_decision* tr,
-                                              int64_t cap, int32_t* err, bool writer) {
-  const uint64_t w = static_cast<uint64_t>(static_cast<uint32_t>(id)) |
-                     (static_cast<uint64_t>(kind) << 32) |
-                     (static_cast<uint64_t>(static_cast<uint32_t>(load)) << 40);
-  L.h = hstep(L.h, dbits(t));
-  L.h = hstep(L.h, w ^ rotl64(pb, 17) ^ rotl64(rb, 43));
-  if (kTrace && tr != nullptr && writer) {
-    if (L.n < cap) {
-      saber_decision& d = tr[L.n];
-      d.time = t;
-      d.request_id = static_cast<uint64_t>(id);
-      d.kind = kind;
-      d.load_before = load;
-      d.has_pred = pb != kAbsent;
-      d.has_req = rb != kAbsent;
-      d.pred_speed = pb != kAbsent ? bitsd(pb) : nan("");
-      d.req_speed = rb != kAbsent ? bitsd(rb) : nan("");
-    } else {
-      atomicCAS(err, kErrNone, kErrTraceOverflow);
-    }
-  }
-  ++L.n;
-  L.k0 += kind == 0;
-  L.k1 += kind == 1;
-  L.k2 += kind == 2;
-  L.k3 += kind == 3;
-  L.k4 += kind == 4;
-}
 
 // Shared-memory slot arrays of one group: slot k lives at row k / G, column
 // grp * G + k % G of the warp's [rows][32] tile (so lane k % G of the group
@@ -597,7 +462,7 @@ __device__ __forceinline__ void simulate_one(const SimParams& P, int ti, const S
 }
 
 template <int NW, int G, bool kTrace, bool kRecords>
-__global__ void __launch_bounds__(kSimBlock) sim_kernel(const SimParams P) {
+__global__ void __launch_bounds__(kSimBlock, SABER_SIM_MIN_BLOCKS) sim_kernel(const SimParams P) {
   extern __shared__ __align__(16) uint64_t smem[];
   __shared__ uint32_t inv[kMaxWindow + 1];  // ceil(2^32 / d) for d = 2..16
   if (threadIdx.x >= 2 && threadIdx.x <= kMaxWindow)
@@ -748,11 +613,14 @@ int plan_sim(int nmax, int group, SimLaunch* out) {
     return 1;
   if (per_sm < 1) return 3;
   l.grid = sms * per_sm;
+  l.lane = 0;
+  l.block = kSimBlock;
   *out = l;
   return 0;
 }
 
 int launch_sim(const SimParams& p, const SimLaunch& l, void* stream) {
+  if (l.lane) return launch_sim_lane(p, l, stream);
   const bool trace = p.out.trace != nullptr;
   const bool records = p.out.admit != nullptr || p.out.demoted != nullptr;
   void* k = pick_kernel(l.nwords, l.group, trace, records);
