@@ -180,73 +180,147 @@ __device__ double cv_cells(const double* sc, int n_rps, int col, int flag) {
   return sqrt(var) / mean;
 }
 
-// One warp per (mix, variant); variant 0 = saber, 1 = best static.
-__global__ void summary_mix_kernel(const SummaryParams p) {
-  const int mi = blockIdx.x;
-  const int variant = threadIdx.x >> 5;
-  const int lane = threadIdx.x & 31;
-  __shared__ double means[2];
+// Pooled sequential sums for one (mix, variant): a 2-warp block.  Warp 1
+// streams the pooled ratio blocks (rps in grid order, the chosen cell's rows,
+// request ids in order) into a double-buffered shared ring; lane 0 of warp 0
+// runs the reference's left-to-right add chain over it, so the chain (8-cycle
+// DADD latency) never waits on memory.  Pass 1 sums, pass 2 sums squares of
+// deviations from the pass-1 mean (cv(), metrics.cpp:49-59).
+constexpr int kChunk = 1024;
+
+// Walks the pooled sequence lazily: segment = the contiguous ratio block
+// (R rows x n requests) of the chosen cell at each rps, in grid order.
+struct SegmentWalk {
+  int ri = 0, wi = -1;
+  __device__ bool next(const SummaryParams& p, int mi, int variant, const double** ptr,
+                       int64_t* len) {
+    const int R = p.repeats;
+    const int per_rps = p.n_caps * R + (p.with_saber ? R : 0);
+    while (ri < p.n_rps) {
+      const int64_t base = (static_cast<int64_t>(mi) * p.n_rps + ri) * per_rps;
+      if (variant == 0) {
+        if (wi < 0) {
+          wi = 0;
+          *ptr = p.ratios + (base + static_cast<int64_t>(p.n_caps) * R) * p.n;
+          *len = static_cast<int64_t>(R) * p.n;
+          return true;
+        }
+      } else {
+        const int bc = p.best_cap[mi * p.n_rps + ri];
+        for (++wi; wi < p.n_caps; ++wi)
+          if (p.caps[wi] == bc) {
+            *ptr = p.ratios + (base + static_cast<int64_t>(wi) * R) * p.n;
+            *len = static_cast<int64_t>(R) * p.n;
+            return true;
+          }
+      }
+      ++ri;
+      wi = -1;
+    }
+    return false;
+  }
+};
+
+__device__ int64_t pool_length(const SummaryParams& p, int mi, int variant) {
+  SegmentWalk w;
+  const double* ptr;
+  int64_t len, total = 0;
+  while (w.next(p, mi, variant, &ptr, &len)) total += len;
+  return total;
+}
+
+__global__ void __launch_bounds__(64) summary_mix_kernel(const SummaryParams p) {
+  const int mi = blockIdx.x >> 1;
+  const int variant = blockIdx.x & 1;  // 0 = saber, 1 = best static
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  __shared__ double ring[2][kChunk];
+  __shared__ double s_out[3];
   const double* sc = p.scratch + static_cast<int64_t>(mi) * p.n_rps * kCellScratch;
-  const int R = p.repeats;
-  const int per_rps = p.n_caps * R + (p.with_saber ? R : 0);
   const bool present = variant == 0 ? p.with_saber != 0 : p.n_caps > 0;
+  const int64_t total = present ? pool_length(p, mi, variant) : 0;
+  const int chunks = present ? static_cast<int>((total + kChunk - 1) / kChunk) : 0;
+  double sum = 0.0, acc = 0.0, mean = 0.0;
+  int64_t cnt = 0;
+  for (int pass = 0; pass < 2; ++pass) {
+    if (pass == 1) {
+      if (threadIdx.x == 0) s_out[0] = cnt > 0 ? sum / static_cast<double>(cnt) : 0.0;
+      __syncthreads();
+      mean = s_out[0];
+      if (!(cnt > 0 && mean != 0.0)) break;
+    }
+    // loader state (warp 1): current segment and offset in it
+    SegmentWalk walk;
+    const double* sp = nullptr;
+    int64_t slen = 0, off = 0;
+    bool have = walk.next(p, mi, variant, &sp, &slen);
+    for (int c = 0; c <= chunks; ++c) {
+      if (warp == 1 && c < chunks) {
+        double* dst = ring[c & 1];
+        int filled = 0;
+        while (filled < kChunk && have) {
+          const int64_t avail = slen - off;
+          const int take = static_cast<int>(avail < kChunk - filled ? avail : kChunk - filled);
+          for (int i = lane; i < take; i += 32) dst[filled + i] = sp[off + i];
+          filled += take;
+          off += take;
+          if (off == slen) {
+            have = walk.next(p, mi, variant, &sp, &slen);
+            off = 0;
+          }
+        }
+        for (int i = filled + lane; i < kChunk; i += 32) dst[i] = nan("");
+      }
+      if (warp == 0 && lane == 0 && c > 0) {
+        const double2* src = reinterpret_cast<const double2*>(ring[(c - 1) & 1]);
+        if (pass == 0) {
+          for (int i = 0; i < kChunk / 2; ++i) {
+            const double2 v = src[i];
+            const bool a = !isnan(v.x), b = !isnan(v.y);
+            sum += a ? v.x : 0.0;  // sum >= +0, ratios >= 0: adding +0.0 is exact
+            sum += b ? v.y : 0.0;
+            cnt += a + b;
+          }
+        } else {
+          for (int i = 0; i < kChunk / 2; ++i) {
+            const double2 v = src[i];
+            const double dx = isnan(v.x) ? 0.0 : (v.x - mean) * (v.x - mean);
+            const double dy = isnan(v.y) ? 0.0 : (v.y - mean) * (v.y - mean);
+            acc += dx;
+            acc += dy;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+  if (threadIdx.x != 0) return;
   const double nanv = nan("");
   double mean_goodput = nanv, pooled = nanv, rps_cv = nanv;
-  const int64_t block = static_cast<int64_t>(R) * p.n;
   if (present) {
     double s = 0.0;
     for (int ri = 0; ri < p.n_rps; ++ri) s += sc[ri * kCellScratch + (variant == 0 ? 0 : 1)];
     mean_goodput = s / static_cast<double>(p.n_rps);
-    // pooled ratios: rps in grid order, the chosen cell's rows, ids in order
-    double sum = 0.0;
-    int64_t cnt = 0;
-    for (int ri = 0; ri < p.n_rps; ++ri) {
-      const int64_t base = (static_cast<int64_t>(mi) * p.n_rps + ri) * per_rps;
-      if (variant == 0) {
-        warp_seq_sum(p.ratios + (base + static_cast<int64_t>(p.n_caps) * R) * p.n, block, sum, cnt);
-      } else {
-        const int bc = p.best_cap[mi * p.n_rps + ri];
-        for (int w = 0; w < p.n_caps; ++w)
-          if (p.caps[w] == bc)
-            warp_seq_sum(p.ratios + (base + static_cast<int64_t>(w) * R) * p.n, block, sum, cnt);
-      }
-    }
-    if (cnt > 0) {
-      const double mean = sum / static_cast<double>(cnt);
-      if (mean != 0.0) {
-        double acc = 0.0;
-        for (int ri = 0; ri < p.n_rps; ++ri) {
-          const int64_t base = (static_cast<int64_t>(mi) * p.n_rps + ri) * per_rps;
-          if (variant == 0) {
-            warp_seq_sq(p.ratios + (base + static_cast<int64_t>(p.n_caps) * R) * p.n, block, mean,
-                        acc);
-          } else {
-            const int bc = p.best_cap[mi * p.n_rps + ri];
-            for (int w = 0; w < p.n_caps; ++w)
-              if (p.caps[w] == bc)
-                warp_seq_sq(p.ratios + (base + static_cast<int64_t>(w) * R) * p.n, block, mean,
-                            acc);
-          }
-        }
-        pooled = sqrt(acc / static_cast<double>(cnt)) / mean;
-      }
-    }
+    if (cnt > 0 && mean != 0.0) pooled = sqrt(acc / static_cast<double>(cnt)) / mean;
     rps_cv = cv_cells(sc, p.n_rps, variant == 0 ? 2 : 3, variant == 0 ? 4 : 5);
   }
-  if (lane == 0) means[variant] = mean_goodput;
-  __syncthreads();
-  if (lane != 0) return;
   saber_mix_summary* out = p.summary + mi;
   if (variant == 0) {
     out->saber_mean_goodput = mean_goodput;
     out->saber_pooled_cv = pooled;
     out->saber_rps_mean_cv = rps_cv;
-    out->delta = means[0] - means[1];
   } else {
     out->best_static_mean_goodput = mean_goodput;
     out->best_static_pooled_cv = pooled;
     out->best_static_rps_mean_cv = rps_cv;
   }
+}
+
+// delta = saber - best static (simloop.cpp:262), after both variants wrote.
+__global__ void summary_delta_kernel(const SummaryParams p) {
+  const int mi = blockIdx.x * blockDim.x + threadIdx.x;
+  if (mi >= p.n_mixes) return;
+  saber_mix_summary* out = p.summary + mi;
+  out->delta = out->saber_mean_goodput - out->best_static_mean_goodput;
 }
 
 }  // namespace
@@ -257,7 +331,8 @@ int launch_summary(const SummaryParams& p, void* stream) {
   if (cells == 0) return 0;
   ratios_kernel<<<1184, 256, 0, s>>>(p);
   summary_cells_kernel<<<(cells * 32 + 127) / 128, 128, 0, s>>>(p);
-  summary_mix_kernel<<<p.n_mixes, 64, 0, s>>>(p);
+  summary_mix_kernel<<<2 * p.n_mixes, 64, 0, s>>>(p);
+  summary_delta_kernel<<<1, 32, 0, s>>>(p);
   return cudaGetLastError() == cudaSuccess ? 0 : 1;
 }
 
