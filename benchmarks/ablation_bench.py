@@ -1,0 +1,102 @@
+#!/usr/bin/env python3
+"""BASELINE config 3: estimator ablation — SABER with the usl / linear / logistic
+models of SURVEY §8(d) across W1-W3 x the paper's 12 request rates x 1024 seeds
+(3 x 36,864 = 110,592 trajectories), generalising the reference's
+usl-vs-linear ablation (acceptance_main.cpp:585-639).
+
+    python benchmarks/ablation_bench.py [--seeds 1024] [--cpu-seeds 8]
+
+Prints one JSON line: GPU trajectories/s (device time of the staged sweeps and
+end-to-end through saber_cuda_sweep), per-(mix, rps) mean goodput per family,
+and the reference (oracle/_ref saber::sweep, all host threads) on a seed sample
+with a goodput equality check on that sample.
+"""
+import argparse
+import json
+import os
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "oracle"))
+
+MODELS = {  # calibrate(profile(EngineConfig{}, {w3, n=1000, seed 42}, 50))
+    "usl": (0, (99.999999999997357, 0.049999999999992085, 0.0010000000000001078)),
+    "logistic": (1, (200.0, 0.046625169303483933, -6.3061840170033063)),
+    "linear": (2, (-1.292318089365694, 72.295958816519274, 0.0)),
+}
+MIXES = ["w1", "w2", "w3"]
+RPS = [1.0, 2.0, 3.0, 4.0, 5.0, 6.0, 7.0, 8.0, 9.0, 10.0, 15.0, 20.0]
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--seeds", type=int, default=1024)
+    ap.add_argument("--cpu-seeds", type=int, default=8)
+    ap.add_argument("--reps", type=int, default=2)
+    args = ap.parse_args()
+    import paper_2506_19677_b200 as S
+    grid = S.SweepGrid(MIXES, RPS, [], True)
+    out = {"config": "config3: SABER x {usl, linear, logistic} x W1-W3 x 12 rps x seeds, n=100",
+           "seeds": args.seeds, "families": {}}
+    total_dev = total_wall = 0.0
+    n_traj = 0
+    gpu_rows = {}
+    for name, (fam, p) in MODELS.items():
+        base = S.SimConfig(model=S.SpeedModel(fam, p), repeats=args.seeds, seed=42)
+        plan = S.SweepPlan(grid, base)
+        best_dev = 1e30
+        for _ in range(args.reps + 1):
+            plan.run()
+            plan.summarize()
+            best_dev = min(best_dev, plan.stats()[0])
+        rows, _, summ, _ = plan.fetch()
+        plan.close()
+        t0 = time.perf_counter()
+        res = S.sweep(grid, base)
+        wall = time.perf_counter() - t0
+        g = rows["goodput"].reshape(len(MIXES), len(RPS), args.seeds)
+        gpu_rows[name] = rows
+        out["families"][name] = {
+            "device_ms": best_dev, "e2e_ms": wall * 1e3,
+            "decisions": int(rows["decisions"].sum()),
+            "mean_goodput": {m: [float(x) for x in g[i].mean(axis=1)] for i, m in enumerate(MIXES)},
+            "saber_mean_goodput_by_mix": {m: summ[i].saber_mean_goodput for i, m in enumerate(MIXES)},
+        }
+        total_dev += best_dev
+        total_wall += wall
+        n_traj += len(rows)
+    out["trajectories"] = n_traj
+    out["gpu_traj_per_s_device"] = n_traj / (total_dev / 1e3)
+    out["gpu_traj_per_s_e2e"] = n_traj / total_wall
+    mu_u = out["families"]["usl"]["mean_goodput"]["w2"][-1]
+    mu_l = out["families"]["linear"]["mean_goodput"]["w2"][-1]
+    out["w2_at_20rps"] = {"usl": mu_u, "linear": mu_l}
+    import oracle as O
+    if O.reference_available() and args.cpu_seeds > 0:
+        ref = O.Oracle("reference")
+        k = args.cpu_seeds
+        same = True
+        t_cpu = 0.0
+        n_cpu = 0
+        for name, (fam, p) in MODELS.items():
+            b = O.make_config(mix="w3", n=100, seed=42, model=(fam, p))
+            b.has_model = 1
+            t0 = time.perf_counter()
+            r = ref.sweep(b, MIXES, RPS, [], True, k, jobs=0)
+            t_cpu += time.perf_counter() - t0
+            n_cpu += len(r["goodput"])
+            g = gpu_rows[name]["goodput"].reshape(len(MIXES) * len(RPS), args.seeds)[:, :k].reshape(-1)
+            same = same and bool(np.array_equal(g, r["goodput"]))
+        out["cpu_baseline"] = {"value": n_cpu / t_cpu, "unit": "traj/s", "cores": os.cpu_count(),
+                               "kind": "reference",
+                               "sample": f"saber::sweep, seeds 42..{41 + k}, 3 families, jobs=0"}
+        out["same_goodput_on_sample"] = same
+    print(json.dumps(out))
+
+
+if __name__ == "__main__":
+    main()
