@@ -264,6 +264,69 @@ typedef struct {
 saber_status saber_cuda_run_batch(const saber_run_batch_desc* desc, saber_run_batch_out* out);
 
 /* --------------------------------------------------------------------------
+ * Monte-Carlo sweep with bursty arrivals (BASELINE config 5; no reference
+ * counterpart: the reference generator is Poisson only, workload.cpp:60).
+ * Trajectory k (0 <= k < n_traj) simulates cell k % n_cells of the grid
+ * mix -> rps -> [caps..., saber] on its own arrival trace: a 2-state MMPP
+ * (burst rate = burst_factor * rps, exponential holding times with means
+ * mean_calm / mean_burst) drawn from Philox4x32-10 keyed by (seed, k); tasks
+ * and lengths follow generate()'s rules.  Its scheduler seed (SimConfig::seed)
+ * is scheduler_seed + k % scheduler_seeds.  saber_cuda_mc_trace() rebuilds any
+ * trajectory's requests and config on the host, bit-identically, so it can
+ * be replayed through run_with_requests().
+ * -------------------------------------------------------------------------- */
+#define SABER_MC_STATS 8   /* trajectories, requests, met, completed, decisions,
+                              admitted, sum of decision-hash low bits, ticks */
+#define SABER_MC_BINS 64   /* latency/SLA ratio bins: 4 per octave from 2^-6 */
+
+typedef struct {
+  int64_t n_traj;
+  const int32_t* mixes;
+  int32_t n_mixes;
+  const double* rps;
+  int32_t n_rps;
+  const int32_t* caps;
+  int32_t n_caps;
+  int32_t with_saber;
+  int32_t num_requests;
+  double length_jitter;
+  int32_t window_size;
+  double tick;
+  int32_t has_model;
+  saber_model model;
+  saber_model ground_truth;
+  double prefill_rate;
+  /* bursty arrivals */
+  uint64_t seed;
+  double burst_factor;
+  double mean_calm;
+  double mean_burst;
+  uint64_t scheduler_seed;
+  int32_t scheduler_seeds;
+  /* execution */
+  int32_t device;
+  int32_t shard_index;   /* this process runs trajectories k with k % shard_count == shard_index */
+  int32_t shard_count;
+  int64_t chunk;         /* trajectories per device batch (0 = automatic) */
+} saber_mc_desc;
+
+typedef struct {
+  int64_t* cell_stats;     /* [n_cells][SABER_MC_STATS], accumulated (not cleared) */
+  int64_t* cell_hist;      /* [n_cells][SABER_MC_BINS + 1] (+1: never completed), accumulated, or NULL */
+  saber_traj_row* rows;    /* [n_traj] rows of this shard's trajectories, or NULL */
+  double device_ms;
+  double sim_kernel_ms;
+  int32_t kernel_launches;
+} saber_mc_out;
+
+int64_t saber_cuda_mc_cells(const saber_mc_desc* desc);
+saber_status saber_cuda_mc_sweep(const saber_mc_desc* desc, saber_mc_out* out);
+/* Host twin: trajectory k's requests (num_requests entries) and its config
+ * (spec->requests is left NULL).  Pure host code, no device needed. */
+saber_status saber_cuda_mc_trace(const saber_mc_desc* desc, int64_t k, saber_request* requests,
+                                 saber_traj_spec* spec);
+
+/* --------------------------------------------------------------------------
  * Batched fitting (estimator.cpp:33-375, calibration.cpp:137-168).
  * Curve c owns samples [offsets[c], offsets[c+1]).
  * -------------------------------------------------------------------------- */

@@ -130,6 +130,34 @@ class saber_fit_out(C.Structure):
                 ("kernel_launches", C.c_int32)]
 
 
+SABER_MC_STATS = 8
+SABER_MC_BINS = 64
+
+
+class saber_mc_desc(C.Structure):
+    _fields_ = [
+        ("n_traj", C.c_int64),
+        ("mixes", C.POINTER(C.c_int32)), ("n_mixes", C.c_int32),
+        ("rps", C.POINTER(C.c_double)), ("n_rps", C.c_int32),
+        ("caps", C.POINTER(C.c_int32)), ("n_caps", C.c_int32),
+        ("with_saber", C.c_int32),
+        ("num_requests", C.c_int32), ("length_jitter", C.c_double),
+        ("window_size", C.c_int32), ("tick", C.c_double),
+        ("has_model", C.c_int32), ("model", saber_model), ("ground_truth", saber_model),
+        ("prefill_rate", C.c_double),
+        ("seed", C.c_uint64), ("burst_factor", C.c_double), ("mean_calm", C.c_double),
+        ("mean_burst", C.c_double), ("scheduler_seed", C.c_uint64), ("scheduler_seeds", C.c_int32),
+        ("device", C.c_int32), ("shard_index", C.c_int32), ("shard_count", C.c_int32),
+        ("chunk", C.c_int64),
+    ]
+
+
+class saber_mc_out(C.Structure):
+    _fields_ = [("cell_stats", C.POINTER(C.c_int64)), ("cell_hist", C.POINTER(C.c_int64)),
+                ("rows", C.POINTER(saber_traj_row)), ("device_ms", C.c_double),
+                ("sim_kernel_ms", C.c_double), ("kernel_launches", C.c_int32)]
+
+
 # (name, restype, argtypes) for every symbol include/saber_cuda.h declares.
 _P = C.POINTER
 SYMBOLS = [
@@ -145,6 +173,10 @@ SYMBOLS = [
     ("saber_cuda_sweep_plan_destroy", None, [C.c_void_p]),
     ("saber_cuda_run_batch", C.c_int, [_P(saber_run_batch_desc), _P(saber_run_batch_out)]),
     ("saber_cuda_fit_batch", C.c_int, [_P(saber_fit_desc), _P(saber_fit_out)]),
+    ("saber_cuda_mc_cells", C.c_int64, [_P(saber_mc_desc)]),
+    ("saber_cuda_mc_sweep", C.c_int, [_P(saber_mc_desc), _P(saber_mc_out)]),
+    ("saber_cuda_mc_trace", C.c_int, [_P(saber_mc_desc), C.c_int64, _P(saber_request),
+                                      _P(saber_traj_spec)]),
     ("saber_cuda_predict_table", C.c_int, [_P(saber_model), C.c_int32, _P(C.c_double)]),
     ("saber_cuda_last_error", C.c_char_p, []),
     ("saber_cuda_abi_version", C.c_int32, []),

@@ -693,3 +693,100 @@ def calibrate(samples, device: int = 0) -> CalibrationReport:
                                                       float(res.r2[f, 0])) if ok else None,
                               "" if ok else f"fit failed for {FAMILIES[f]}"))
     return CalibrationReport(fits[b].model, fits)
+
+
+# ------------------------------------------------- bursty Monte-Carlo (config 5)
+@dataclass
+class BurstyArrivals:
+    """2-state MMPP of BASELINE config 5; see csrc/bursty.h."""
+    seed: int = 2026
+    burst_factor: float = 5.0
+    mean_calm: float = 8.0
+    mean_burst: float = 2.0
+
+
+@dataclass
+class McResult:
+    cell_stats: np.ndarray      # [n_cells][8]: trajectories, requests, met, completed,
+    #                             decisions, admitted, hash-low-bit sum, ticks
+    cell_hist: np.ndarray       # [n_cells][65]: latency/SLA bins (4/octave from 2^-6) + never
+    rows: Optional[np.ndarray]  # [n_traj] ROW_DTYPE (this shard's rows filled)
+    device_ms: float
+    sim_kernel_ms: float
+    kernel_launches: int
+
+
+def _mc_desc(n_traj, grid: SweepGrid, base: SimConfig, arrivals: BurstyArrivals, scheduler_seeds,
+             device, shard_index, shard_count, chunk, keep):
+    d = N.saber_mc_desc()
+    mix_ids = (C.c_int32 * len(grid.mixes))(*[int(m[1:]) for m in grid.mixes])
+    rps = (C.c_double * len(grid.rps_list))(*[float(r) for r in grid.rps_list])
+    caps = (C.c_int32 * max(1, len(grid.caps)))(*[int(c) for c in grid.caps])
+    keep += [mix_ids, rps, caps]
+    d.n_traj = n_traj
+    d.mixes, d.n_mixes = mix_ids, len(grid.mixes)
+    d.rps, d.n_rps = rps, len(grid.rps_list)
+    d.caps, d.n_caps = caps, len(grid.caps)
+    d.with_saber = 1 if grid.with_saber else 0
+    d.num_requests = base.workload.num_requests
+    d.length_jitter = base.workload.length_jitter
+    d.window_size = base.scheduler.window_size
+    d.tick = base.scheduler.tick
+    d.has_model = 1 if base.model is not None else 0
+    if base.model is not None:
+        d.model = _model(base.model)
+    d.ground_truth = _model(base.engine.ground_truth)
+    d.prefill_rate = base.engine.prefill_rate
+    d.seed = arrivals.seed
+    d.burst_factor = arrivals.burst_factor
+    d.mean_calm = arrivals.mean_calm
+    d.mean_burst = arrivals.mean_burst
+    d.scheduler_seed = int(base.seed) & 0xFFFFFFFFFFFFFFFF
+    d.scheduler_seeds = scheduler_seeds
+    d.device, d.shard_index, d.shard_count, d.chunk = device, shard_index, shard_count, chunk
+    return d
+
+
+def mc_sweep(n_traj: int, grid: SweepGrid, base: SimConfig, arrivals: BurstyArrivals = None,
+             scheduler_seeds: int = 1024, rows: bool = False, device: int = 0, shard_index: int = 0,
+             shard_count: int = 1, chunk: int = 0) -> McResult:
+    """Bursty Monte-Carlo sweep (saber_cuda_mc_sweep): trajectory k simulates
+    cell k % n_cells on its own Philox MMPP trace."""
+    keep = []
+    d = _mc_desc(n_traj, grid, base, arrivals or BurstyArrivals(), scheduler_seeds, device,
+                 shard_index, shard_count, chunk, keep)
+    cells = int(N.lib().saber_cuda_mc_cells(C.byref(d)))
+    stats = np.zeros((cells, N.SABER_MC_STATS), dtype=np.int64)
+    hist = np.zeros((cells, N.SABER_MC_BINS + 1), dtype=np.int64)
+    rws = np.zeros(n_traj, dtype=ROW_DTYPE) if rows else None
+    o = N.saber_mc_out()
+    o.cell_stats = stats.ctypes.data_as(C.POINTER(C.c_int64))
+    o.cell_hist = hist.ctypes.data_as(C.POINTER(C.c_int64))
+    if rows:
+        o.rows = rws.ctypes.data_as(C.POINTER(N.saber_traj_row))
+    _check(N.lib().saber_cuda_mc_sweep(C.byref(d), C.byref(o)))
+    return McResult(stats, hist, rws, o.device_ms, o.sim_kernel_ms, o.kernel_launches)
+
+
+def mc_trace(k: int, n_traj: int, grid: SweepGrid, base: SimConfig, arrivals: BurstyArrivals = None,
+             scheduler_seeds: int = 1024):
+    """Host twin: trajectory k's requests and SimConfig, bit-identical to what
+    the device simulates (for replay through run_with_requests)."""
+    keep = []
+    d = _mc_desc(n_traj, grid, base, arrivals or BurstyArrivals(), scheduler_seeds, 0, 0, 1, 0, keep)
+    n = base.workload.num_requests
+    reqs = (N.saber_request * n)()
+    spec = N.saber_traj_spec()
+    _check(N.lib().saber_cuda_mc_trace(C.byref(d), k, reqs, C.byref(spec)))
+    out = [Request(i, TASK_NAMES[r.task], r.arrival_time, r.input_tokens, r.max_output_tokens,
+                   r.sla_seconds, r.deadline) for i, r in enumerate(reqs)]
+    cfg = SimConfig()
+    cfg.workload = WorkloadSpec(WorkloadMix({TASK_NAMES[t]: spec.mix.frac[t] for t in range(4)
+                                             if spec.mix.present[t]}), spec.rps, n, 0,
+                                spec.length_jitter)
+    cfg.scheduler = SchedulerConfig(spec.mode, spec.window_size, spec.tick, spec.static_batch_size)
+    cfg.model = SpeedModel(spec.model.family, tuple(spec.model.params)) if spec.has_model else None
+    cfg.engine = EngineConfig(SpeedModel(spec.ground_truth.family, tuple(spec.ground_truth.params)),
+                              spec.prefill_rate)
+    cfg.seed = spec.seed
+    return out, cfg

@@ -1184,3 +1184,315 @@ extern "C" saber_status saber_cuda_fit_batch(const saber_fit_desc* desc, saber_f
   out->kernel_launches = launches;
   return SABER_OK;
 }
+
+// ===================================================== bursty Monte-Carlo ==
+namespace {
+
+saber_status validate_mc(const saber_mc_desc& d) {
+  if (d.n_traj < 0) return fail(SABER_EINVAL, "mc: n_traj must be >= 0");
+  if (d.n_mixes < 1 || d.n_rps < 1 || (d.n_caps < 1 && !d.with_saber))
+    return fail(SABER_EINVAL, "mc: empty grid");
+  if (d.with_saber && !d.has_model) return fail(SABER_EINVAL, "mc: saber variant requires a model");
+  for (int i = 0; i < d.n_mixes; ++i)
+    if (d.mixes[i] < 1 || d.mixes[i] > 3)
+      return fail(SABER_EINVAL, "unknown mix preset: w" + std::to_string(d.mixes[i]));
+  for (int i = 0; i < d.n_rps; ++i)
+    if (!(d.rps[i] > 0.0)) return fail(SABER_EINVAL, "rps must be > 0");
+  for (int i = 0; i < d.n_caps; ++i)
+    if (d.caps[i] < 1) return fail(SABER_EINVAL, "static mode requires a positive batch size");
+  if (d.num_requests < 1) return fail(SABER_EINVAL, "num_requests must be >= 1");
+  if (d.num_requests > kMaxRequests)
+    return fail(SABER_EINVAL, "num_requests > " + std::to_string(kMaxRequests) +
+                                  " is not supported by the B200 engine");
+  if (d.length_jitter < 0.0 || d.length_jitter >= 1.0)
+    return fail(SABER_EINVAL, "length_jitter must be in [0, 1)");
+  if (d.window_size < 1) return fail(SABER_EINVAL, "window_size must be >= 1");
+  if (d.window_size > kMaxWindow)
+    return fail(SABER_EINVAL, "window_size > " + std::to_string(kMaxWindow) +
+                                  " is not supported by the B200 engine");
+  if (!(d.tick > 0.0)) return fail(SABER_EINVAL, "tick must be > 0");
+  if (saber_status s = validate_model(d.ground_truth, "ground truth")) return s;
+  if (d.has_model)
+    if (saber_status s = validate_model(d.model, "model")) return s;
+  if (!(eval_model(d.ground_truth, 1.0) > 0.0))
+    return fail(SABER_EINVAL, "engine ground truth must be positive");
+  if (!(d.burst_factor > 0.0) || !(d.mean_calm > 0.0) || !(d.mean_burst > 0.0))
+    return fail(SABER_EINVAL, "mc: burst factor and holding-time means must be > 0");
+  if (d.scheduler_seeds < 1) return fail(SABER_EINVAL, "mc: scheduler_seeds must be >= 1");
+  if (d.shard_count < 1 || d.shard_index < 0 || d.shard_index >= d.shard_count)
+    return fail(SABER_EINVAL, "bad shard index/count");
+  return SABER_OK;
+}
+
+int64_t mc_cells(const saber_mc_desc& d) {
+  return static_cast<int64_t>(d.n_mixes) * d.n_rps * (d.n_caps + (d.with_saber ? 1 : 0));
+}
+
+bursty::Params mc_params(const saber_mc_desc& d) {
+  return bursty::Params{d.seed, d.burst_factor, d.mean_calm, d.mean_burst};
+}
+
+}  // namespace
+
+extern "C" int64_t saber_cuda_mc_cells(const saber_mc_desc* d) { return d ? mc_cells(*d) : 0; }
+
+extern "C" saber_status saber_cuda_mc_trace(const saber_mc_desc* desc, int64_t k,
+                                            saber_request* requests, saber_traj_spec* spec) {
+  if (!desc || !requests || !spec) return fail(SABER_EINVAL, "null argument");
+  if (saber_status s = validate_mc(*desc)) return s;
+  if (k < 0 || k >= desc->n_traj) return fail(SABER_EINVAL, "mc_trace: trajectory out of range");
+  const int per_rps = desc->n_caps + (desc->with_saber ? 1 : 0);
+  const int64_t cell = k % mc_cells(*desc);
+  const int v = static_cast<int>(cell % per_rps);
+  const int ri = static_cast<int>((cell / per_rps) % desc->n_rps);
+  const int mi = static_cast<int>((cell / per_rps) / desc->n_rps);
+  const saber_mix mix = preset(desc->mixes[mi]);
+  double th[4];
+  int8_t tt[4], tl;
+  mix_thresholds(mix, th, tt, &tl);
+  const bursty::Params bp = mc_params(*desc);
+  bursty::Gen g;
+  bursty::gen_init(g, bp, static_cast<uint64_t>(k));
+  const double rps = desc->rps[ri];
+  for (int q = 0; q < desc->num_requests; ++q) {
+    const double arrival = bursty::gen_arrival(g, bp, rps);
+    const double u = bursty::gen_uniform(g);
+    int task = tl;  // sample_task (workload.cpp:28-39)
+    for (int a = 0; a < 4; ++a)
+      if (tt[a] >= 0 && u < th[a]) {
+        task = tt[a];
+        break;
+      }
+    auto jl = [&](int avg) {  // jittered_length (workload.cpp:21-26)
+      const double lo = avg * (1.0 - desc->length_jitter);
+      const double hi = avg * (1.0 + desc->length_jitter);
+      return std::max(1, static_cast<int>(std::llround(lo + bursty::gen_uniform(g) * (hi - lo))));
+    };
+    saber_request& r = requests[q];
+    r.arrival_time = arrival;
+    r.input_tokens = jl(kAvgInH[task]);
+    r.max_output_tokens = jl(kAvgOutH[task]);
+    r.sla_seconds = kSlaH[task];
+    r.deadline = arrival + kSlaH[task];
+    r.task = task;
+    r.pad_ = 0;
+  }
+  *spec = saber_traj_spec{};
+  spec->mix = mix;
+  spec->rps = rps;
+  spec->num_requests = desc->num_requests;
+  spec->length_jitter = desc->length_jitter;
+  spec->requests = nullptr;
+  const bool saber = desc->with_saber && v == desc->n_caps;
+  spec->mode = saber ? SABER_MODE_SABER : SABER_MODE_STATIC;
+  spec->window_size = desc->window_size;
+  spec->tick = desc->tick;
+  spec->static_batch_size = saber ? 0 : desc->caps[v];
+  spec->has_model = saber ? 1 : 0;
+  spec->model = desc->model;
+  spec->ground_truth = desc->ground_truth;
+  spec->prefill_rate = desc->prefill_rate;
+  spec->has_horizon = 0;
+  spec->seed = desc->scheduler_seed + static_cast<uint64_t>(k % desc->scheduler_seeds);
+  return SABER_OK;
+}
+
+extern "C" saber_status saber_cuda_mc_sweep(const saber_mc_desc* desc, saber_mc_out* out) {
+  if (!desc || !out) return fail(SABER_EINVAL, "null argument");
+  if (saber_status s = validate_mc(*desc)) return s;
+  if (!out->cell_stats) return fail(SABER_EINVAL, "mc: cell_stats output required");
+  if (saber_status s = use_device(desc->device)) return s;
+  const saber_mc_desc& d = *desc;
+  const int dev = d.device, n = d.num_requests;
+  const int64_t cells = mc_cells(d);
+  const int64_t mine = d.n_traj > d.shard_index
+                           ? (d.n_traj - d.shard_index + d.shard_count - 1) / d.shard_count
+                           : 0;
+  const int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(d.chunk > 0 ? d.chunk : 262144,
+                                                               std::max<int64_t>(mine, 1)));
+  // tables, mixes, caps, rps
+  const int tl = n + 2;
+  std::vector<double> tab(static_cast<size_t>(2 * tl));
+  fill_table(d.ground_truth, n + 1, &tab[0]);
+  double ceiling = std::nan("");
+  if (d.has_model) {
+    fill_table(d.model, n + 1, &tab[static_cast<size_t>(tl)]);
+    ceiling = tab[static_cast<size_t>(tl) + 1];
+  }
+  std::vector<double> th(static_cast<size_t>(d.n_mixes) * 4);
+  std::vector<int8_t> tt(static_cast<size_t>(d.n_mixes) * 4), tlast(static_cast<size_t>(d.n_mixes));
+  for (int mi = 0; mi < d.n_mixes; ++mi)
+    mix_thresholds(preset(d.mixes[mi]), &th[static_cast<size_t>(mi) * 4],
+                   &tt[static_cast<size_t>(mi) * 4], &tlast[static_cast<size_t>(mi)]);
+  DevBuf tables, rps_d, caps_d, th_d, tt_d, tl_d, hmax, seeds_d, off_d, len_d, draws_d, descs, rows,
+      comp, cursor, err, stats, hist;
+  Workloads wl;
+  Scratch scratch;
+  ALLOC_TRY(tables, dev, tab.size() * 8);
+  ALLOC_TRY(rps_d, dev, static_cast<size_t>(d.n_rps) * 8);
+  ALLOC_TRY(caps_d, dev, std::max<size_t>(1, static_cast<size_t>(d.n_caps)) * 4);
+  ALLOC_TRY(th_d, dev, th.size() * 8);
+  ALLOC_TRY(tt_d, dev, tt.size());
+  ALLOC_TRY(tl_d, dev, tlast.size());
+  ALLOC_TRY(hmax, dev, 16);
+  ALLOC_TRY(stats, dev, static_cast<size_t>(cells) * SABER_MC_STATS * 8);
+  ALLOC_TRY(hist, dev, static_cast<size_t>(cells) * (SABER_MC_BINS + 1) * 8);
+  ALLOC_TRY(descs, dev, static_cast<size_t>(chunk) * sizeof(TrajDesc));
+  ALLOC_TRY(rows, dev, static_cast<size_t>(chunk) * sizeof(saber_traj_row));
+  ALLOC_TRY(comp, dev, static_cast<size_t>(chunk) * n * 8);
+  ALLOC_TRY(cursor, dev, 16);
+  ALLOC_TRY(err, dev, 16);
+  if (saber_status s = wl.alloc(dev, chunk, n)) return s;
+  if (saber_status s = scratch.alloc(dev, n)) return s;
+  CUDA_TRY(cudaMemcpy(tables.p, tab.data(), tab.size() * 8, cudaMemcpyHostToDevice));
+  CUDA_TRY(cudaMemcpy(rps_d.p, d.rps, static_cast<size_t>(d.n_rps) * 8, cudaMemcpyHostToDevice));
+  if (d.n_caps > 0)
+    CUDA_TRY(cudaMemcpy(caps_d.p, d.caps, static_cast<size_t>(d.n_caps) * 4, cudaMemcpyHostToDevice));
+  CUDA_TRY(cudaMemcpy(th_d.p, th.data(), th.size() * 8, cudaMemcpyHostToDevice));
+  CUDA_TRY(cudaMemcpy(tt_d.p, tt.data(), tt.size(), cudaMemcpyHostToDevice));
+  CUDA_TRY(cudaMemcpy(tl_d.p, tlast.data(), tlast.size(), cudaMemcpyHostToDevice));
+
+  McParams mp{};
+  mp.n_mixes = d.n_mixes;
+  mp.n_rps = d.n_rps;
+  mp.n_caps = d.n_caps;
+  mp.with_saber = d.with_saber;
+  mp.n_cells = static_cast<int32_t>(cells);
+  mp.rps = rps_d.as<double>();
+  mp.caps = caps_d.as<int32_t>();
+  mp.mix_thresh = th_d.as<double>();
+  mp.mix_task = tt_d.as<int8_t>();
+  mp.mix_last = tl_d.as<int8_t>();
+  mp.n = n;
+  mp.jitter = d.length_jitter;
+  mp.ceiling = d.with_saber ? ceiling : std::nan("");
+  mp.bp = mc_params(d);
+  mp.shard_index = d.shard_index;
+  mp.shard_count = d.shard_count;
+  mp.sched_seeds = d.scheduler_seeds;
+  mp.window = d.window_size;
+  mp.tick = d.tick;
+  mp.prefill_rate = d.prefill_rate;
+  mp.model_tab = d.has_model ? tl : -1;
+  mp.gt_tab = 0;
+  mp.arrival = wl.arr.as<double>();
+  mp.deadline = wl.dl.as<double>();
+  mp.sla = wl.sla.as<double>();
+  mp.max_out = wl.mo.as<double>();
+  mp.input = wl.in.as<double>();
+  mp.demote_after = wl.dem.as<double>();
+  mp.horizon = wl.hor.as<double>();
+  mp.task = wl.task.as<int8_t>();
+  mp.descs = descs.as<TrajDesc>();
+
+  Timer all, simt;
+  if (saber_status s = all.init()) return s;
+  if (saber_status s = simt.init()) return s;
+  cudaStream_t st = nullptr;
+  int launches = 0;
+  float sim_ms_total = 0.f;
+  CUDA_TRY(cudaEventRecord(all.a, st));
+  CUDA_TRY(cudaMemsetAsync(stats.p, 0, stats.bytes, st));
+  CUDA_TRY(cudaMemsetAsync(hist.p, 0, hist.bytes, st));
+  CUDA_TRY(cudaMemsetAsync(err.p, 0, 16, st));
+  // Scheduler RNG streams sized by the longest default horizon of this shard.
+  int32_t pool = 0;
+  if (d.with_saber && mine > 0) {
+    CUDA_TRY(cudaMemsetAsync(hmax.p, 0, 16, st));
+    LAUNCH_TRY(launch_mc_horizon(mp, mine, hmax.as<unsigned long long>(), st));
+    ++launches;
+    double hm = 0.0;
+    CUDA_TRY(cudaMemcpy(&hm, hmax.p, 8, cudaMemcpyDeviceToHost));
+    pool = static_cast<int32_t>(std::min<int64_t>(d.scheduler_seeds, d.n_traj));
+    const int64_t len = draw_bound(hm + 1.0, d.tick, d.window_size, n);
+    std::vector<uint64_t> seeds(static_cast<size_t>(pool));
+    std::vector<int64_t> off(static_cast<size_t>(pool)), lens(static_cast<size_t>(pool), len);
+    for (int32_t s = 0; s < pool; ++s) {
+      seeds[static_cast<size_t>(s)] = (d.scheduler_seed + static_cast<uint64_t>(s)) ^ kSchedulerSeedSalt;
+      off[static_cast<size_t>(s)] = static_cast<int64_t>(s) * len;
+    }
+    ALLOC_TRY(seeds_d, dev, seeds.size() * 8);
+    ALLOC_TRY(off_d, dev, off.size() * 8);
+    ALLOC_TRY(len_d, dev, lens.size() * 8);
+    ALLOC_TRY(draws_d, dev, static_cast<size_t>(std::max<int64_t>(1, len * pool)) * 4);
+    CUDA_TRY(cudaMemcpy(seeds_d.p, seeds.data(), seeds.size() * 8, cudaMemcpyHostToDevice));
+    CUDA_TRY(cudaMemcpy(off_d.p, off.data(), off.size() * 8, cudaMemcpyHostToDevice));
+    CUDA_TRY(cudaMemcpy(len_d.p, lens.data(), lens.size() * 8, cudaMemcpyHostToDevice));
+    RngGenParams rg{};
+    rg.seeds = seeds_d.as<uint64_t>();
+    rg.draws = draws_d.as<uint32_t>();
+    rg.off = off_d.as<int64_t>();
+    rg.len = len_d.as<int64_t>();
+    rg.n_streams = pool;
+    LAUNCH_TRY(launch_rng_streams(rg, st));
+    ++launches;
+  }
+  std::vector<saber_traj_row> host_rows;
+  if (out->rows) host_rows.resize(static_cast<size_t>(chunk));
+  for (int64_t k0 = 0; k0 < mine; k0 += chunk) {
+    mp.k0 = k0;
+    mp.count = std::min<int64_t>(chunk, mine - k0);
+    LAUNCH_TRY(launch_mc_workloads(mp, st));
+    CUDA_TRY(cudaMemsetAsync(rows.p, 0, static_cast<size_t>(mp.count) * sizeof(saber_traj_row), st));
+    CUDA_TRY(cudaMemsetAsync(cursor.p, 0, 16, st));
+    LAUNCH_TRY(launch_fill_rows(comp.as<double>(), mp.count, n, 0, 1, st));
+    SimParams sp{};
+    sp.traj = descs.as<TrajDesc>();
+    sp.n_traj = static_cast<int32_t>(mp.count);
+    sp.wl = wl.view(n);
+    sp.tables = tables.as<double>();
+    sp.rng.draws = draws_d.as<uint32_t>();
+    sp.rng.off = off_d.as<int64_t>();
+    sp.rng.len = len_d.as<int64_t>();
+    sp.scratch = scratch.view;
+    sp.slot_rows = scratch.launch.slot_rows;
+    sp.out.rows = rows.as<saber_traj_row>();
+    sp.out.completion = comp.as<double>();
+    sp.out.error = err.as<int32_t>();
+    sp.next_traj = cursor.as<int32_t>();
+    CUDA_TRY(cudaEventRecord(simt.a, st));
+    LAUNCH_TRY(launch_sim(sp, scratch.launch, st));
+    CUDA_TRY(cudaEventRecord(simt.b, st));
+    RowMetricsParams rm{};
+    rm.rows = rows.as<saber_traj_row>();
+    rm.completion = comp.as<double>();
+    rm.wl = sp.wl;
+    rm.traj = sp.traj;
+    rm.n_traj = sp.n_traj;
+    LAUNCH_TRY(launch_row_metrics(rm, st));
+    LAUNCH_TRY(launch_mc_reduce(mp, rows.as<saber_traj_row>(), comp.as<double>(), stats.as<int64_t>(),
+                                out->cell_hist ? hist.as<int64_t>() : nullptr, st));
+    launches += 5;
+    CUDA_TRY(cudaEventSynchronize(simt.b));
+    float ms = 0.f;
+    CUDA_TRY(cudaEventElapsedTime(&ms, simt.a, simt.b));
+    sim_ms_total += ms;
+    if (out->rows) {
+      CUDA_TRY(cudaMemcpy(host_rows.data(), rows.p, static_cast<size_t>(mp.count) * sizeof(saber_traj_row),
+                          cudaMemcpyDeviceToHost));
+      for (int64_t i = 0; i < mp.count; ++i)
+        out->rows[d.shard_index + (k0 + i) * d.shard_count] = host_rows[static_cast<size_t>(i)];
+    }
+  }
+  CUDA_TRY(cudaEventRecord(all.b, st));
+  CUDA_TRY(cudaEventSynchronize(all.b));
+  float ms = 0.f;
+  CUDA_TRY(cudaEventElapsedTime(&ms, all.a, all.b));
+  std::vector<int64_t> hs(static_cast<size_t>(cells) * SABER_MC_STATS);
+  CUDA_TRY(cudaMemcpy(hs.data(), stats.p, hs.size() * 8, cudaMemcpyDeviceToHost));
+  for (size_t i = 0; i < hs.size(); ++i) out->cell_stats[i] += hs[i];
+  if (out->cell_hist) {
+    std::vector<int64_t> hh(static_cast<size_t>(cells) * (SABER_MC_BINS + 1));
+    CUDA_TRY(cudaMemcpy(hh.data(), hist.p, hh.size() * 8, cudaMemcpyDeviceToHost));
+    for (size_t i = 0; i < hh.size(); ++i) out->cell_hist[i] += hh[i];
+  }
+  out->device_ms = ms;
+  out->sim_kernel_ms = sim_ms_total;
+  out->kernel_launches = launches;
+  int32_t e = 0;
+  CUDA_TRY(cudaMemcpy(&e, err.p, 4, cudaMemcpyDeviceToHost));
+  if (e == kErrRngExhausted)
+    return fail(SABER_EINTERNAL, "scheduler RNG stream exhausted (draw bound violated)");
+  if (e != 0) return fail(SABER_EINTERNAL, "trajectory kernel error " + std::to_string(e));
+  return SABER_OK;
+}

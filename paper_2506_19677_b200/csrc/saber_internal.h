@@ -201,6 +201,36 @@ struct SummaryParams {
 };
 int launch_summary(const SummaryParams& p, void* stream);
 
+// Bursty Monte-Carlo sweep (mc.cu, BASELINE config 5).
+}  // namespace saberb200
+#include "bursty.h"
+namespace saberb200 {
+struct McParams {
+  int32_t n_mixes, n_rps, n_caps, with_saber, n_cells;
+  const double* rps;
+  const int32_t* caps;
+  const double* mix_thresh;
+  const int8_t* mix_task;
+  const int8_t* mix_last;
+  int32_t n;
+  double jitter;
+  double ceiling;
+  bursty::Params bp;
+  int64_t k0, count;  // chunk: local i -> trajectory k = shard_index + (k0 + i) * shard_count
+  int32_t shard_index, shard_count;
+  int32_t sched_seeds;
+  int32_t window;
+  double tick, prefill_rate;
+  int32_t model_tab, gt_tab;
+  double *arrival, *deadline, *sla, *max_out, *input, *demote_after, *horizon;
+  int8_t* task;
+  TrajDesc* descs;
+};
+int launch_mc_horizon(const McParams& p, int64_t count, unsigned long long* hmax, void* stream);
+int launch_mc_workloads(const McParams& p, void* stream);
+int launch_mc_reduce(const McParams& p, const saber_traj_row* rows, const double* comp,
+                     int64_t* stats, int64_t* hist, void* stream);
+
 // Fitting.
 struct FitParams {
   const int32_t* loads;
