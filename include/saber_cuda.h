@@ -17,6 +17,8 @@
  *                                 CalibrationReport calibrate(const std::vector<LoadSpeedSample>&)
  *                                 calibration.hpp:54, calibration.cpp:137-168
  *                                 (many independent curves per call)
+ *   saber_cuda_profile_batch  <- profile(const EngineConfig&, const WorkloadSpec&, int l_max)
+ *                                 calibration.hpp:29-31, calibration.cpp:58-135 (batched)
  *   saber_cuda_predict_table  <- double predict(const SpeedModel&, int)       estimator.hpp:39
  *
  * Conventions: plain C, POD structs, caller-owned memory, no exceptions.  Every
@@ -325,6 +327,41 @@ saber_status saber_cuda_mc_sweep(const saber_mc_desc* desc, saber_mc_out* out);
  * (spec->requests is left NULL).  Pure host code, no device needed. */
 saber_status saber_cuda_mc_trace(const saber_mc_desc* desc, int64_t k, saber_request* requests,
                                  saber_traj_spec* spec);
+
+/* --------------------------------------------------------------------------
+ * Batched offline profiling <- std::vector<LoadSpeedSample>
+ *   profile(const EngineConfig&, const WorkloadSpec&, int l_max)
+ *   calibration.hpp:29-31, calibration.cpp:58-135
+ * Each profile's samples land at [sample_offsets[p], sample_offsets[p+1]).
+ * -------------------------------------------------------------------------- */
+typedef struct {
+  saber_model ground_truth;  /* EngineConfig (engine.hpp:16-19) */
+  double prefill_rate;
+  saber_mix mix;             /* profiling WorkloadSpec (rps unused, calibration.hpp:28) */
+  int32_t num_requests;
+  uint64_t seed;
+  double length_jitter;
+  int32_t l_max;
+} saber_profile_spec;
+
+typedef struct {
+  const saber_profile_spec* specs;
+  int32_t n_profiles;
+  int32_t device;
+} saber_profile_desc;
+
+typedef struct {
+  int64_t* sample_offsets;   /* [n_profiles + 1], filled by the call */
+  int32_t* loads;            /* [capacity] LoadSpeedSample::load */
+  double* speeds;            /* [capacity] LoadSpeedSample::speed */
+  int64_t capacity;
+  int32_t* status;           /* [n_profiles]: 0 ok, 1 CalibrationError (< 3 distinct loads) */
+  double device_ms;
+} saber_profile_out;
+
+/* Number of samples profile() yields for one spec (host-side, no device). */
+int64_t saber_cuda_profile_samples(const saber_profile_spec* spec);
+saber_status saber_cuda_profile_batch(const saber_profile_desc* desc, saber_profile_out* out);
 
 /* --------------------------------------------------------------------------
  * Batched fitting (estimator.cpp:33-375, calibration.cpp:137-168).

@@ -7,7 +7,7 @@ mirroring the reference's API names (see api.py).
 from .api import *  # noqa: F401,F403
 from .api import (BatchResult, CalibrationError, DomainError, FitError, InvalidArgument,  # noqa: F401
                   FitBatchResult, LoadSpeedSample, CalibrationReport, fit, fit_batch, calibrate,
-                  BurstyArrivals, McResult, mc_sweep, mc_trace,
+                  BurstyArrivals, McResult, mc_sweep, mc_trace, profile, profile_batch,
                   ROW_DTYPE, SweepPlan, run_batch, sweep_row_keys)
 from ._native import LIB_PATH, SaberError, lib  # noqa: F401
 

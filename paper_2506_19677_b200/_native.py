@@ -158,6 +158,23 @@ class saber_mc_out(C.Structure):
                 ("sim_kernel_ms", C.c_double), ("kernel_launches", C.c_int32)]
 
 
+class saber_profile_spec(C.Structure):
+    _fields_ = [("ground_truth", saber_model), ("prefill_rate", C.c_double), ("mix", saber_mix),
+                ("num_requests", C.c_int32), ("seed", C.c_uint64), ("length_jitter", C.c_double),
+                ("l_max", C.c_int32)]
+
+
+class saber_profile_desc(C.Structure):
+    _fields_ = [("specs", C.POINTER(saber_profile_spec)), ("n_profiles", C.c_int32),
+                ("device", C.c_int32)]
+
+
+class saber_profile_out(C.Structure):
+    _fields_ = [("sample_offsets", C.POINTER(C.c_int64)), ("loads", C.POINTER(C.c_int32)),
+                ("speeds", C.POINTER(C.c_double)), ("capacity", C.c_int64),
+                ("status", C.POINTER(C.c_int32)), ("device_ms", C.c_double)]
+
+
 # (name, restype, argtypes) for every symbol include/saber_cuda.h declares.
 _P = C.POINTER
 SYMBOLS = [
@@ -173,6 +190,8 @@ SYMBOLS = [
     ("saber_cuda_sweep_plan_destroy", None, [C.c_void_p]),
     ("saber_cuda_run_batch", C.c_int, [_P(saber_run_batch_desc), _P(saber_run_batch_out)]),
     ("saber_cuda_fit_batch", C.c_int, [_P(saber_fit_desc), _P(saber_fit_out)]),
+    ("saber_cuda_profile_samples", C.c_int64, [_P(saber_profile_spec)]),
+    ("saber_cuda_profile_batch", C.c_int, [_P(saber_profile_desc), _P(saber_profile_out)]),
     ("saber_cuda_mc_cells", C.c_int64, [_P(saber_mc_desc)]),
     ("saber_cuda_mc_sweep", C.c_int, [_P(saber_mc_desc), _P(saber_mc_out)]),
     ("saber_cuda_mc_trace", C.c_int, [_P(saber_mc_desc), C.c_int64, _P(saber_request),

@@ -790,3 +790,55 @@ def mc_trace(k: int, n_traj: int, grid: SweepGrid, base: SimConfig, arrivals: Bu
                               spec.prefill_rate)
     cfg.seed = spec.seed
     return out, cfg
+
+
+# ---------------------------------------------------------------- profiling
+def _profile_spec(engine: EngineConfig, spec: WorkloadSpec, l_max: int) -> N.saber_profile_spec:
+    s = N.saber_profile_spec()
+    s.ground_truth = _model(engine.ground_truth)
+    s.prefill_rate = engine.prefill_rate
+    s.mix = _mix(spec.mix)
+    s.num_requests = spec.num_requests
+    s.seed = int(spec.seed) & 0xFFFFFFFFFFFFFFFF
+    s.length_jitter = spec.length_jitter
+    s.l_max = l_max
+    return s
+
+
+def profile_batch(items, device: int = 0):
+    """Many profile() calls in one launch: items = [(EngineConfig, WorkloadSpec, l_max)].
+    Returns a list of (loads, speeds) arrays; raises CalibrationError like the
+    reference when a profile yields fewer than 3 distinct loads."""
+    P = len(items)
+    specs = (N.saber_profile_spec * P)(*[_profile_spec(e, w, l) for e, w, l in items])
+    total = 0
+    for k in range(P):
+        c = int(N.lib().saber_cuda_profile_samples(C.byref(specs[k])))
+        if c < 0:
+            raise CalibrationError("profile: " + N.lib().saber_cuda_last_error().decode())
+        total += c
+    offs = np.zeros(P + 1, dtype=np.int64)
+    loads = np.zeros(max(1, total), dtype=np.int32)
+    speeds = np.zeros(max(1, total))
+    status = np.zeros(P, dtype=np.int32)
+    d = N.saber_profile_desc(specs, P, device)
+    o = N.saber_profile_out()
+    o.sample_offsets = offs.ctypes.data_as(C.POINTER(C.c_int64))
+    o.loads = loads.ctypes.data_as(C.POINTER(C.c_int32))
+    o.speeds = speeds.ctypes.data_as(C.POINTER(C.c_double))
+    o.capacity = total
+    o.status = status.ctypes.data_as(C.POINTER(C.c_int32))
+    _check(N.lib().saber_cuda_profile_batch(C.byref(d), C.byref(o)))
+    out = []
+    for k in range(P):
+        if status[k] != 0:
+            raise CalibrationError("profile: insufficient distinct loads (< 3)")
+        out.append((loads[offs[k]:offs[k + 1]].copy(), speeds[offs[k]:offs[k + 1]].copy()))
+    return out
+
+
+def profile(engine_config: EngineConfig, profiling_spec: WorkloadSpec, l_max: int = 50,
+            device: int = 0) -> List[LoadSpeedSample]:
+    """calibration.cpp:58-135 on the GPU."""
+    loads, speeds = profile_batch([(engine_config, profiling_spec, l_max)], device)[0]
+    return [LoadSpeedSample(int(l), float(s)) for l, s in zip(loads, speeds)]

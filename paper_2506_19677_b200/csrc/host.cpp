@@ -1496,3 +1496,150 @@ extern "C" saber_status saber_cuda_mc_sweep(const saber_mc_desc* desc, saber_mc_
   if (e != 0) return fail(SABER_EINTERNAL, "trajectory kernel error " + std::to_string(e));
   return SABER_OK;
 }
+
+// ================================================================ profile ==
+namespace {
+
+struct BurstPlan {
+  std::vector<int32_t> size;
+  std::vector<double> in, out;
+  int64_t issued = 0;
+};
+
+// The burst schedule of profile() (calibration.cpp:72-96): sizes cycle
+// 1..l_max; each burst draws one task, one input and one output length.
+saber_status plan_bursts(const saber_profile_spec& s, BurstPlan* plan) {
+  if (s.l_max < 1) return fail(SABER_EINVAL, "profile: l_max must be >= 1");
+  if (saber_status e = validate_mix(s.mix)) return e;
+  if (s.num_requests < 1) return fail(SABER_EINVAL, "profile: target sample count must be >= 1");
+  if (s.length_jitter < 0.0 || s.length_jitter >= 1.0)
+    return fail(SABER_EINVAL, "length_jitter must be in [0, 1)");
+  if (saber_status e = validate_model(s.ground_truth, "ground truth")) return e;
+  if (!(eval_model(s.ground_truth, 1.0) > 0.0))
+    return fail(SABER_EINVAL, "engine ground truth must be positive");
+  double th[4];
+  int8_t tt[4], tl;
+  mix_thresholds(s.mix, th, tt, &tl);
+  std::mt19937_64 rng(s.seed);
+  auto u01 = [&]() { return static_cast<double>(rng() >> 11) * 0x1.0p-53; };
+  auto jl = [&](int avg) {
+    const double lo = avg * (1.0 - s.length_jitter);
+    const double hi = avg * (1.0 + s.length_jitter);
+    return std::max(1, static_cast<int>(std::llround(lo + u01() * (hi - lo))));
+  };
+  int size = 0;
+  plan->issued = 0;
+  while (plan->issued < s.num_requests) {
+    size = size % s.l_max + 1;
+    const double u = u01();
+    int task = tl;
+    for (int a = 0; a < 4; ++a)
+      if (tt[a] >= 0 && u < th[a]) {
+        task = tt[a];
+        break;
+      }
+    const int in = jl(kAvgInH[task]);
+    const int outl = jl(kAvgOutH[task]);
+    plan->size.push_back(size);
+    plan->in.push_back(static_cast<double>(in));
+    plan->out.push_back(static_cast<double>(outl));
+    plan->issued += size;
+  }
+  return SABER_OK;
+}
+
+}  // namespace
+
+extern "C" int64_t saber_cuda_profile_samples(const saber_profile_spec* spec) {
+  if (!spec) return -1;
+  BurstPlan plan;
+  if (plan_bursts(*spec, &plan) != SABER_OK) return -1;
+  return plan.issued;
+}
+
+extern "C" saber_status saber_cuda_profile_batch(const saber_profile_desc* desc,
+                                                 saber_profile_out* out) {
+  if (!desc || !out || !desc->specs) return fail(SABER_EINVAL, "null argument");
+  const int P = desc->n_profiles;
+  if (P < 1) return fail(SABER_EINVAL, "profile_batch: no profiles");
+  if (!out->sample_offsets || !out->loads || !out->speeds || !out->status)
+    return fail(SABER_EINVAL, "profile_batch: outputs required");
+  std::vector<int64_t> boff(static_cast<size_t>(P) + 1, 0), soff(static_cast<size_t>(P) + 1, 0);
+  std::vector<int32_t> bsize;
+  std::vector<double> bin, bout, prate(static_cast<size_t>(P));
+  int lmax = 1;
+  for (int i = 0; i < P; ++i) lmax = std::max(lmax, desc->specs[i].l_max);
+  const int stride = lmax + 2;
+  std::vector<double> tab(static_cast<size_t>(P) * stride);
+  for (int i = 0; i < P; ++i) {
+    const saber_profile_spec& s = desc->specs[i];
+    BurstPlan plan;
+    if (saber_status e = plan_bursts(s, &plan)) return e;
+    bsize.insert(bsize.end(), plan.size.begin(), plan.size.end());
+    bin.insert(bin.end(), plan.in.begin(), plan.in.end());
+    bout.insert(bout.end(), plan.out.begin(), plan.out.end());
+    boff[static_cast<size_t>(i) + 1] = static_cast<int64_t>(bsize.size());
+    soff[static_cast<size_t>(i) + 1] = soff[static_cast<size_t>(i)] + plan.issued;
+    prate[static_cast<size_t>(i)] = s.prefill_rate;
+    fill_table(s.ground_truth, lmax + 1, &tab[static_cast<size_t>(i) * stride]);
+  }
+  const int64_t S = soff[static_cast<size_t>(P)];
+  std::memcpy(out->sample_offsets, soff.data(), soff.size() * 8);
+  if (out->capacity < S)
+    return fail(SABER_ECAPACITY, "profile_batch: sample buffer too small (" + std::to_string(S) + ")");
+  if (saber_status e = use_device(desc->device)) return e;
+  const int dev = desc->device;
+  DevBuf tables, pr, bo, bs, bi, bt, so, ld, sp;
+  ALLOC_TRY(tables, dev, tab.size() * 8);
+  ALLOC_TRY(pr, dev, prate.size() * 8);
+  ALLOC_TRY(bo, dev, boff.size() * 8);
+  ALLOC_TRY(bs, dev, std::max<size_t>(1, bsize.size()) * 4);
+  ALLOC_TRY(bi, dev, std::max<size_t>(1, bin.size()) * 8);
+  ALLOC_TRY(bt, dev, std::max<size_t>(1, bout.size()) * 8);
+  ALLOC_TRY(so, dev, soff.size() * 8);
+  ALLOC_TRY(ld, dev, static_cast<size_t>(std::max<int64_t>(1, S)) * 4);
+  ALLOC_TRY(sp, dev, static_cast<size_t>(std::max<int64_t>(1, S)) * 8);
+  Timer tm;
+  if (saber_status e = tm.init()) return e;
+  cudaStream_t st = nullptr;
+  CUDA_TRY(cudaEventRecord(tm.a, st));
+  CUDA_TRY(cudaMemcpyAsync(tables.p, tab.data(), tab.size() * 8, cudaMemcpyHostToDevice, st));
+  CUDA_TRY(cudaMemcpyAsync(pr.p, prate.data(), prate.size() * 8, cudaMemcpyHostToDevice, st));
+  CUDA_TRY(cudaMemcpyAsync(bo.p, boff.data(), boff.size() * 8, cudaMemcpyHostToDevice, st));
+  if (!bsize.empty()) {
+    CUDA_TRY(cudaMemcpyAsync(bs.p, bsize.data(), bsize.size() * 4, cudaMemcpyHostToDevice, st));
+    CUDA_TRY(cudaMemcpyAsync(bi.p, bin.data(), bin.size() * 8, cudaMemcpyHostToDevice, st));
+    CUDA_TRY(cudaMemcpyAsync(bt.p, bout.data(), bout.size() * 8, cudaMemcpyHostToDevice, st));
+  }
+  CUDA_TRY(cudaMemcpyAsync(so.p, soff.data(), soff.size() * 8, cudaMemcpyHostToDevice, st));
+  ProfileParams pp{};
+  pp.n_profiles = P;
+  pp.tables = tables.as<double>();
+  pp.table_stride = stride;
+  pp.prefill_rate = pr.as<double>();
+  pp.burst_off = bo.as<int64_t>();
+  pp.burst_size = bs.as<int32_t>();
+  pp.burst_in = bi.as<double>();
+  pp.burst_out = bt.as<double>();
+  pp.sample_off = so.as<int64_t>();
+  pp.loads = ld.as<int32_t>();
+  pp.speeds = sp.as<double>();
+  LAUNCH_TRY(launch_profile(pp, st));
+  if (S > 0) {
+    CUDA_TRY(cudaMemcpyAsync(out->loads, ld.p, static_cast<size_t>(S) * 4, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaMemcpyAsync(out->speeds, sp.p, static_cast<size_t>(S) * 8, cudaMemcpyDeviceToHost, st));
+  }
+  CUDA_TRY(cudaEventRecord(tm.b, st));
+  CUDA_TRY(cudaEventSynchronize(tm.b));
+  float ms = 0.f;
+  CUDA_TRY(cudaEventElapsedTime(&ms, tm.a, tm.b));
+  out->device_ms = ms;
+  for (int i = 0; i < P; ++i) {  // profile(): < 3 distinct loads -> CalibrationError
+    std::vector<int32_t> l(out->loads + soff[static_cast<size_t>(i)],
+                           out->loads + soff[static_cast<size_t>(i) + 1]);
+    std::sort(l.begin(), l.end());
+    const int64_t distinct = std::unique(l.begin(), l.end()) - l.begin();
+    out->status[i] = distinct < 3 ? 1 : 0;
+  }
+  return SABER_OK;
+}

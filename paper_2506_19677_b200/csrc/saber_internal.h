@@ -231,6 +231,22 @@ int launch_mc_workloads(const McParams& p, void* stream);
 int launch_mc_reduce(const McParams& p, const saber_traj_row* rows, const double* comp,
                      int64_t* stats, int64_t* hist, void* stream);
 
+// Batched profile() (profile_kernel.cu).
+struct ProfileParams {
+  int32_t n_profiles;
+  const double* tables;        // [n_profiles][table_stride] ground-truth predict tables
+  int32_t table_stride;
+  const double* prefill_rate;  // [n_profiles]
+  const int64_t* burst_off;    // [n_profiles + 1]
+  const int32_t* burst_size;   // [bursts]
+  const double* burst_in;      // [bursts] input tokens
+  const double* burst_out;     // [bursts] output tokens
+  const int64_t* sample_off;   // [n_profiles + 1]
+  int32_t* loads;              // [samples]
+  double* speeds;              // [samples]
+};
+int launch_profile(const ProfileParams& p, void* stream);
+
 // Fitting.
 struct FitParams {
   const int32_t* loads;

@@ -102,3 +102,27 @@ def test_calibrate_profiled_samples_matches_reference(engine, ref):
     a = logistic_sse(rep.fits[1].model.params, L, speeds)
     b = logistic_sse(cal["params"][1], L, speeds)
     assert abs(a - b) <= LOGISTIC_SSE_RTOL * b
+
+
+def test_profile_batch_matches_reference(engine, ref):
+    """profile() (calibration.cpp:58-135) on the GPU, bit-exact, over ground
+    truths of every family, prefill on/off, several mixes, seeds and l_max."""
+    S = engine
+    items, orc_args = [], []
+    for k, (gt, pr, mix, n, l_max) in enumerate([
+            ((0, (100.0, 0.05, 0.001)), 2000.0, "w3", 1000, 50),
+            ((0, (80.0, 0.12, 0.002)), 0.0, "w1", 400, 20),
+            ((1, (120.0, 0.1, 30.0)), 2000.0, "w2", 700, 50),
+            ((2, (-0.8, 100.8, 0.0)), 500.0, "w3", 300, 12),
+            ((0, (100.0, 0.05, 0.001)), 2000.0, "w3", 1000, 50)]):
+        seed = 42 if k == 0 else 1000 + k
+        items.append((S.EngineConfig(S.SpeedModel(gt[0], gt[1]), pr),
+                      S.WorkloadSpec(S.preset_mix(mix), 1.0, n, seed, 0.2), l_max))
+        orc_args.append(dict(gt=gt, prefill_rate=pr, mix=mix, num_requests=n, seed=seed, l_max=l_max))
+    got = S.profile_batch(items)
+    for (loads, speeds), a in zip(got, orc_args):
+        rl, rs = ref.profile(**a)
+        assert np.array_equal(loads, rl) and np.array_equal(speeds, rs), a
+    # the full calibration pipeline on the device reproduces SURVEY §8(d)
+    rep = S.calibrate(list(zip(got[0][0].tolist(), got[0][1].tolist())))
+    assert list(rep.best.params) == [99.999999999997357, 0.049999999999992085, 0.0010000000000001078]
