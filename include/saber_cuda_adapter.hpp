@@ -258,4 +258,98 @@ inline SweepResult sweep(const SweepGrid& grid, const SimConfig& base, int jobs 
   return res;
 }
 
+// estimator.hpp:61.  Throws FitError with the reference's payload.
+inline SpeedModel fit(const std::vector<LoadSpeedSample>& samples, ModelFamily family,
+                      int device = 0) {
+  std::vector<int32_t> loads(samples.size());
+  std::vector<double> speeds(samples.size());
+  for (size_t i = 0; i < samples.size(); ++i) {
+    loads[i] = samples[i].load;
+    speeds[i] = samples[i].speed;
+  }
+  const int64_t offsets[2] = {0, static_cast<int64_t>(samples.size())};
+  const int f = static_cast<int>(family);
+  saber_fit_desc d{loads.data(), speeds.data(), offsets, 1, 1 << f, 0, device};
+  double params[9] = {}, r2[3] = {};
+  int32_t status[3] = {};
+  saber_fit_out o{};
+  o.params = params;
+  o.r2 = r2;
+  o.status = status;
+  detail::check(saber_cuda_fit_batch(&d, &o));
+  const std::array<double, 3> p = {params[3 * f], params[3 * f + 1], params[3 * f + 2]};
+  if (status[f] != 0)
+    throw FitError(std::string("fit failed for ") + to_string(family), family, p, r2[f]);
+  SpeedModel m;
+  m.family = family;
+  m.params = p;
+  m.fit_r2 = r2[f];
+  return m;
+}
+
+// calibration.hpp:54
+inline CalibrationReport calibrate(const std::vector<LoadSpeedSample>& samples, int device = 0) {
+  std::vector<int32_t> loads(samples.size());
+  std::vector<double> speeds(samples.size());
+  for (size_t i = 0; i < samples.size(); ++i) {
+    loads[i] = samples[i].load;
+    speeds[i] = samples[i].speed;
+  }
+  const int64_t offsets[2] = {0, static_cast<int64_t>(samples.size())};
+  saber_fit_desc d{loads.data(), speeds.data(), offsets, 1, 7, 1, device};
+  double params[9] = {}, r2[3] = {};
+  int32_t status[3] = {}, best = -1;
+  saber_fit_out o{};
+  o.params = params;
+  o.r2 = r2;
+  o.status = status;
+  o.best_family = &best;
+  detail::check(saber_cuda_fit_batch(&d, &o));
+  if (best == -2) throw CalibrationError("calibrate: insufficient distinct loads");
+  if (best == -1) throw CalibrationError("calibrate: no model family produced a fit");
+  CalibrationReport rep;
+  for (int f = 0; f < 3; ++f) {
+    FamilyFit e;
+    e.family = static_cast<ModelFamily>(f);
+    e.ok = status[f] == 0;
+    if (e.ok) {
+      e.model.family = e.family;
+      e.model.params = {params[3 * f], params[3 * f + 1], params[3 * f + 2]};
+      e.model.fit_r2 = r2[f];
+    } else {
+      e.error = std::string("fit failed for ") + to_string(e.family);
+    }
+    rep.fits.push_back(e);
+  }
+  rep.best = rep.fits[static_cast<size_t>(best)].model;
+  return rep;
+}
+
+// calibration.hpp:29-31
+inline std::vector<LoadSpeedSample> profile(const EngineConfig& engine_config,
+                                            const WorkloadSpec& profiling_spec, int l_max = 50,
+                                            int device = 0) {
+  saber_profile_spec s{};
+  s.ground_truth = detail::model_of(engine_config.ground_truth);
+  s.prefill_rate = engine_config.prefill_rate;
+  s.mix = detail::mix_of(profiling_spec.mix);
+  s.num_requests = profiling_spec.num_requests;
+  s.seed = profiling_spec.seed;
+  s.length_jitter = profiling_spec.length_jitter;
+  s.l_max = l_max;
+  const int64_t n = saber_cuda_profile_samples(&s);
+  if (n < 0) throw CalibrationError(saber_cuda_last_error());
+  std::vector<int32_t> loads(static_cast<size_t>(n));
+  std::vector<double> speeds(static_cast<size_t>(n));
+  int64_t offs[2] = {0, 0};
+  int32_t status = 0;
+  saber_profile_desc d{&s, 1, device};
+  saber_profile_out o{offs, loads.data(), speeds.data(), n, &status, 0.0};
+  detail::check(saber_cuda_profile_batch(&d, &o));
+  if (status != 0) throw CalibrationError("profile: insufficient distinct loads (< 3)");
+  std::vector<LoadSpeedSample> out(static_cast<size_t>(n));
+  for (int64_t i = 0; i < n; ++i) out[static_cast<size_t>(i)] = {loads[static_cast<size_t>(i)], speeds[static_cast<size_t>(i)]};
+  return out;
+}
+
 }  // namespace saber::cuda

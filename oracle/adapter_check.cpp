@@ -94,6 +94,34 @@ int main() {
     const saber::SweepResult b = saber::cuda::sweep(grid, base, 0);
     expect(saber::results_to_csv(a.rows) == saber::results_to_csv(b.rows), "sweep results.csv");
     expect(saber::summary_to_json(a) == saber::summary_to_json(b), "sweep summary.json");
+
+    // The calibration pipeline: profile -> calibrate (USL and linear are
+    // bit-exact; the logistic evaluates exp(), compared by its r^2 only).
+    saber::EngineConfig ec;
+    saber::WorkloadSpec prof;
+    prof.mix = saber::preset_mix("w3");
+    prof.num_requests = 1000;
+    prof.seed = 20260816;
+    const auto sa = saber::profile(ec, prof, 50);
+    const auto sb = saber::cuda::profile(ec, prof, 50);
+    expect(saber::samples_to_csv(sa) == saber::samples_to_csv(sb), "profile samples.csv");
+    const auto ca = saber::calibrate(sa);
+    const auto cb = saber::cuda::calibrate(sb);
+    expect(saber::to_json(ca.best) == saber::to_json(cb.best), "calibrate best_model.json");
+    for (int f : {0, 2})
+      expect(saber::to_json(ca.fits[f].model) == saber::to_json(cb.fits[f].model),
+             std::string("calibrate family ") + std::to_string(f));
+    expect(std::abs(*ca.fits[1].model.fit_r2 - *cb.fits[1].model.fit_r2) < 1e-9, "logistic r2");
+    const auto fa = saber::fit(sa, saber::ModelFamily::Usl);
+    const auto fb = saber::cuda::fit(sb, saber::ModelFamily::Usl);
+    expect(saber::to_json(fa) == saber::to_json(fb), "fit usl");
+    bool threw = false;
+    try {
+      saber::cuda::fit({{1, 10.0}, {2, 12.0}}, saber::ModelFamily::Linear);
+    } catch (const saber::FitError& e) {
+      threw = e.family == saber::ModelFamily::Linear;
+    }
+    expect(threw, "FitError for an increasing linear fit");
   } catch (const std::exception& e) {
     std::printf("EXCEPTION %s\n", e.what());
     return 2;
