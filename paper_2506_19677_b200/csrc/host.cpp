@@ -366,7 +366,7 @@ struct saber_sweep_plan {
 
   Workloads wl;
   DevBuf tables, seeds, s_off, s_len, draws, descs, rows, comp, cursor, err, caps_d;
-  DevBuf summary, best_cap, cell_scratch, ratios;
+  DevBuf summary, best_cap, cell_scratch, ratios, order;
   Scratch scratch;
   Timer all, sim;
   double last_ms = 0.0, sim_ms = 0.0;
@@ -531,6 +531,30 @@ saber_status saber_cuda_sweep_plan_create(const saber_sweep_desc* desc, saber_sw
   }
   if (saber_status s = P->scratch.alloc(dev, n)) return s;
 
+  // Longest-first execution order: the kernel time is set by
+  // the last trajectories to finish, and a trajectory's tick count grows with
+  // its arrival span n / rps, so low rates start first (SABER before static
+  // at equal rate: its ticks carry the gate's decisions).
+  {
+    const int per_rps = desc->n_caps * R + (desc->with_saber ? R : 0);
+    std::vector<std::pair<double, int32_t>> key(static_cast<size_t>(P->rows_shard));
+    for (int64_t k = 0; k < P->rows_shard; ++k) {
+      const int64_t r = desc->shard_index + k * desc->shard_count;
+      const int ri = static_cast<int>((r / per_rps) % n_rps);
+      const bool sab = (r % per_rps) >= desc->n_caps * R;
+      key[static_cast<size_t>(k)] = {-(n / P->rps[static_cast<size_t>(ri)]) - (sab ? 1.0 : 0.0),
+                                     static_cast<int32_t>(k)};
+    }
+    std::stable_sort(key.begin(), key.end(),
+                     [](const auto& a, const auto& b) { return a.first < b.first; });
+    std::vector<int32_t> ord(key.size());
+    for (size_t k = 0; k < key.size(); ++k) ord[k] = key[k].second;
+    ALLOC_TRY(P->order, dev, std::max<size_t>(1, ord.size()) * 4);
+    if (!ord.empty())
+      CUDA_TRY(cudaMemcpy(P->order.p, ord.data(), ord.size() * 4, cudaMemcpyHostToDevice));
+    P->h2d_bytes += static_cast<int64_t>(ord.size() * 4);
+  }
+
   CUDA_TRY(cudaMemcpy(P->wl.items.p, items.data(), items.size() * sizeof(WorkloadItem),
                       cudaMemcpyHostToDevice));
   CUDA_TRY(cudaMemcpy(P->wl.seed_base.p, base.data(), base.size() * 8, cudaMemcpyHostToDevice));
@@ -635,6 +659,7 @@ saber_status saber_cuda_sweep_plan_run(saber_sweep_plan* P, void* stream) {
   sp.out.completion = P->comp.as<double>();
   sp.out.error = P->err.as<int32_t>();
   sp.next_traj = P->cursor.as<int32_t>();
+  sp.order = P->order.as<int32_t>();
   CUDA_TRY(cudaEventRecord(P->sim.a, s));
   LAUNCH_TRY(launch_sim(sp, P->scratch.launch, s));
   CUDA_TRY(cudaEventRecord(P->sim.b, s));

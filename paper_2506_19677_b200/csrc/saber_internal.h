@@ -91,6 +91,7 @@ struct SimParams {
   int32_t slot_rows;          // ceil(nmax / G): shared-memory slot rows per warp
   SimOutputs out;
   int32_t* next_traj;         // work-queue cursor (device)
+  const int32_t* order;       // execution order of the descriptors (longest first), or null
 };
 
 // Error codes written to SimOutputs::error.

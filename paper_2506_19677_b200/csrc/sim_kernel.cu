@@ -67,7 +67,7 @@ __device__ __forceinline__ void simulate_one(const SimParams& P, int ti, const S
                                              double* __restrict__ LNEED,
                                              uint16_t* __restrict__ LOW,
                                              const uint32_t* __restrict__ INV) {
-  const TrajDesc d = P.traj[ti];
+  const TrajDesc d = P.traj[P.order ? P.order[ti] : ti];
   const int n = d.n;
   const int nmax = P.wl.nmax;
   const int64_t wo = static_cast<int64_t>(d.workload) * nmax;
@@ -108,6 +108,9 @@ __device__ __forceinline__ void simulate_one(const SimParams& P, int ti, const S
   double rem_lb = kInf;   // lower bound on min (max_out - generated) over decode slots
   bool rem_exact = true;  // rem_lb is the exact minimum
   double m_hi = 0.0;      // >= max_output_tokens of every active slot
+  // speed_A caches predict(gt, A); it changes only with A.
+  double speed_A = 0.0;
+  auto retune = [&]() { speed_A = GT[A]; };
 
   int next = 0;
   double na_t = n > 0 ? ARR[0] : kInf;
@@ -136,6 +139,7 @@ __device__ __forceinline__ void simulate_one(const SimParams& P, int ti, const S
     m_hi = (m_hi < m) ? m : m_hi;
     S.m[s] = dbits(m) | static_cast<uint64_t>(id);
     ++A;
+    retune();
     if (kRecords && ADM && leader) ADM[id] = now;
   };
 
@@ -194,43 +198,85 @@ __device__ __forceinline__ void simulate_one(const SimParams& P, int ti, const S
         // Fisher-Yates over the window: j = rng() % (i+1) for i = w-1..1.
         // Draws are stored mod lcm(1..16); x % d is exact via the reciprocal
         // table (x < 2^20).
-        for (int i = w - 1; i >= 1; --i) {
-          const uint32_t x = draws[draw_pos++];
-          const uint32_t d1 = static_cast<uint32_t>(i + 1);
-          const uint32_t j = x - __umulhi(x, INV[d1]) * d1;
-          const uint64_t a = (ord >> (4 * i)) & 15ull;
-          const uint64_t bb = (ord >> (4 * j)) & 15ull;
-          const uint64_t x2 = a ^ bb;
-          ord ^= (x2 << (4 * i)) | (x2 << (4 * j));
+        // All w-1 draws are independent loads, issued before the shuffle
+        // consumes them (the loop over draw index q is unrolled, so the
+        // registers are indexed statically).
+        uint32_t xq[kMaxWindow - 1];
+#pragma unroll
+        for (int q = 0; q < kMaxWindow - 1; ++q) xq[q] = q < w - 1 ? draws[draw_pos + q] : 0u;
+#pragma unroll
+        for (int q = 0; q < kMaxWindow - 1; ++q) {
+          if (q < w - 1) {
+            const int i = w - 1 - q;
+            const uint32_t d1 = static_cast<uint32_t>(i + 1);
+            const uint32_t j = xq[q] - __umulhi(xq[q], INV[d1]) * d1;
+            const uint64_t a = (ord >> (4 * i)) & 15ull;
+            const uint64_t bb = (ord >> (4 * j)) & 15ull;
+            const uint64_t x2 = a ^ bb;
+            ord ^= (x2 << (4 * i)) | (x2 << (4 * j));
+          }
         }
+        draw_pos += w - 1;
         rng_draws += w - 1;
         const double pred = MT[load + 1];
         const bool violates = pred < ledger_max;  // ActiveLedger::violates
         ledger_scanned += ledger_size;
-        for (int c = 0; c < w; ++c) {
-          const int pos = static_cast<int>((ord >> (4 * c)) & 15ull);
-          const int id = high.select(pos);
+        // The gate (scheduler.cpp:71-94), evaluated for the whole window at
+        // once: lane sub of the group takes shuffled positions c = sub + G*q.
+        // Candidate c is admitted iff it is the first with pred >= need and no
+        // ledger violation; decisions are then emitted in shuffled order.
+        constexpr int kQ = (kMaxWindow + G - 1) / G;
+        int cid[kQ];
+        double cneed[kQ];
+        unsigned okmask = 0;
+#pragma unroll
+        for (int q = 0; q < kQ; ++q) {
+          const int c = sub + G * q;
+          cid[q] = 0;
+          cneed[q] = 0.0;
+          if (c < w) {
+            cid[q] = high.select(static_cast<int>((ord >> (4 * c)) & 15ull));
+            cneed[q] = queued_need(MO[cid[q]], DL[cid[q]], t);
+            if (!(pred < cneed[q]) && !violates) okmask |= 1u << c;
+          }
+        }
+        if (G > 1) okmask = __reduce_or_sync(gmask, okmask);
+        const int first = okmask ? __ffs(okmask) - 1 : w;  // admitted position, or none
+        const int last = first < w ? first : w - 1;
+        for (int c = 0; c <= last; ++c) {
+          int id;
+          double need;
+          if (G == 1) {
+            id = cid[c];
+            need = cneed[c];
+          } else {
+            const int q = c / G;
+            int myid = cid[0];
+            double myneed = cneed[0];
+#pragma unroll
+            for (int qq = 1; qq < kQ; ++qq)
+              if (qq == q) {
+                myid = cid[qq];
+                myneed = cneed[qq];
+              }
+            id = __shfl_sync(gmask, myid, S.col0 + (c % G));
+            need = __shfl_sync(gmask, myneed, S.col0 + (c % G));
+          }
           ++cands;
-          const double need = queued_need(MO[id], DL[id], t);
-          if (pred < need) {
-            push_decision<kTrace>(L, t, id, SABER_REJECT_OWN, load, dbits(pred), dbits(need),
-                                  tr, P.out.trace_cap, P.out.error, leader);
-            continue;
+          if (c < first) {
+            push_decision<kTrace>(L, t, id, pred < need ? SABER_REJECT_OWN : SABER_REJECT_ACTIVE,
+                                  load, dbits(pred), dbits(need), tr, P.out.trace_cap, P.out.error,
+                                  leader);
+          } else {
+            admit(id, t);
+            ledger.set(id);
+            ++ledger_size;
+            LNEED[id] = need;
+            ledger_max = (ledger_max < need) ? need : ledger_max;
+            high.reset(id);
+            push_decision<kTrace>(L, t, id, SABER_ADMIT_HIGH, load, dbits(pred), dbits(need), tr,
+                                  P.out.trace_cap, P.out.error, leader);
           }
-          if (violates) {
-            push_decision<kTrace>(L, t, id, SABER_REJECT_ACTIVE, load, dbits(pred), dbits(need),
-                                  tr, P.out.trace_cap, P.out.error, leader);
-            continue;
-          }
-          admit(id, t);
-          ledger.set(id);
-          ++ledger_size;
-          LNEED[id] = need;
-          ledger_max = (ledger_max < need) ? need : ledger_max;
-          high.reset(id);
-          push_decision<kTrace>(L, t, id, SABER_ADMIT_HIGH, load, dbits(pred), dbits(need), tr,
-                                P.out.trace_cap, P.out.error, leader);
-          break;
         }
       } else if (low_head < low_tail) {
         // admission_step, low tier (scheduler.cpp:97-108).
@@ -263,8 +309,8 @@ __device__ __forceinline__ void simulate_one(const SimParams& P, int ti, const S
         break;
       }
       ++passes;
-      const double speed = GT[A];
       double dt = nt - clock;
+      const double speed = speed_A;
       if (min_pf < dt) dt = min_pf;
       // Quiet pass: no prefill ends (min_pf is exact) and the
       // lower bound on min(max_out - generated) proves both that the decode
@@ -381,6 +427,7 @@ __device__ __forceinline__ void simulate_one(const SimParams& P, int ti, const S
           __syncwarp(gmask);
         }
         A -= 1;
+        retune();
         completed += 1;
       } else if (ndone) {
         // Several completions in one pass (lockstep bursts): every lane
@@ -415,6 +462,7 @@ __device__ __forceinline__ void simulate_one(const SimParams& P, int ti, const S
         }
         __syncwarp(gmask);
         A -= static_cast<int>(ndone);
+        retune();
         completed += static_cast<int>(ndone);
         if (dirty) {
           double mx = -kInf;

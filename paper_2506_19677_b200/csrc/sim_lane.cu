@@ -76,7 +76,7 @@ __global__ void __launch_bounds__(kLaneBlock) sim_lane_kernel(const SimParams P)
     base = g.shfl(base, 0);
     ti = base + static_cast<int>(g.thread_rank());
     if (ti >= P.n_traj) return false;
-    d = P.traj[ti];
+    d = P.traj[P.order ? P.order[ti] : ti];
     n = d.n;
     const int64_t wo = static_cast<int64_t>(d.workload) * nmax;
     ARR = P.wl.arrival + wo;
