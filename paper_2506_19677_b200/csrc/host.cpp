@@ -17,6 +17,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <ctime>
 #include <map>
 #include <memory>
 #include <mutex>
@@ -53,19 +54,55 @@ saber_status fail(saber_status s, const std::string& msg) {
 
 // ---------------------------------------------------------------- devices --
 saber_status use_device(int device) {
+  // Validated once per device (cudaGetDeviceProperties costs milliseconds and
+  // would sit inside every one-shot call's timed region).
+  static std::mutex mu;
+  static std::vector<int> ok;
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    if (device >= 0 && device < static_cast<int>(ok.size()) && ok[static_cast<size_t>(device)]) {
+      CUDA_TRY(cudaSetDevice(device));
+      return SABER_OK;
+    }
+  }
   int count = 0;
   cudaError_t e = cudaGetDeviceCount(&count);
   if (e != cudaSuccess || count == 0)
-    return fail(SABER_ECUDA, "no CUDA device available (the engine has no CPU fallback)");
+    return fail(SABER_ECUDA, std::string("no CUDA device: ") + cudaGetErrorString(e));
   if (device < 0 || device >= count)
     return fail(SABER_EINVAL, "device ordinal " + std::to_string(device) + " out of range");
-  cudaDeviceProp prop;
-  CUDA_TRY(cudaGetDeviceProperties(&prop, device));
-  if (prop.major != 10)
+  int major = 0;
+  CUDA_TRY(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, device));
+  if (major != 10) {
+    cudaDeviceProp prop;
+    CUDA_TRY(cudaGetDeviceProperties(&prop, device));
     return fail(SABER_ECUDA, std::string("device is not sm_100 (Blackwell): ") + prop.name);
+  }
   CUDA_TRY(cudaSetDevice(device));
+  std::lock_guard<std::mutex> lk(mu);
+  if (static_cast<int>(ok.size()) < count) ok.resize(static_cast<size_t>(count), 0);
+  ok[static_cast<size_t>(device)] = 1;
   return SABER_OK;
 }
+
+// Phase timings of the host path (SABER_HOST_TRACE=1 prints them to stderr).
+struct HostTrace {
+  bool on;
+  double t0;
+  const char* what;
+  static double now() {
+    timespec ts;
+    clock_gettime(CLOCK_MONOTONIC, &ts);
+    return ts.tv_sec * 1e3 + ts.tv_nsec * 1e-6;
+  }
+  explicit HostTrace(const char* w) : on(std::getenv("SABER_HOST_TRACE") != nullptr), t0(now()), what(w) {}
+  void mark(const char* phase) {
+    if (!on) return;
+    const double t = now();
+    std::fprintf(stderr, "[saber host] %s %s %.3f ms\n", what, phase, t - t0);
+    t0 = t;
+  }
+};
 
 // -------------------------------------------------- grow-only device cache --
 struct Block {
@@ -257,7 +294,7 @@ int nwords_for(int n) {
   if (n <= 64) return 1;
   if (n <= 128) return 2;
   if (n <= 256) return 4;
-  return 8;
+  return 32;
 }
 
 // ---------------------------------------------------------- group scratch --
@@ -266,9 +303,9 @@ int group_size() {
   const char* e = std::getenv("SABER_GROUP");
   if (e) {
     const int g = std::atoi(e);
-    if (g == 1 || g == 2 || g == 4 || g == 8 || g == 16) return g;
+    if (g == 1 || g == 2 || g == 4 || g == 8 || g == 16 || g == 32) return g;
   }
-  return 8;
+  return 32;
 }
 
 struct Scratch {
@@ -329,6 +366,46 @@ struct Workloads {
   }
 };
 
+// Tick table for quiet streaks (saber_internal.h TickTable):
+// T[k] = fl(T[k-1] + tick) exactly as simloop.cpp:99-100 accumulates t, up to
+// a bound on every horizon of the launch (beyond it streaks simply stop).
+struct TickTableBuf {
+  DevBuf T, DT;
+  TickTable view{};
+  int64_t bytes = 0;
+  saber_status build(int dev, double tick, double hbound) {
+    view = TickTable{};
+    bytes = 0;
+    if (std::getenv("SABER_NO_STREAK")) return SABER_OK;
+    if (!(tick > 0.0) || !(hbound > 0.0)) return SABER_OK;
+    double est = hbound / tick * (1.0 + 1e-9) + 8.0;
+    if (!(est < static_cast<double>(1 << 22))) est = static_cast<double>(1 << 22);
+    const int len = static_cast<int>(est);
+    if (len < 4) return SABER_OK;
+    std::vector<double> t(static_cast<size_t>(len)), dt(static_cast<size_t>(len - 1));
+    t[0] = 0.0;
+    double dmax = 0.0;
+    for (int k = 1; k < len; ++k) {
+      t[static_cast<size_t>(k)] = t[static_cast<size_t>(k - 1)] + tick;
+      const double d = t[static_cast<size_t>(k)] - t[static_cast<size_t>(k - 1)];
+      dt[static_cast<size_t>(k - 1)] = d;
+      dmax = std::max(dmax, d);
+    }
+    ALLOC_TRY(T, dev, t.size() * 8);
+    ALLOC_TRY(DT, dev, dt.size() * 8);
+    CUDA_TRY(cudaMemcpy(T.p, t.data(), t.size() * 8, cudaMemcpyHostToDevice));
+    CUDA_TRY(cudaMemcpy(DT.p, dt.data(), dt.size() * 8, cudaMemcpyHostToDevice));
+    view.T = T.as<double>();
+    view.DT = DT.as<double>();
+    view.len = len;
+    view.tick = tick;
+    view.inv_tick = 1.0 / tick;
+    view.dt_max = dmax;
+    bytes = static_cast<int64_t>((t.size() + dt.size()) * 8);
+    return SABER_OK;
+  }
+};
+
 struct Timer {
   cudaEvent_t a = nullptr, b = nullptr;
   ~Timer() {
@@ -368,6 +445,7 @@ struct saber_sweep_plan {
   DevBuf tables, seeds, s_off, s_len, draws, descs, rows, comp, cursor, err, caps_d;
   DevBuf summary, best_cap, cell_scratch, ratios, order;
   Scratch scratch;
+  TickTableBuf ticktab;
   Timer all, sim;
   double last_ms = 0.0, sim_ms = 0.0;
   int launches = 0;
@@ -427,7 +505,9 @@ saber_status saber_cuda_sweep_plan_create(const saber_sweep_desc* desc, saber_sw
   if (!desc || !out) return fail(SABER_EINVAL, "null argument");
   *out = nullptr;
   if (saber_status s = validate_sweep(*desc)) return s;
+  HostTrace tr("sweep_plan_create");
   if (saber_status s = use_device(desc->device)) return s;
+  tr.mark("use_device");
   auto* P = new saber_sweep_plan();
   std::unique_ptr<saber_sweep_plan> guard(P);
   P->desc = *desc;
@@ -454,6 +534,7 @@ saber_status saber_cuda_sweep_plan_create(const saber_sweep_desc* desc, saber_sw
     seed_draws(desc->seed + static_cast<uint64_t>(i), n, &base[static_cast<size_t>(i) * n * 4],
                &neglog_sum[static_cast<size_t>(i)]);
 
+  tr.mark("seed_draws");
   // Predict tables: [gt | model], index L in 1..n+1.
   const int tl = n + 2;
   std::vector<double> tab(static_cast<size_t>(2 * tl));
@@ -505,6 +586,17 @@ saber_status saber_cuda_sweep_plan_create(const saber_sweep_desc* desc, saber_sw
     }
   }
 
+  // Horizon bound over every seed (tick table length).
+  double hb_max = 0.0;
+  {
+    double rmin = P->rps[0];
+    for (double r : P->rps) rmin = std::min(rmin, r);
+    for (int i = 0; i < R; ++i) {
+      const double last = neglog_sum[static_cast<size_t>(i)] / rmin * (1.0 + 1e-9) + n * 1e-6;
+      hb_max = std::max(hb_max, desc->has_horizon ? desc->horizon : last + 10.0 * 12.0 + 1.0);
+    }
+  }
+  tr.mark("host tables");
   // Device buffers.
   if (saber_status s = P->wl.alloc(dev, P->n_items, n)) return s;
   ALLOC_TRY(P->wl.items, dev, items.size() * sizeof(WorkloadItem));
@@ -529,7 +621,9 @@ saber_status saber_cuda_sweep_plan_create(const saber_sweep_desc* desc, saber_sw
     ALLOC_TRY(P->s_len, dev, off.size() * 8);
     ALLOC_TRY(P->draws, dev, static_cast<size_t>(std::max<int64_t>(1, P->total_draws)) * 4);
   }
+  tr.mark("device buffers");
   if (saber_status s = P->scratch.alloc(dev, n)) return s;
+  tr.mark("scratch + kernel plan");
 
   // Longest-first execution order: the kernel time is set by
   // the last trajectories to finish, and a trajectory's tick count grows with
@@ -555,6 +649,7 @@ saber_status saber_cuda_sweep_plan_create(const saber_sweep_desc* desc, saber_sw
     P->h2d_bytes += static_cast<int64_t>(ord.size() * 4);
   }
 
+  tr.mark("order");
   CUDA_TRY(cudaMemcpy(P->wl.items.p, items.data(), items.size() * sizeof(WorkloadItem),
                       cudaMemcpyHostToDevice));
   CUDA_TRY(cudaMemcpy(P->wl.seed_base.p, base.data(), base.size() * 8, cudaMemcpyHostToDevice));
@@ -569,11 +664,16 @@ saber_status saber_cuda_sweep_plan_create(const saber_sweep_desc* desc, saber_sw
     CUDA_TRY(cudaMemcpy(P->s_off.p, off.data(), off.size() * 8, cudaMemcpyHostToDevice));
     CUDA_TRY(cudaMemcpy(P->s_len.p, P->stream_len.data(), off.size() * 8, cudaMemcpyHostToDevice));
   }
-  P->h2d_bytes = static_cast<int64_t>(items.size() * sizeof(WorkloadItem) + base.size() * 8 +
+  P->h2d_bytes += static_cast<int64_t>(items.size() * sizeof(WorkloadItem) + base.size() * 8 +
                                       th.size() * 8 + tt.size() + tlast.size() + tab.size() * 8 +
                                       P->caps.size() * 4 + seeds.size() * 8 + off.size() * 16);
+  tr.mark("h2d");
+  if (saber_status s = P->ticktab.build(dev, desc->tick, hb_max)) return s;
+  P->h2d_bytes += P->ticktab.bytes;
+  tr.mark("tick table");
   if (saber_status s = P->all.init()) return s;
   if (saber_status s = P->sim.init()) return s;
+  tr.mark("events");
   *out = guard.release();
   return SABER_OK;
 }
@@ -660,6 +760,7 @@ saber_status saber_cuda_sweep_plan_run(saber_sweep_plan* P, void* stream) {
   sp.out.error = P->err.as<int32_t>();
   sp.next_traj = P->cursor.as<int32_t>();
   sp.order = P->order.as<int32_t>();
+  sp.ticks = P->ticktab.view;
   CUDA_TRY(cudaEventRecord(P->sim.a, s));
   LAUNCH_TRY(launch_sim(sp, P->scratch.launch, s));
   CUDA_TRY(cudaEventRecord(P->sim.b, s));
@@ -885,6 +986,7 @@ extern "C" saber_status saber_cuda_run_batch(const saber_run_batch_desc* desc,
   const int tl = nmax + 2;
   std::vector<double> tab(static_cast<size_t>(T) * 2 * tl);
   std::vector<TrajDesc> descs(static_cast<size_t>(T));
+  std::vector<std::pair<double, double>> tick_hb;  // (tick, horizon bound) per trajectory
   std::vector<uint64_t> seeds;
   std::vector<int64_t> off, len;
   int64_t total_draws = 0;
@@ -943,8 +1045,9 @@ extern "C" saber_status saber_cuda_run_batch(const saber_run_batch_desc* desc,
     d.prefill_rate = s.prefill_rate;
     d.row = k;
     d.stream = -1;
+    const double hb = s.has_horizon ? s.horizon : last_bound + 10.0 * max_sla + 1.0;
+    tick_hb.emplace_back(s.tick, hb);
     if (s.mode == SABER_MODE_SABER) {
-      const double hb = s.has_horizon ? s.horizon : last_bound + 10.0 * max_sla + 1.0;
       d.stream = static_cast<int32_t>(seeds.size());
       seeds.push_back(s.seed ^ kSchedulerSeedSalt);
       off.push_back(total_draws);
@@ -992,6 +1095,26 @@ extern "C" saber_status saber_cuda_run_batch(const saber_run_batch_desc* desc,
   for (size_t i = 0; i < cells; ++i)
     if (!(mo[i] <= kLaneMaxOutput)) lane_ok = false;
   if (saber_status s = scratch.alloc(dev, nmax, lane_ok)) return s;
+  // One tick table, for the most common tick of the batch.
+  TickTableBuf ticktab;
+  {
+    std::map<double, std::pair<int, double>> by_tick;
+    for (const auto& th_ : tick_hb) {
+      auto& e = by_tick[th_.first];
+      e.first += 1;
+      e.second = std::max(e.second, th_.second);
+    }
+    double best_tick = 0.0, best_hb = 0.0;
+    int best_n = 0;
+    for (const auto& e : by_tick)
+      if (e.second.first > best_n) {
+        best_n = e.second.first;
+        best_tick = e.first;
+        best_hb = e.second.second;
+      }
+    if (best_n > 0)
+      if (saber_status s = ticktab.build(dev, best_tick, best_hb)) return s;
+  }
 
   CUDA_TRY(cudaMemcpy(wl.items.p, items.data(), items.size() * sizeof(WorkloadItem), cudaMemcpyHostToDevice));
   CUDA_TRY(cudaMemcpy(wl.seed_base.p, base.data(), base.size() * 8, cudaMemcpyHostToDevice));
@@ -1075,6 +1198,7 @@ extern "C" saber_status saber_cuda_run_batch(const saber_run_batch_desc* desc,
   sp.out.trace_cap = trace ? out->decision_cap : 0;
   sp.out.error = err_d.as<int32_t>();
   sp.next_traj = cursor_d.as<int32_t>();
+  sp.ticks = ticktab.view;
   LAUNCH_TRY(launch_sim(sp, scratch.launch, st));
   ++launches;
   RowMetricsParams rm{};
@@ -1422,12 +1546,16 @@ extern "C" saber_status saber_cuda_mc_sweep(const saber_mc_desc* desc, saber_mc_
   CUDA_TRY(cudaMemsetAsync(err.p, 0, 16, st));
   // Scheduler RNG streams sized by the longest default horizon of this shard.
   int32_t pool = 0;
-  if (d.with_saber && mine > 0) {
+  double hm = 0.0;
+  TickTableBuf ticktab;
+  if (mine > 0) {
     CUDA_TRY(cudaMemsetAsync(hmax.p, 0, 16, st));
     LAUNCH_TRY(launch_mc_horizon(mp, mine, hmax.as<unsigned long long>(), st));
     ++launches;
-    double hm = 0.0;
     CUDA_TRY(cudaMemcpy(&hm, hmax.p, 8, cudaMemcpyDeviceToHost));
+    if (saber_status s = ticktab.build(dev, d.tick, hm + 1.0)) return s;
+  }
+  if (d.with_saber && mine > 0) {
     pool = static_cast<int32_t>(std::min<int64_t>(d.scheduler_seeds, d.n_traj));
     const int64_t len = draw_bound(hm + 1.0, d.tick, d.window_size, n);
     std::vector<uint64_t> seeds(static_cast<size_t>(pool));
@@ -1475,6 +1603,7 @@ extern "C" saber_status saber_cuda_mc_sweep(const saber_mc_desc* desc, saber_mc_
     sp.out.completion = comp.as<double>();
     sp.out.error = err.as<int32_t>();
     sp.next_traj = cursor.as<int32_t>();
+    sp.ticks = ticktab.view;
     CUDA_TRY(cudaEventRecord(simt.a, st));
     LAUNCH_TRY(launch_sim(sp, scratch.launch, st));
     CUDA_TRY(cudaEventRecord(simt.b, st));

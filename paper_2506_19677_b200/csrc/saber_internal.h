@@ -81,6 +81,19 @@ struct SimOutputs {
   int32_t* error;             // [1] first error code (0 = none)
 };
 
+// The tick grid of the reference's run loop (simloop.cpp:99-100): t_0 = 0,
+// t_{k+1} = fl(t_k + tick) below the horizon.  It depends only on `tick`, so
+// one host-built table serves every trajectory with that tick; DT[k] =
+// T[k+1] - T[k] is exact (Sterbenz) and is the dt of a tick's single full pass.
+struct TickTable {
+  const double* T;    // [len]
+  const double* DT;   // [len - 1]
+  int32_t len;        // 0 = no table (streaks off)
+  double tick;        // trajectories with d.tick == tick use it
+  double inv_tick;    // 1 / tick (index estimate only; exactness from T)
+  double dt_max;      // max DT
+};
+
 struct SimParams {
   const TrajDesc* traj;
   int32_t n_traj;
@@ -92,6 +105,8 @@ struct SimParams {
   SimOutputs out;
   int32_t* next_traj;         // work-queue cursor (device)
   const int32_t* order;       // execution order of the descriptors (longest first), or null
+  int32_t no_streak;          // 1 = disable quiet streaks (A/B runs, SABER_NO_STREAK)
+  TickTable ticks;            // shared tick grid for quiet streaks
 };
 
 // Error codes written to SimOutputs::error.
@@ -100,6 +115,7 @@ enum : int32_t {
   kErrRngExhausted = 1,   // scheduler stream too short (host bound violated)
   kErrTraceOverflow = 2,  // decision trace capacity exceeded
   kErrBadDesc = 3,
+  kErrTickTable = 4,      // t != T[k] at a streak (tick-table invariant broken)
 };
 
 // Kernel launchers (defined in the .cu files).

@@ -32,6 +32,7 @@
 
 #include <cmath>
 #include <cstdint>
+#include <cstdlib>
 
 #include "saber_internal.h"
 #include "sim_common.cuh"
@@ -59,6 +60,65 @@ struct Slots {
     return ((k / G) << 5) + col0 + (k & (G - 1));
   }
 };
+
+// An integer q <= a / b (a >= 0 finite, b > 0), capped at 2^30: float
+// arithmetic with directed rounding keeps it a lower bound without a DDIV.
+__device__ __forceinline__ int floor_div_lb(double a, double b) {
+  const float q = __fmul_rd(__double2float_rd(a), __frcp_rd(__double2float_ru(b)));
+  return static_cast<int>(fminf(q, 1073741824.0f));
+}
+
+// min{k : T[k] >= x} over the tick table (len if none; x may be +inf).
+__device__ __forceinline__ int tick_index(const TickTable& tt, double x) {
+  int k = static_cast<int>(fmin(fmax(x * tt.inv_tick, 0.0), static_cast<double>(tt.len)));
+  while (k > 0 && tt.T[k - 1] >= x) --k;
+  while (k < tt.len && tt.T[k] < x) ++k;
+  return k;
+}
+
+// Quiet streak: K consecutive ticks k0 .. k0+K-1, each one
+// full quiet pass of dt = DT[k], applied slot by slot from registers.
+// Per pass the reference computes g += speed*dt (decode) or
+// prefill_left -= dt (prefill, stored as g = -prefill_left), which is exactly
+// what runs here; the caller has proved that no pass of the streak ends a
+// prefill, binds the decode boundary or completes a slot.
+template <int G>
+__device__ __forceinline__ void streak_slots(const Slots<G>& S, int sub, int A, double speed,
+                                             const double* __restrict__ DT, int K) {
+  constexpr int kC = G >= 16 ? 2 : 4;  // slots per lane per chunk (registers)
+  for (int base = sub; base < A; base += kC * G) {
+    double g[kC];
+    double pre[kC];  // 1.0 for prefill slots, 0.0 for decode slots
+#pragma unroll
+    for (int i = 0; i < kC; ++i) {
+      const int k = base + i * G;
+      g[i] = k < A ? S.g[S.idx(k)] : 0.0;
+      pre[i] = g[i] < 0.0 ? 1.0 : 0.0;
+    }
+    int j = 0;
+#pragma unroll 1
+    for (; j + 2 <= K; j += 2) {
+      const double d0 = DT[j], d1 = DT[j + 1];
+      const double s0 = speed * d0, s1 = speed * d1;
+#pragma unroll
+      for (int i = 0; i < kC; ++i) {
+        g[i] = g[i] + (pre[i] != 0.0 ? d0 : s0);
+        g[i] = g[i] + (pre[i] != 0.0 ? d1 : s1);
+      }
+    }
+    if (j < K) {
+      const double d0 = DT[j];
+      const double s0 = speed * d0;
+#pragma unroll
+      for (int i = 0; i < kC; ++i) g[i] = g[i] + (pre[i] != 0.0 ? d0 : s0);
+    }
+#pragma unroll
+    for (int i = 0; i < kC; ++i) {
+      const int k = base + i * G;
+      if (k < A) S.g[S.idx(k)] = g[i];
+    }
+  }
+}
 
 // Simulates trajectory `ti` on this group.
 template <int NW, int G, bool kTrace, bool kRecords>
@@ -110,6 +170,7 @@ __device__ __forceinline__ void simulate_one(const SimParams& P, int ti, const S
   double m_hi = 0.0;      // >= max_output_tokens of every active slot
   // speed_A caches predict(gt, A); it changes only with A.
   double speed_A = 0.0;
+  bool sblock = false;  // quiet-streak bounds exhausted until the next event (§3.5)
   auto retune = [&]() { speed_A = GT[A]; };
 
   int next = 0;
@@ -139,9 +200,19 @@ __device__ __forceinline__ void simulate_one(const SimParams& P, int ti, const S
     m_hi = (m_hi < m) ? m : m_hi;
     S.m[s] = dbits(m) | static_cast<uint64_t>(id);
     ++A;
+    sblock = false;
     retune();
     if (kRecords && ADM && leader) ADM[id] = now;
   };
+
+  // Tick table: kh = first tick index at/after the horizon,
+  // ka = first tick index at/after the next arrival (lazily, -1 = stale).
+  bool use_tab = !P.no_streak && P.ticks.len > 0 && tick == P.ticks.tick;
+  const int kh = use_tab ? tick_index(P.ticks, horizon) : 0;
+  int ka = -1;
+#ifdef SABER_STREAK_STATS
+  int st_ticks = 0, st_count = 0, st_quiet = 0, st_exact = 0;
+#endif
 
   double t = 0.0;
   for (;;) {
@@ -151,6 +222,7 @@ __device__ __forceinline__ void simulate_one(const SimParams& P, int ti, const S
       if (saber) min_td = dmin(min_td, DEM[next]);
       ++next;
       na_t = next < n ? ARR[next] : kInf;
+      ka = -1;
     }
     ++ticks;
     const int load = A;
@@ -300,6 +372,65 @@ __device__ __forceinline__ void simulate_one(const SimParams& P, int ti, const S
     }
 
     if (t >= horizon) break;
+
+    // Quiet streak: from this tick on, consecutive ticks
+    // whose scheduler step is provably a no-op (no arrival, nothing
+    // admissible) and whose single engine pass is provably quiet run as one
+    // register-resident sweep over the slots.  K is bounded by the next
+    // arrival's tick, the horizon, and the prefill / decode minima:
+    //   * min_pf_j > dt_j (1 + 1e-12) for every pass j (no prefill ends);
+    //   * min_rem_j >= sdt_j (1 + 1e-9) + 1e-15 (m_hi + sdt_j + 1), the
+    //     quiet-pass test below (decode boundary cannot bind, no completion);
+    // both minima shrink by at most dt_max / speed*dt_max (+ rounding) per pass.
+    if (use_tab && !sblock && A > 0 &&
+        (saber ? (!high.any() && low_head == low_tail) : !(A < d.cap && high.any()))) {
+      const int k0 = ticks - 1;
+      const double dtm = P.ticks.dt_max;
+      // Kb passes keep both minima provably quiet: for pass j <= Kb - 1 the
+      // remaining margin is still >= one full per-pass decrement.
+      int Kb = 1 << 30;
+      if (npre > 0) Kb = floor_div_lb(min_pf * (1.0 - 2e-7), dtm * (1.0 + 1e-6));
+      double delta = 0.0;
+      if (A > npre) {
+        const double sm = speed_A * dtm * (1.0 + 1e-15);
+        delta = sm * (1.0 + 1e-6) + 2e-15 * (m_hi + sm + 1.0);
+        Kb = min(Kb, floor_div_lb(rem_lb, delta));
+      }
+      // The bounds only shrink until the next admission / exact pass.
+      if (Kb < 2) sblock = true;
+      int K = 0;
+      if (Kb >= 2) {
+        if (ka < 0) ka = tick_index(P.ticks, na_t);
+        K = min(Kb, min(ka - k0, kh - 1 - k0));
+      }
+      if (K >= 2) {
+        if (P.ticks.T[k0] != t || clock != t) {  // invariant: loud, never silent
+          if (leader) atomicCAS(P.out.error, kErrNone, kErrTickTable);
+          use_tab = false;
+        } else {
+          const double* __restrict__ DTk = P.ticks.DT + k0;
+          streak_slots<G>(S, sub, A, speed_A, DTk, K);
+          if (npre > 0) {
+            double pf = min_pf;
+            for (int j = 0; j < K; ++j) pf = pf - DTk[j];
+            min_pf = pf;  // exact, as the per-pass updates
+          }
+          if (A > npre) rem_lb = rem_lb - static_cast<double>(K) * delta;
+          rem_exact = false;
+#ifdef SABER_STREAK_STATS
+          st_ticks += K;
+          st_count += 1;
+#endif
+          ticks += K - 1;  // this tick was counted above
+          passes += K;
+          prefill_updates += K * npre;
+          decode_updates += K * (A - npre);
+          t = P.ticks.T[k0 + K];
+          clock = t;
+          continue;
+        }
+      }
+    }
     const double nt = (horizon < t + tick) ? horizon : t + tick;
 
     // Engine::advance_to(nt) (engine.cpp:51-127).
@@ -333,9 +464,16 @@ __device__ __forceinline__ void simulate_one(const SimParams& P, int ti, const S
         prefill_updates += npre;
         decode_updates += A - npre;
         clock = clock + dt;
+#ifdef SABER_STREAK_STATS
+        st_quiet += 1;
+#endif
         continue;
       }
       // Exact pass.  First make the decode minimum exact if it is a bound.
+      sblock = false;
+#ifdef SABER_STREAK_STATS
+      st_exact += 1;
+#endif
       if (!rem_exact) {
         double r = kInf;
         for (int k = sub, s = S.idx(sub); k < A; k += G, s += kWarp) {
@@ -505,6 +643,11 @@ __device__ __forceinline__ void simulate_one(const SimParams& P, int ti, const S
     R->rng_draws = rng_draws;
     R->last_arrival = n > 0 ? ARR[n - 1] : 0.0;
     R->horizon = horizon;
+#ifdef SABER_STREAK_STATS
+    R->last_arrival = st_ticks;
+    R->horizon = st_count;
+    R->decision_hash = (static_cast<uint64_t>(st_quiet) << 32) | static_cast<uint32_t>(st_exact);
+#endif
     if (kTrace && P.out.trace_count) P.out.trace_count[d.row] = L.n;
   }
 }
@@ -617,6 +760,7 @@ void* pick_g(int g, bool trace, bool records) {
     case 4: return pick_tr<NW, 4>(trace, records);
     case 8: return pick_tr<NW, 8>(trace, records);
     case 16: return pick_tr<NW, 16>(trace, records);
+    case 32: return pick_tr<NW, 32>(trace, records);
   }
   return nullptr;
 }
@@ -642,7 +786,7 @@ int plan_sim(int nmax, int group, SimLaunch* out) {
     l.group = group;
     l.slot_rows = (nmax + group - 1) / group;
     l.smem = static_cast<size_t>(kSimBlock / kWarp) * l.slot_rows * kWarp * 16;
-    if (l.smem <= kTileBudget || group >= 16) break;
+    if (l.smem <= kTileBudget || group >= 32) break;
     group *= 2;
   }
   void* k = pick_kernel(l.nwords, group, false, false);
@@ -673,7 +817,9 @@ int launch_sim(const SimParams& p, const SimLaunch& l, void* stream) {
   const bool records = p.out.admit != nullptr || p.out.demoted != nullptr;
   void* k = pick_kernel(l.nwords, l.group, trace, records);
   if (!k) return 1;
-  void* args[] = {const_cast<SimParams*>(&p)};
+  SimParams q = p;
+  q.no_streak = std::getenv("SABER_NO_STREAK") != nullptr;
+  void* args[] = {&q};
   return cudaLaunchKernel(k, dim3(l.grid), dim3(kSimBlock), args, l.smem,
                           static_cast<cudaStream_t>(stream)) == cudaSuccess
              ? 0

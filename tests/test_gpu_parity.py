@@ -52,6 +52,31 @@ def test_random_trajectories_match_restatement(engine, orc):
     assert bad == []
 
 
+@pytest.mark.parametrize("group", [1, 2, 4, 8, 16, 32])
+@pytest.mark.parametrize("streak", [True, False])
+def test_every_group_size_and_streak_mode(engine, orc, monkeypatch, group, streak):
+    """Every trajectory-kernel configuration (SABER_GROUP lanes per trajectory,
+    quiet streaks on/off, DESIGN.md §3.1/§3.5) is bit-exact."""
+    monkeypatch.setenv("SABER_GROUP", str(group))
+    if streak:
+        monkeypatch.delenv("SABER_NO_STREAK", raising=False)
+    else:
+        monkeypatch.setenv("SABER_NO_STREAK", "1")
+    cfgs = random_configs(96, seed=1000 + group)
+    res = engine.run_batch(cfgs)
+    bad = []
+    for k, cfg in enumerate(cfgs):
+        o = orc.run(orc_config(cfg), records=True)
+        errs = compare_row(res.rows[k], o.out)
+        for i, rec in enumerate(o.records):
+            if not same_float(res.completion_times[k, i], rec.completion_time):
+                errs.append(f"completion[{i}]")
+                break
+        if errs:
+            bad.append((k, errs[:4]))
+    assert bad == []
+
+
 def test_random_trajectories_match_reference(engine, ref):
     cfgs = random_configs(120, seed=99)
     res = engine.run_batch(cfgs)
