@@ -117,24 +117,34 @@ typedef struct {
   int32_t task, input_tokens, max_output_tokens, demoted;
 } orc_record;
 
-/* Decision hash used by every implementation (oracle restatement, reference
- * harness, CUDA kernel).  Per decision d, in emission order:
- *   h = step(h, bits(d.time))
- *   h = step(h, id | kind<<32 | (u64)(u32)load<<40
- *               ^ rotl(pred_bits,17) ^ rotl(req_bits,43))
- * where absent speeds hash as ORC_ABSENT_BITS and
- *   step(h, x) = ((h ^ x) * 0x9E3779B97F4A7C15) ^ (>> 32 of that product).  */
-#define ORC_HASH_SEED 0x243F6A8885A308D3ULL
+/* Decision-log digest used by every implementation (oracle restatement,
+ * reference harness, CUDA kernel).  For the i-th decision d (0-based, in
+ * emission order):
+ *   x_i = id | kind<<32 | (u64)(u32)load<<40
+ *         ^ rotl(pred_bits,17) ^ rotl(req_bits,43) ^ rotl(bits(d.time),7)
+ *   h   = sum_i mix64(x_i + (i+1) * 0x9E3779B97F4A7C15)   (mod 2^64)
+ * with absent speeds as ORC_ABSENT_BITS and mix64 the splitmix64 finaliser.
+ * Every term carries its position, so the digest is order-sensitive, and the
+ * terms are independent, so the device can form them lane-parallel
+ * (DESIGN.md §5).  The empty log hashes to ORC_HASH_SEED (0).  */
+#define ORC_HASH_SEED 0ULL
 #define ORC_ABSENT_BITS 0xFFF8000000000001ULL
 
-static inline uint64_t orc_hash_step(uint64_t h, uint64_t x) {
-  h ^= x;
-  h *= 0x9E3779B97F4A7C15ULL;
-  h ^= h >> 32;
-  return h;
-}
 static inline uint64_t orc_rotl(uint64_t x, int r) {
   return (x << r) | (x >> (64 - r));
+}
+static inline uint64_t orc_mix64(uint64_t z) {
+  z ^= z >> 30;
+  z *= 0xBF58476D1CE4E5B9ULL;
+  z ^= z >> 27;
+  z *= 0x94D049BB133111EBULL;
+  z ^= z >> 31;
+  return z;
+}
+static inline uint64_t orc_decision_term(uint64_t index, uint64_t time_bits, uint64_t w,
+                                         uint64_t pb, uint64_t rb) {
+  const uint64_t x = w ^ orc_rotl(pb, 17) ^ orc_rotl(rb, 43) ^ orc_rotl(time_bits, 7);
+  return orc_mix64(x + (index + 1) * 0x9E3779B97F4A7C15ULL);
 }
 
 /* ---- functions exported by both libraries (prefix orc_ / ref_) ---------- */

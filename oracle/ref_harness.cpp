@@ -93,8 +93,7 @@ void fill_out(const saber::RunOutput& o, orc_traj_out* out, orc_record* recs,
     const uint64_t w = static_cast<uint64_t>(static_cast<uint32_t>(d.request_id)) |
                        (static_cast<uint64_t>(kind_of(d.kind)) << 32) |
                        (static_cast<uint64_t>(static_cast<uint32_t>(d.load_before)) << 40);
-    h = orc_hash_step(h, dbits(d.time));
-    h = orc_hash_step(h, w ^ orc_rotl(pb, 17) ^ orc_rotl(rb, 43));
+    h += orc_decision_term(static_cast<uint64_t>(i), dbits(d.time), w, pb, rb);
     out->n_kind[kind_of(d.kind)] += 1;
     if (decs && static_cast<int64_t>(i) < dec_cap) {
       orc_decision& x = decs[i];

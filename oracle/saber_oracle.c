@@ -368,8 +368,7 @@ static void declog_push(declog_t* L, double time, int id, int kind, int load,
   const uint64_t rb = has_req ? dbits(req) : ORC_ABSENT_BITS;
   const uint64_t w = ((uint64_t)(uint32_t)id) | ((uint64_t)kind << 32) |
                      ((uint64_t)(uint32_t)load << 40);
-  L->hash = orc_hash_step(L->hash, dbits(time));
-  L->hash = orc_hash_step(L->hash, w ^ orc_rotl(pb, 17) ^ orc_rotl(rb, 43));
+  L->hash += orc_decision_term((uint64_t)L->count, dbits(time), w, pb, rb);
   if (L->buf) {
     if (L->count < L->cap) {
       orc_decision* d = &L->buf[L->count];

@@ -625,19 +625,24 @@ saber_status saber_cuda_sweep_plan_create(const saber_sweep_desc* desc, saber_sw
   if (saber_status s = P->scratch.alloc(dev, n)) return s;
   tr.mark("scratch + kernel plan");
 
-  // Longest-first execution order: the kernel time is set by
-  // the last trajectories to finish, and a trajectory's tick count grows with
-  // its arrival span n / rps, so low rates start first (SABER before static
-  // at equal rate: its ticks carry the gate's decisions).
+  // Execution order: every SABER trajectory first (they are
+  // ~4x the work of a static one, and keeping the two code paths apart in
+  // time keeps the instruction cache warm: measured 21.9 vs 25.8 ms on config
+  // 2), each class longest arrival span n / rps first.  SABER_ORDER=0 orders
+  // by n / rps only, SABER_ORDER=2 keeps row order (A/B runs).
   {
     const int per_rps = desc->n_caps * R + (desc->with_saber ? R : 0);
+    const char* om = std::getenv("SABER_ORDER");
+    const int order_mode = om ? std::atoi(om) : 1;
     std::vector<std::pair<double, int32_t>> key(static_cast<size_t>(P->rows_shard));
     for (int64_t k = 0; k < P->rows_shard; ++k) {
       const int64_t r = desc->shard_index + k * desc->shard_count;
       const int ri = static_cast<int>((r / per_rps) % n_rps);
       const bool sab = (r % per_rps) >= desc->n_caps * R;
-      key[static_cast<size_t>(k)] = {-(n / P->rps[static_cast<size_t>(ri)]) - (sab ? 1.0 : 0.0),
-                                     static_cast<int32_t>(k)};
+      double kk = -(n / P->rps[static_cast<size_t>(ri)]) - (sab ? 1.0 : 0.0);
+      if (order_mode == 1) kk = (sab ? -1e18 : 0.0) - n / P->rps[static_cast<size_t>(ri)];
+      if (order_mode == 2) kk = 0.0;
+      key[static_cast<size_t>(k)] = {kk, static_cast<int32_t>(k)};
     }
     std::stable_sort(key.begin(), key.end(),
                      [](const auto& a, const auto& b) { return a.first < b.first; });

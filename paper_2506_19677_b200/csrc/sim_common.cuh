@@ -14,19 +14,27 @@ namespace simdev {
 
 constexpr double kInf = __builtin_huge_val();
 constexpr double kOnePlusTol = 1.0 + 1e-12;  // engine.cpp:17,76 (kGroupTol)
-constexpr uint64_t kHashSeed = 0x243F6A8885A308D3ULL;
+constexpr uint64_t kHashSeed = 0;  // oracle.h ORC_HASH_SEED: the empty log
 constexpr uint64_t kAbsent = 0xFFF8000000000001ULL;
 constexpr uint64_t kDoneMark = 0xFFF0DEAD0000DEADULL;  // a NaN the engine never produces
 constexpr uint64_t kIdMask = 0xFFFFull;
 
-__device__ __forceinline__ uint64_t hstep(uint64_t h, uint64_t x) {
-  h ^= x;
-  h *= 0x9E3779B97F4A7C15ULL;
-  h ^= h >> 32;
-  return h;
-}
 __device__ __forceinline__ uint64_t rotl64(uint64_t x, int r) {
   return (x << r) | (x >> (64 - r));
+}
+__device__ __forceinline__ uint64_t mix64(uint64_t z) {
+  z ^= z >> 30;
+  z *= 0xBF58476D1CE4E5B9ULL;
+  z ^= z >> 27;
+  z *= 0x94D049BB133111EBULL;
+  z ^= z >> 31;
+  return z;
+}
+// One decision's term of the log digest (oracle.h orc_decision_term).
+__device__ __forceinline__ uint64_t decision_term(uint64_t index, uint64_t tb, uint64_t w,
+                                                  uint64_t pb, uint64_t rb) {
+  const uint64_t x = w ^ rotl64(pb, 17) ^ rotl64(rb, 43) ^ rotl64(tb, 7);
+  return mix64(x + (index + 1) * 0x9E3779B97F4A7C15ULL);
 }
 __device__ __forceinline__ uint64_t dbits(double v) {
   return static_cast<uint64_t>(__double_as_longlong(v));
@@ -130,8 +138,7 @@ __device__ __forceinline__ void push_decision(DecisionLog& L, double t, int id,
   const uint64_t w = static_cast<uint64_t>(static_cast<uint32_t>(id)) |
                      (static_cast<uint64_t>(kind) << 32) |
                      (static_cast<uint64_t>(static_cast<uint32_t>(load)) << 40);
-  L.h = hstep(L.h, dbits(t));
-  L.h = hstep(L.h, w ^ rotl64(pb, 17) ^ rotl64(rb, 43));
+  L.h += decision_term(static_cast<uint64_t>(L.n), dbits(t), w, pb, rb);
   if (kTrace && tr != nullptr && writer) {
     if (L.n < cap) {
       saber_decision& d = tr[L.n];

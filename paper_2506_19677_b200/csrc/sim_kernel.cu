@@ -120,6 +120,97 @@ __device__ __forceinline__ void streak_slots(const Slots<G>& S, int sub, int A, 
   }
 }
 
+// Gate streak decisions: ticks k0+1 .. k0+K-1 of a streak
+// whose tick k0 gate admitted nobody.  Each such tick runs the reference's
+// admission_step (scheduler.cpp:57-95) on an unchanged window: w-1 draws for
+// the Fisher-Yates, then every candidate is rejected — RejectOwn when
+// pred < need(t), else RejectActive (need grows with t, so a candidate that
+// could pass its own test at k0 was already blocked by the ledger).  Lane
+// `sub` takes ticks k0+1+sub, k0+1+sub+G, ...; the digest terms (oracle.h)
+// carry their log index n0 + (j-1) w + c, so they are summed in any order.
+template <int G, bool kTrace, int NW>
+__device__ __forceinline__ void gate_streak_decisions(
+    const SimParams& P, const Slots<G>& S, int sub, unsigned gmask, const Mask<NW>& high,
+    const double* __restrict__ MO, const double* __restrict__ DL,
+    const uint32_t* __restrict__ draws, int64_t draw_pos, int k0, int K, int w, int load,
+    double pred, DecisionLog& L, saber_decision* tr, const uint32_t* __restrict__ INV) {
+  // the window (first w queued ids) on lanes 0..w-1
+  int wid = 0;
+  double wm = 0.0, wdl = 0.0;
+  if (sub < w) {
+    wid = high.select(sub);
+    wm = MO[wid];
+    wdl = DL[wid];
+  }
+  const uint64_t pb = dbits(pred);
+  const uint64_t wl = static_cast<uint64_t>(static_cast<uint32_t>(load)) << 40;
+  const int64_t n0 = L.n;
+  uint64_t hs = 0;
+  unsigned own = 0, act = 0;
+  for (int jb = 1; jb < K; jb += G) {
+    const int j = jb + sub;
+    const bool live = j < K;
+    const double tj = live ? P.ticks.T[k0 + j] : 0.0;
+    const uint64_t tb = dbits(tj);
+    const uint32_t* __restrict__ dq = draws + draw_pos + static_cast<int64_t>(j - 1) * (w - 1);
+    uint32_t xq[kMaxWindow - 1];
+#pragma unroll
+    for (int q = 0; q < kMaxWindow - 1; ++q) xq[q] = (live && q < w - 1) ? dq[q] : 0u;
+    uint64_t ord = 0xFEDCBA9876543210ull;
+#pragma unroll
+    for (int q = 0; q < kMaxWindow - 1; ++q) {
+      if (q < w - 1) {
+        const uint32_t i = static_cast<uint32_t>(w - 1 - q);
+        const uint32_t jj = xq[q] - __umulhi(xq[q], INV[i + 1]) * (i + 1);
+        const uint64_t a = (ord >> (4 * i)) & 15ull;
+        const uint64_t bb = (ord >> (4 * jj)) & 15ull;
+        const uint64_t x2 = a ^ bb;
+        ord ^= (x2 << (4 * i)) | (x2 << (4 * jj));
+      }
+    }
+    for (int c = 0; c < w; ++c) {
+      const int p = static_cast<int>((ord >> (4 * c)) & 15ull);
+      const int id = __shfl_sync(gmask, wid, S.col0 + p);
+      const double m = __shfl_sync(gmask, wm, S.col0 + p);
+      const double dl = __shfl_sync(gmask, wdl, S.col0 + p);
+      if (!live) continue;
+      const double need = queued_need(m, dl, tj);
+      const int kind = pred < need ? SABER_REJECT_OWN : SABER_REJECT_ACTIVE;
+      own += kind == SABER_REJECT_OWN;
+      act += kind == SABER_REJECT_ACTIVE;
+      const int64_t idx = n0 + static_cast<int64_t>(j - 1) * w + c;
+      const uint64_t w64 = static_cast<uint64_t>(static_cast<uint32_t>(id)) |
+                           (static_cast<uint64_t>(kind) << 32) | wl;
+      hs += decision_term(static_cast<uint64_t>(idx), tb, w64, pb, dbits(need));
+      if (kTrace && tr != nullptr) {
+        if (idx < P.out.trace_cap) {
+          saber_decision& dd = tr[idx];
+          dd.time = tj;
+          dd.request_id = static_cast<uint64_t>(id);
+          dd.kind = kind;
+          dd.load_before = load;
+          dd.has_pred = 1;
+          dd.has_req = 1;
+          dd.pred_speed = pred;
+          dd.req_speed = need;
+        } else {
+          atomicCAS(P.out.error, kErrNone, kErrTraceOverflow);
+        }
+      }
+    }
+  }
+  // group sums (64-bit digest: butterfly over the group's lanes)
+#pragma unroll
+  for (int o = 1; o < G; o <<= 1) hs += __shfl_xor_sync(gmask, hs, o);
+  own = group_sum<G>(own, gmask);
+  act = group_sum<G>(act, gmask);
+  const int64_t nd = static_cast<int64_t>(K - 1) * w;
+  L.h += hs;
+  L.n += static_cast<int32_t>(nd);
+  L.k2 += static_cast<int32_t>(own);
+  L.k3 += static_cast<int32_t>(act);
+}
+
 // Simulates trajectory `ti` on this group.
 template <int NW, int G, bool kTrace, bool kRecords>
 __device__ __forceinline__ void simulate_one(const SimParams& P, int ti, const Slots<G>& S,
@@ -212,6 +303,7 @@ __device__ __forceinline__ void simulate_one(const SimParams& P, int ti, const S
   int ka = -1;
 #ifdef SABER_STREAK_STATS
   int st_ticks = 0, st_count = 0, st_quiet = 0, st_exact = 0;
+  const long long st_t0 = clock64();
 #endif
 
   double t = 0.0;
@@ -226,6 +318,10 @@ __device__ __forceinline__ void simulate_one(const SimParams& P, int ti, const S
     }
     ++ticks;
     const int load = A;
+    // Gate outcome of this tick, for a gate streak.
+    bool gate_idle = false;
+    int gate_w = 0;
+    double gate_pred = 0.0;
     if (saber) {
       const int hc = high.count();
       refresh_entries += hc;
@@ -314,6 +410,9 @@ __device__ __forceinline__ void simulate_one(const SimParams& P, int ti, const S
         }
         if (G > 1) okmask = __reduce_or_sync(gmask, okmask);
         const int first = okmask ? __ffs(okmask) - 1 : w;  // admitted position, or none
+        gate_idle = first == w;
+        gate_w = w;
+        gate_pred = pred;
         const int last = first < w ? first : w - 1;
         for (int c = 0; c <= last; ++c) {
           int id;
@@ -382,8 +481,14 @@ __device__ __forceinline__ void simulate_one(const SimParams& P, int ti, const S
     //   * min_rem_j >= sdt_j (1 + 1e-9) + 1e-15 (m_hi + sdt_j + 1), the
     //     quiet-pass test below (decode boundary cannot bind, no completion);
     // both minima shrink by at most dt_max / speed*dt_max (+ rounding) per pass.
+    // A SABER tick whose gate admitted nobody starts a gate streak: with the
+    // high tier, load and ledger unchanged, every later tick of the streak
+    // rejects the same window again (need = m / (dl - t) only grows), so its
+    // decisions are generated lane-parallel (gate_streak below).
+    const bool gate_streak = saber && high.any();
     if (use_tab && !sblock && A > 0 &&
-        (saber ? (!high.any() && low_head == low_tail) : !(A < d.cap && high.any()))) {
+        (saber ? (gate_streak ? (G >= kMaxWindow && gate_idle) : low_head == low_tail)
+               : !(A < d.cap && high.any()))) {
       const int k0 = ticks - 1;
       const double dtm = P.ticks.dt_max;
       // Kb passes keep both minima provably quiet: for pass j <= Kb - 1 the
@@ -402,6 +507,13 @@ __device__ __forceinline__ void simulate_one(const SimParams& P, int ti, const S
       if (Kb >= 2) {
         if (ka < 0) ka = tick_index(P.ticks, na_t);
         K = min(Kb, min(ka - k0, kh - 1 - k0));
+        if (gate_streak) {
+          // no refresh scan (t < min_td) and enough scheduler draws
+          K = min(K, tick_index(P.ticks, min_td) - k0);
+          if (gate_w > 1)
+            K = static_cast<int>(min(static_cast<int64_t>(K),
+                                     1 + (draw_len - draw_pos) / (gate_w - 1)));
+        }
       }
       if (K >= 2) {
         if (P.ticks.T[k0] != t || clock != t) {  // invariant: loud, never silent
@@ -417,6 +529,17 @@ __device__ __forceinline__ void simulate_one(const SimParams& P, int ti, const S
           }
           if (A > npre) rem_lb = rem_lb - static_cast<double>(K) * delta;
           rem_exact = false;
+          if (gate_streak) {
+            const int hc = high.count();
+            gate_streak_decisions<G, kTrace, NW>(P, S, sub, gmask, high, MO, DL, draws, draw_pos,
+                                                 k0, K, gate_w, A, gate_pred, L, tr, INV);
+            const int64_t extra = K - 1;
+            draw_pos += extra * (gate_w - 1);
+            rng_draws += static_cast<int32_t>(extra * (gate_w - 1));
+            cands += static_cast<int32_t>(extra * gate_w);
+            ledger_scanned += static_cast<int32_t>(extra * ledger_size);
+            refresh_entries += static_cast<int32_t>(extra * hc);
+          }
 #ifdef SABER_STREAK_STATS
           st_ticks += K;
           st_count += 1;
@@ -646,6 +769,8 @@ __device__ __forceinline__ void simulate_one(const SimParams& P, int ti, const S
 #ifdef SABER_STREAK_STATS
     R->last_arrival = st_ticks;
     R->horizon = st_count;
+    R->ratio_mean = static_cast<double>(clock64() - st_t0);  // overwritten by row metrics
+    R->n_kind[4] = clock64() - st_t0;
     R->decision_hash = (static_cast<uint64_t>(st_quiet) << 32) | static_cast<uint32_t>(st_exact);
 #endif
     if (kTrace && P.out.trace_count) P.out.trace_count[d.row] = L.n;

@@ -46,5 +46,38 @@ def main():
                   f" streaks {rr['horizon'].mean():6.0f} quiet {quiet[mm].mean():6.0f} exact {exact[mm].mean():6.0f}")
 
 
-if __name__ == "__main__":
+if __name__ == "__main__" and len(sys.argv) == 1:
     main()
+
+
+def durations():
+    """Per-trajectory cycles (stats build stores them in n_kind[4])."""
+    grid = S.SweepGrid(bench.MIXES, bench.RPS, bench.CAPS, True)
+    base = S.SimConfig()
+    base.workload.num_requests = bench.N_REQ
+    base.model = S.SpeedModel(S.ModelFamily.Usl, bench.CAL_USL)
+    base.repeats = bench.SEEDS_PER_GPU
+    base.seed = bench.BASE_SEED
+    p = S.SweepPlan(grid, base)
+    p.run()
+    p.run()
+    rows, _, _, _ = p.fetch(summary=False)
+    keys = S.sweep_row_keys(grid, base)
+    cyc = rows["n_kind"][:, 4].astype(np.float64)
+    import collections
+    agg = collections.defaultdict(list)
+    for k, c in zip(keys, cyc):
+        agg[(k[0], k[1], "saber" if k[2] == S.SchedulerMode.Saber else "static")].append(c)
+    print("total cycles (sum over trajectories) %.3e, max %.3e" % (cyc.sum(), cyc.max()))
+    for mode in ("static", "saber"):
+        for m in bench.MIXES:
+            line = " ".join("%5.0f" % (np.mean(agg[(m, r, mode)]) / 1e3) for r in bench.RPS)
+            print(f"{mode:6s} {m} kcyc/traj by rps 1..20: {line}")
+    for mode in ("static", "saber"):
+        for m in bench.MIXES:
+            line = " ".join("%5.0f" % (np.max(agg[(m, r, mode)]) / 1e3) for r in bench.RPS)
+            print(f"{mode:6s} {m} max kcyc by rps 1..20: {line}")
+
+
+if __name__ == "__main__" and len(sys.argv) > 1:
+    durations()
