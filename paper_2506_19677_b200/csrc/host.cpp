@@ -446,6 +446,14 @@ struct saber_sweep_plan {
   DevBuf summary, best_cap, cell_scratch, ratios, order;
   Scratch scratch;
   TickTableBuf ticktab;
+  int32_t n_saber_first = 0;  // SABER rows lead the order: split launch
+  cudaStream_t side = nullptr;
+  cudaEvent_t fork = nullptr, join = nullptr;
+  ~saber_sweep_plan() {
+    if (side) cudaStreamDestroy(side);
+    if (fork) cudaEventDestroy(fork);
+    if (join) cudaEventDestroy(join);
+  }
   Timer all, sim;
   double last_ms = 0.0, sim_ms = 0.0;
   int launches = 0;
@@ -643,6 +651,7 @@ saber_status saber_cuda_sweep_plan_create(const saber_sweep_desc* desc, saber_sw
       if (order_mode == 1) kk = (sab ? -1e18 : 0.0) - n / P->rps[static_cast<size_t>(ri)];
       if (order_mode == 2) kk = 0.0;
       key[static_cast<size_t>(k)] = {kk, static_cast<int32_t>(k)};
+      if (order_mode == 1 && sab) ++P->n_saber_first;
     }
     std::stable_sort(key.begin(), key.end(),
                      [](const auto& a, const auto& b) { return a.first < b.first; });
@@ -678,6 +687,11 @@ saber_status saber_cuda_sweep_plan_create(const saber_sweep_desc* desc, saber_sw
   tr.mark("tick table");
   if (saber_status s = P->all.init()) return s;
   if (saber_status s = P->sim.init()) return s;
+  if (P->n_saber_first > 0 && P->n_saber_first < P->rows_shard) {
+    CUDA_TRY(cudaStreamCreateWithFlags(&P->side, cudaStreamNonBlocking));
+    CUDA_TRY(cudaEventCreateWithFlags(&P->fork, cudaEventDisableTiming));
+    CUDA_TRY(cudaEventCreateWithFlags(&P->join, cudaEventDisableTiming));
+  }
   tr.mark("events");
   *out = guard.release();
   return SABER_OK;
@@ -767,9 +781,29 @@ saber_status saber_cuda_sweep_plan_run(saber_sweep_plan* P, void* stream) {
   sp.order = P->order.as<int32_t>();
   sp.ticks = P->ticktab.view;
   CUDA_TRY(cudaEventRecord(P->sim.a, s));
-  LAUNCH_TRY(launch_sim(sp, P->scratch.launch, s));
+  const bool split = P->side != nullptr && P->scratch.launch.group == 32 && !P->scratch.launch.lane &&
+                     std::getenv("SABER_NO_SPLIT") == nullptr;
+  if (split) {
+    // SABER rows [0, ns) on the SABER-only kernel, static rows [ns, N) on the
+    // static-only kernel, concurrently (the second fills SMs as the first drains).
+    SimParams sa = sp, st = sp;
+    sa.mode_sel = 2;
+    sa.n_traj = P->n_saber_first;
+    st.mode_sel = 1;
+    st.first_traj = P->n_saber_first;
+    st.next_traj = P->cursor.as<int32_t>() + 1;
+    CUDA_TRY(cudaEventRecord(P->fork, s));
+    CUDA_TRY(cudaStreamWaitEvent(P->side, P->fork, 0));
+    LAUNCH_TRY(launch_sim(sa, P->scratch.launch, s));
+    LAUNCH_TRY(launch_sim(st, P->scratch.launch, P->side));
+    CUDA_TRY(cudaEventRecord(P->join, P->side));
+    CUDA_TRY(cudaStreamWaitEvent(s, P->join, 0));
+    P->launches += 2;
+  } else {
+    LAUNCH_TRY(launch_sim(sp, P->scratch.launch, s));
+    ++P->launches;
+  }
   CUDA_TRY(cudaEventRecord(P->sim.b, s));
-  ++P->launches;
 
   RowMetricsParams rm{};
   rm.rows = P->rows.as<saber_traj_row>();

@@ -106,6 +106,8 @@ struct SimParams {
   int32_t* next_traj;         // work-queue cursor (device)
   const int32_t* order;       // execution order of the descriptors (longest first), or null
   int32_t no_streak;          // 1 = disable quiet streaks (A/B runs, SABER_NO_STREAK)
+  int32_t mode_sel;           // 0 any, 1 static-only, 2 SABER-only kernel (sim_kernel.cu)
+  int32_t first_traj;         // this launch simulates order[first_traj .. n_traj)
   TickTable ticks;            // shared tick grid for quiet streaks
 };
 
@@ -126,6 +128,7 @@ struct SimLaunch {
   int lane;       // 1 = lane-per-trajectory lockstep kernel (sim_lane.cu)
   int block;      // threads per block
   int grid;       // persistent blocks
+  int grid_sel[3];  // persistent blocks per mode-specialised variant (G = 32)
   int slot_rows;  // group kernel: ceil(nmax / group); lane kernel: nmax
   size_t smem;    // dynamic shared memory per block
 };

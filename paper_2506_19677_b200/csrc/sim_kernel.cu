@@ -45,6 +45,15 @@ using namespace simdev;
 #ifndef SABER_SIM_MIN_BLOCKS
 #define SABER_SIM_MIN_BLOCKS 4
 #endif
+#ifndef SABER_STATIC_MIN_BLOCKS
+#define SABER_STATIC_MIN_BLOCKS 6
+#endif
+
+// Scheduler-mode specialisation of the trajectory kernel:
+// kSel 0 = any trajectory, 1 = static only, 2 = SABER only.  The specialised
+// variants drop the other mode's code (smaller footprint in the instruction
+// cache, fewer live registers) and serve the sweep's two row classes.
+enum : int { kSelAny = 0, kSelStatic = 1, kSelSaber = 2 };
 
 
 // Shared-memory slot arrays of one group: slot k lives at row k / G, column
@@ -212,7 +221,7 @@ __device__ __forceinline__ void gate_streak_decisions(
 }
 
 // Simulates trajectory `ti` on this group.
-template <int NW, int G, bool kTrace, bool kRecords>
+template <int NW, int G, bool kTrace, bool kRecords, int kSel>
 __device__ __forceinline__ void simulate_one(const SimParams& P, int ti, const Slots<G>& S,
                                              int sub, unsigned gmask,
                                              double* __restrict__ LNEED,
@@ -228,7 +237,13 @@ __device__ __forceinline__ void simulate_one(const SimParams& P, int ti, const S
   const double* __restrict__ IN = P.wl.input + wo;
   const double* __restrict__ DEM = P.wl.demote_after + wo;
   const double* __restrict__ GT = P.tables + d.gt_tab;
-  const bool saber = d.mode == SABER_MODE_SABER;
+  const bool saber = kSel == kSelSaber ? true
+                     : kSel == kSelStatic ? false
+                                          : d.mode == SABER_MODE_SABER;
+  if (kSel != kSelAny && saber != (d.mode == SABER_MODE_SABER)) {
+    if (sub == 0) atomicCAS(P.out.error, kErrNone, kErrBadDesc);  // loud: wrong kernel
+    return;
+  }
   const double* __restrict__ MT = P.tables + (saber ? d.model_tab : d.gt_tab);
   const double horizon = isnan(d.horizon) ? P.wl.horizon[d.workload] : d.horizon;
   const double tick = d.tick;
@@ -777,8 +792,10 @@ __device__ __forceinline__ void simulate_one(const SimParams& P, int ti, const S
   }
 }
 
-template <int NW, int G, bool kTrace, bool kRecords>
-__global__ void __launch_bounds__(kSimBlock, SABER_SIM_MIN_BLOCKS) sim_kernel(const SimParams P) {
+template <int NW, int G, bool kTrace, bool kRecords, int kSel>
+__global__ void __launch_bounds__(kSimBlock, kSel == kSelStatic ? SABER_STATIC_MIN_BLOCKS
+                                                                 : SABER_SIM_MIN_BLOCKS)
+    sim_kernel(const SimParams P) {
   extern __shared__ __align__(16) uint64_t smem[];
   __shared__ uint32_t inv[kMaxWindow + 1];  // ceil(2^32 / d) for d = 2..16
   if (threadIdx.x >= 2 && threadIdx.x <= kMaxWindow)
@@ -801,10 +818,10 @@ __global__ void __launch_bounds__(kSimBlock, SABER_SIM_MIN_BLOCKS) sim_kernel(co
   uint16_t* LOW = P.scratch.low_fifo + group_id * P.wl.nmax;
   for (;;) {
     int ti = 0;
-    if (sub == 0) ti = atomicAdd(P.next_traj, 1);
+    if (sub == 0) ti = P.first_traj + atomicAdd(P.next_traj, 1);
     ti = __shfl_sync(gmask, ti, grp * G);
     if (ti >= P.n_traj) break;
-    simulate_one<NW, G, kTrace, kRecords>(P, ti, S, sub, gmask, LNEED, LOW, inv);
+    simulate_one<NW, G, kTrace, kRecords, kSel>(P, ti, S, sub, gmask, LNEED, LOW, inv);
     __syncwarp(gmask);
   }
 }
@@ -863,39 +880,41 @@ __global__ void __launch_bounds__(128) row_metrics_kernel(const RowMetricsParams
   R->cv = mean == 0.0 ? nan("") : R->ratio_std / mean;
 }
 
-template <int NW, int G, bool kTrace, bool kRecords>
+template <int NW, int G, bool kTrace, bool kRecords, int kSel = kSelAny>
 void* kernel_ptr() {
-  return reinterpret_cast<void*>(&sim_kernel<NW, G, kTrace, kRecords>);
+  return reinterpret_cast<void*>(&sim_kernel<NW, G, kTrace, kRecords, kSel>);
 }
 
-using KernelGetter = void* (*)();
-
+// Mode-specialised variants exist for the bench path only: G = 32, no trace,
+// no per-request records; everything else uses kSelAny.
 template <int NW, int G>
-void* pick_tr(bool trace, bool records) {
+void* pick_tr(bool trace, bool records, int sel) {
   if (trace) return kernel_ptr<NW, G, true, true>();
   if (records) return kernel_ptr<NW, G, false, true>();
+  if (G == kWarp && sel == kSelStatic) return kernel_ptr<NW, kWarp, false, false, kSelStatic>();
+  if (G == kWarp && sel == kSelSaber) return kernel_ptr<NW, kWarp, false, false, kSelSaber>();
   return kernel_ptr<NW, G, false, false>();
 }
 
 template <int NW>
-void* pick_g(int g, bool trace, bool records) {
+void* pick_g(int g, bool trace, bool records, int sel) {
   switch (g) {
-    case 1: return pick_tr<NW, 1>(trace, records);
-    case 2: return pick_tr<NW, 2>(trace, records);
-    case 4: return pick_tr<NW, 4>(trace, records);
-    case 8: return pick_tr<NW, 8>(trace, records);
-    case 16: return pick_tr<NW, 16>(trace, records);
-    case 32: return pick_tr<NW, 32>(trace, records);
+    case 1: return pick_tr<NW, 1>(trace, records, sel);
+    case 2: return pick_tr<NW, 2>(trace, records, sel);
+    case 4: return pick_tr<NW, 4>(trace, records, sel);
+    case 8: return pick_tr<NW, 8>(trace, records, sel);
+    case 16: return pick_tr<NW, 16>(trace, records, sel);
+    case 32: return pick_tr<NW, 32>(trace, records, sel);
   }
   return nullptr;
 }
 
-void* pick_kernel(int nw, int g, bool trace, bool records) {
+void* pick_kernel(int nw, int g, bool trace, bool records, int sel = kSelAny) {
   switch (nw) {
-    case 1: return pick_g<1>(g, trace, records);
-    case 2: return pick_g<2>(g, trace, records);
-    case 4: return pick_g<4>(g, trace, records);
-    case 8: return pick_g<8>(g, trace, records);
+    case 1: return pick_g<1>(g, trace, records, sel);
+    case 2: return pick_g<2>(g, trace, records, sel);
+    case 4: return pick_g<4>(g, trace, records, sel);
+    case 8: return pick_g<8>(g, trace, records, sel);
   }
   return nullptr;
 }
@@ -920,16 +939,21 @@ int plan_sim(int nmax, int group, SimLaunch* out) {
   if (cudaGetDevice(&dev) != cudaSuccess) return 1;
   if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) return 1;
   for (int tr = 0; tr < 2; ++tr)
-    for (int rec = 0; rec < 2; ++rec) {
-      void* kk = pick_kernel(l.nwords, group, tr != 0, rec != 0);
-      if (cudaFuncSetAttribute(kk, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               static_cast<int>(l.smem)) != cudaSuccess)
-        return 2;
-    }
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, kSimBlock, l.smem) != cudaSuccess)
-    return 1;
-  if (per_sm < 1) return 3;
-  l.grid = sms * per_sm;
+    for (int rec = 0; rec < 2; ++rec)
+      for (int sel = 0; sel < 3; ++sel) {
+        void* kk = pick_kernel(l.nwords, group, tr != 0, rec != 0, sel);
+        if (cudaFuncSetAttribute(kk, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(l.smem)) != cudaSuccess)
+          return 2;
+      }
+  for (int sel = 0; sel < 3; ++sel) {
+    void* kk = pick_kernel(l.nwords, group, false, false, sel);
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kk, kSimBlock, l.smem) != cudaSuccess)
+      return 1;
+    if (per_sm < 1) return 3;
+    l.grid_sel[sel] = sms * per_sm;
+  }
+  l.grid = l.grid_sel[0];
   l.lane = 0;
   l.block = kSimBlock;
   *out = l;
@@ -940,12 +964,14 @@ int launch_sim(const SimParams& p, const SimLaunch& l, void* stream) {
   if (l.lane) return launch_sim_lane(p, l, stream);
   const bool trace = p.out.trace != nullptr;
   const bool records = p.out.admit != nullptr || p.out.demoted != nullptr;
-  void* k = pick_kernel(l.nwords, l.group, trace, records);
+  const int sel = p.mode_sel;
+  void* k = pick_kernel(l.nwords, l.group, trace, records, sel);
   if (!k) return 1;
+  const int grid = (l.group == kWarp && !trace && !records) ? l.grid_sel[sel] : l.grid;
   SimParams q = p;
   q.no_streak = std::getenv("SABER_NO_STREAK") != nullptr;
   void* args[] = {&q};
-  return cudaLaunchKernel(k, dim3(l.grid), dim3(kSimBlock), args, l.smem,
+  return cudaLaunchKernel(k, dim3(grid), dim3(kSimBlock), args, l.smem,
                           static_cast<cudaStream_t>(stream)) == cudaSuccess
              ? 0
              : 1;
