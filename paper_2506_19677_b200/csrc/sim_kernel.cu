@@ -70,10 +70,14 @@ struct Slots {
   }
 };
 
-// An integer q <= a / b (a >= 0 finite, b > 0), capped at 2^30: float
-// arithmetic with directed rounding keeps it a lower bound without a DDIV.
+// An integer q <= a / b (a >= 0 finite, b > 0), capped at 2^30, without a
+// DDIV: b is rounded up and a down to float, the approximate reciprocal
+// (MUFU, |rel err| < 2^-22) and the product are scaled down by 4e-5, so the
+// result is a strict lower bound of the true quotient.
 __device__ __forceinline__ int floor_div_lb(double a, double b) {
-  const float q = __fmul_rd(__double2float_rd(a), __frcp_rd(__double2float_ru(b)));
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(__double2float_ru(b)));
+  const float q = __double2float_rd(a) * (r * 0.99996f);
   return static_cast<int>(fminf(q, 1073741824.0f));
 }
 
@@ -87,39 +91,44 @@ __device__ __forceinline__ int tick_index(const TickTable& tt, double x) {
 
 // Quiet streak: K consecutive ticks k0 .. k0+K-1, each one
 // full quiet pass of dt = DT[k], applied slot by slot from registers.
-// Per pass the reference computes g += speed*dt (decode) or
-// prefill_left -= dt (prefill, stored as g = -prefill_left), which is exactly
-// what runs here; the caller has proved that no pass of the streak ends a
-// prefill, binds the decode boundary or completes a slot.
-template <int G>
-__device__ __forceinline__ void streak_slots(const Slots<G>& S, int sub, int A, double speed,
-                                             const double* __restrict__ DT, int K) {
-  constexpr int kC = G >= 16 ? 2 : 4;  // slots per lane per chunk (registers)
-  for (int base = sub; base < A; base += kC * G) {
-    double g[kC];
-    double pre[kC];  // 1.0 for prefill slots, 0.0 for decode slots
+// Per pass the reference computes generated += speed*dt (decode) or
+// prefill_left -= dt (prefill, stored as g = -prefill_left); here every slot
+// adds fl(mult * dt) with mult = speed (decode) or 1.0 (prefill: fl(1*dt) = dt),
+// which is that same value.  The caller has proved that no pass of the streak
+// ends a prefill, binds the decode boundary or completes a slot.  Returns the
+// exact prefill minimum after the streak (the per-pass chain min_pf -= dt).
+template <int G, int kC>
+__device__ __forceinline__ double streak_chunks(const Slots<G>& S, int sub, int A, double speed,
+                                               const double* __restrict__ DT, int K, double pf) {
+  // Chunk 0 runs on every lane of the group (it also carries the replicated
+  // min_pf chain); later chunks only while the lane still owns slots.
+  for (int base = sub, first = 1; first || base < A; base += kC * G, first = 0) {
+    double g[kC], mult[kC];
 #pragma unroll
     for (int i = 0; i < kC; ++i) {
       const int k = base + i * G;
       g[i] = k < A ? S.g[S.idx(k)] : 0.0;
-      pre[i] = g[i] < 0.0 ? 1.0 : 0.0;
+      mult[i] = g[i] < 0.0 ? 1.0 : speed;
     }
     int j = 0;
 #pragma unroll 1
-    for (; j + 2 <= K; j += 2) {
-      const double d0 = DT[j], d1 = DT[j + 1];
-      const double s0 = speed * d0, s1 = speed * d1;
+    for (; j + 4 <= K; j += 4) {
+      const double d0 = DT[j], d1 = DT[j + 1], d2 = DT[j + 2], d3 = DT[j + 3];
 #pragma unroll
       for (int i = 0; i < kC; ++i) {
-        g[i] = g[i] + (pre[i] != 0.0 ? d0 : s0);
-        g[i] = g[i] + (pre[i] != 0.0 ? d1 : s1);
+        g[i] = g[i] + mult[i] * d0;
+        g[i] = g[i] + mult[i] * d1;
+        g[i] = g[i] + mult[i] * d2;
+        g[i] = g[i] + mult[i] * d3;
       }
+      if (first) pf = (((pf - d0) - d1) - d2) - d3;
     }
-    if (j < K) {
+#pragma unroll 1
+    for (; j < K; ++j) {
       const double d0 = DT[j];
-      const double s0 = speed * d0;
 #pragma unroll
-      for (int i = 0; i < kC; ++i) g[i] = g[i] + (pre[i] != 0.0 ? d0 : s0);
+      for (int i = 0; i < kC; ++i) g[i] = g[i] + mult[i] * d0;
+      if (first) pf = pf - d0;
     }
 #pragma unroll
     for (int i = 0; i < kC; ++i) {
@@ -127,6 +136,15 @@ __device__ __forceinline__ void streak_slots(const Slots<G>& S, int sub, int A, 
       if (k < A) S.g[S.idx(k)] = g[i];
     }
   }
+  return pf;
+}
+
+template <int G>
+__device__ __forceinline__ double streak_slots(const Slots<G>& S, int sub, int A, double speed,
+                                               const double* __restrict__ DT, int K, double pf) {
+  if (A <= G) return streak_chunks<G, 1>(S, sub, A, speed, DT, K, pf);
+  if (A <= 2 * G) return streak_chunks<G, 2>(S, sub, A, speed, DT, K, pf);
+  return streak_chunks<G, 4>(S, sub, A, speed, DT, K, pf);
 }
 
 // Gate streak decisions: ticks k0+1 .. k0+K-1 of a streak
@@ -536,12 +554,8 @@ __device__ __forceinline__ void simulate_one(const SimParams& P, int ti, const S
           use_tab = false;
         } else {
           const double* __restrict__ DTk = P.ticks.DT + k0;
-          streak_slots<G>(S, sub, A, speed_A, DTk, K);
-          if (npre > 0) {
-            double pf = min_pf;
-            for (int j = 0; j < K; ++j) pf = pf - DTk[j];
-            min_pf = pf;  // exact, as the per-pass updates
-          }
+          // min_pf stays exact: the same per-pass chain min_pf -= dt
+          min_pf = streak_slots<G>(S, sub, A, speed_A, DTk, K, min_pf);
           if (A > npre) rem_lb = rem_lb - static_cast<double>(K) * delta;
           rem_exact = false;
           if (gate_streak) {

@@ -1,10 +1,17 @@
 """Aggregate an ncu SASS-page CSV by CUDA source line using nvdisasm line info."""
 import csv, re, subprocess, sys, collections
 rep, cubin, func_pat = sys.argv[1], sys.argv[2], sys.argv[3]
+import os
 out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"],
                      capture_output=True, text=True).stdout
 r = list(csv.reader(out.splitlines()))
-h = r[1]; rows = r[2:]
+# one section per profiled kernel: ["Kernel Name", name], header, rows...; pick by NCU_KERNEL_SUB
+sub = os.environ.get("NCU_KERNEL_SUB", "")
+starts = [i for i, x in enumerate(r) if x and x[0] == "Kernel Name"] + [len(r)]
+for a, b in zip(starts, starts[1:]):
+    if sub in r[a][1]:
+        h = r[a + 1]; rows = r[a + 2:b]
+        break
 I = lambda n: h.index(n)
 # nvdisasm with line info
 dis = subprocess.run(["nvdisasm", "-g", "-c", cubin], capture_output=True, text=True).stdout
