@@ -70,6 +70,30 @@ __device__ __forceinline__ unsigned group_sum(unsigned v, unsigned gmask) {
   return __reduce_add_sync(gmask, v);
 }
 
+// Position of the k-th set bit of x (0-based, k < popc(x)): branch-free
+// binary search on popcounts (no data-dependent loop, so lanes asking for
+// different k stay converged).
+__device__ __forceinline__ int select64(uint64_t x, int k) {
+  uint32_t v = static_cast<uint32_t>(x);
+  int pos = 0;
+  int c = __popc(v);
+  if (k >= c) {
+    k -= c;
+    pos = 32;
+    v = static_cast<uint32_t>(x >> 32);
+  }
+  c = __popc(v & 0xFFFFu);
+  if (k >= c) { k -= c; pos += 16; v >>= 16; }
+  c = __popc(v & 0xFFu);
+  if (k >= c) { k -= c; pos += 8; v >>= 8; }
+  c = __popc(v & 0xFu);
+  if (k >= c) { k -= c; pos += 4; v >>= 4; }
+  c = __popc(v & 0x3u);
+  if (k >= c) { k -= c; pos += 2; v >>= 2; }
+  if (k >= static_cast<int>(v & 1u)) pos += 1;
+  return pos;
+}
+
 // Per-request tier membership as an NW x 64-bit register bitmask.  Built as a
 // recursive struct of scalar words (no array), so a runtime word index can
 // never turn into a local-memory access.
@@ -102,11 +126,7 @@ struct Mask {
   // k-th set bit in ascending id order (0-based); k < count().
   __device__ __forceinline__ int select(int k) const {
     const int c = __popcll(w);
-    if (k < c) {
-      uint64_t x = w;
-      for (int j = 0; j < k; ++j) x &= x - 1;
-      return B * 64 + __ffsll(static_cast<long long>(x)) - 1;
-    }
+    if (k < c) return B * 64 + select64(w, k);
     return r.select(k - c);
   }
 };

@@ -391,56 +391,76 @@ __device__ __forceinline__ void simulate_one(const SimParams& P, int ti, const S
         // admission_step, high tier (scheduler.cpp:58-95).
         const int hcount = high.count();
         const int w = d.window < hcount ? d.window : hcount;
-        uint64_t ord = 0xFEDCBA9876543210ull;  // window positions as nibbles
         if (draw_pos + (w - 1) > draw_len) {
           failed = true;
           break;
         }
         // Fisher-Yates over the window: j = rng() % (i+1) for i = w-1..1.
         // Draws are stored mod lcm(1..16); x % d is exact via the reciprocal
-        // table (x < 2^20).
-        // All w-1 draws are independent loads, issued before the shuffle
-        // consumes them (the loop over draw index q is unrolled, so the
-        // registers are indexed statically).
+        // table (x < 2^20).  All w-1 draws are independent
+        // loads, issued before anything consumes them.
         uint32_t xq[kMaxWindow - 1];
 #pragma unroll
         for (int q = 0; q < kMaxWindow - 1; ++q) xq[q] = q < w - 1 ? draws[draw_pos + q] : 0u;
+        const double pred = MT[load + 1];
+        const bool violates = pred < ledger_max;  // ActiveLedger::violates
+        unsigned okmask = 0;
+        // The gate (scheduler.cpp:71-94), evaluated for the whole window at
+        // once.  Candidate c is admitted iff it is the first with pred >= need
+        // and no ledger violation; decisions are then emitted in shuffled order.
+        constexpr int kQ = G >= kMaxWindow ? 1 : (kMaxWindow + G - 1) / G;
+        int cid[kQ];
+        double cneed[kQ];
+        if constexpr (G >= kMaxWindow) {
+          // Lane c owns shuffled position c.  The element FY leaves at c is
+          // tau_{w-1}(...tau_1(c)) with tau_i = (i j_i): walked forward over
+          // i = 1..w-1 with compares and selects, all lanes at once.
+          int pos = sub;
 #pragma unroll
-        for (int q = 0; q < kMaxWindow - 1; ++q) {
-          if (q < w - 1) {
-            const int i = w - 1 - q;
-            const uint32_t d1 = static_cast<uint32_t>(i + 1);
-            const uint32_t j = xq[q] - __umulhi(xq[q], INV[d1]) * d1;
-            const uint64_t a = (ord >> (4 * i)) & 15ull;
-            const uint64_t bb = (ord >> (4 * j)) & 15ull;
-            const uint64_t x2 = a ^ bb;
-            ord ^= (x2 << (4 * i)) | (x2 << (4 * j));
+          for (int q = kMaxWindow - 2; q >= 0; --q) {
+            if (q < w - 1) {
+              const int i = w - 1 - q;  // draw q serves swap i
+              const uint32_t d1 = static_cast<uint32_t>(i + 1);
+              const int j = static_cast<int>(xq[q] - __umulhi(xq[q], INV[d1]) * d1);
+              pos = pos == i ? j : (pos == j ? i : pos);
+            }
+          }
+          cid[0] = 0;
+          cneed[0] = 0.0;
+          if (sub < w) {
+            cid[0] = high.select(pos);
+            cneed[0] = queued_need(MO[cid[0]], DL[cid[0]], t);
+            if (!(pred < cneed[0]) && !violates) okmask = 1u << sub;
+          }
+        } else {
+          uint64_t ord = 0xFEDCBA9876543210ull;  // window positions as nibbles
+#pragma unroll
+          for (int q = 0; q < kMaxWindow - 1; ++q) {
+            if (q < w - 1) {
+              const int i = w - 1 - q;
+              const uint32_t d1 = static_cast<uint32_t>(i + 1);
+              const uint32_t j = xq[q] - __umulhi(xq[q], INV[d1]) * d1;
+              const uint64_t a = (ord >> (4 * i)) & 15ull;
+              const uint64_t bb = (ord >> (4 * j)) & 15ull;
+              const uint64_t x2 = a ^ bb;
+              ord ^= (x2 << (4 * i)) | (x2 << (4 * j));
+            }
+          }
+#pragma unroll
+          for (int q = 0; q < kQ; ++q) {
+            const int c = sub + G * q;
+            cid[q] = 0;
+            cneed[q] = 0.0;
+            if (c < w) {
+              cid[q] = high.select(static_cast<int>((ord >> (4 * c)) & 15ull));
+              cneed[q] = queued_need(MO[cid[q]], DL[cid[q]], t);
+              if (!(pred < cneed[q]) && !violates) okmask |= 1u << c;
+            }
           }
         }
         draw_pos += w - 1;
         rng_draws += w - 1;
-        const double pred = MT[load + 1];
-        const bool violates = pred < ledger_max;  // ActiveLedger::violates
         ledger_scanned += ledger_size;
-        // The gate (scheduler.cpp:71-94), evaluated for the whole window at
-        // once: lane sub of the group takes shuffled positions c = sub + G*q.
-        // Candidate c is admitted iff it is the first with pred >= need and no
-        // ledger violation; decisions are then emitted in shuffled order.
-        constexpr int kQ = (kMaxWindow + G - 1) / G;
-        int cid[kQ];
-        double cneed[kQ];
-        unsigned okmask = 0;
-#pragma unroll
-        for (int q = 0; q < kQ; ++q) {
-          const int c = sub + G * q;
-          cid[q] = 0;
-          cneed[q] = 0.0;
-          if (c < w) {
-            cid[q] = high.select(static_cast<int>((ord >> (4 * c)) & 15ull));
-            cneed[q] = queued_need(MO[cid[q]], DL[cid[q]], t);
-            if (!(pred < cneed[q]) && !violates) okmask |= 1u << c;
-          }
-        }
         if (G > 1) okmask = __reduce_or_sync(gmask, okmask);
         const int first = okmask ? __ffs(okmask) - 1 : w;  // admitted position, or none
         gate_idle = first == w;
