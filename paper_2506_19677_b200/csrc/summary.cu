@@ -235,19 +235,31 @@ __global__ void __launch_bounds__(64) summary_mix_kernel(const SummaryParams p) 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   __shared__ double ring[2][kChunk];
   __shared__ double s_out[3];
+  __shared__ int64_t s_cnt;
   const double* sc = p.scratch + static_cast<int64_t>(mi) * p.n_rps * kCellScratch;
   const bool present = variant == 0 ? p.with_saber != 0 : p.n_caps > 0;
   const int64_t total = present ? pool_length(p, mi, variant) : 0;
   const int chunks = present ? static_cast<int>((total + kChunk - 1) / kChunk) : 0;
   double sum = 0.0, acc = 0.0, mean = 0.0;
-  int64_t cnt = 0;
+  int64_t cnt = 0;  // completed ratios in the pool (counted by the loader warp)
   for (int pass = 0; pass < 2; ++pass) {
     if (pass == 1) {
+      if (warp == 1) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(kFull, cnt, o);
+        if (lane == 0) s_cnt = cnt;
+      }
+      __syncthreads();
+      cnt = s_cnt;
       if (threadIdx.x == 0) s_out[0] = cnt > 0 ? sum / static_cast<double>(cnt) : 0.0;
       __syncthreads();
       mean = s_out[0];
       if (!(cnt > 0 && mean != 0.0)) break;
     }
+    // Never-completed requests (NaN) are not in the reference's pool; the
+    // loader replaces them by a value whose contribution is an exact +0:
+    // 0.0 in the sum (sum >= +0) and the mean in the squared deviations.
+    const double fill = pass == 0 ? 0.0 : mean;
     // loader state (warp 1): current segment and offset in it
     SegmentWalk walk;
     const double* sp = nullptr;
@@ -260,7 +272,24 @@ __global__ void __launch_bounds__(64) summary_mix_kernel(const SummaryParams p) 
         while (filled < kChunk && have) {
           const int64_t avail = slen - off;
           const int take = static_cast<int>(avail < kChunk - filled ? avail : kChunk - filled);
-          for (int i = lane; i < take; i += 32) dst[filled + i] = sp[off + i];
+          // eight independent loads in flight per lane before any store
+          for (int i0 = 0; i0 < take; i0 += 8 * 32) {
+            double v[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+              const int i = i0 + u * 32 + lane;
+              v[u] = i < take ? sp[off + i] : 0.0;
+            }
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+              const int i = i0 + u * 32 + lane;
+              if (i < take) {
+                const bool ok = !isnan(v[u]);
+                dst[filled + i] = ok ? v[u] : fill;
+                if (pass == 0) cnt += ok;
+              }
+            }
+          }
           filled += take;
           off += take;
           if (off == slen) {
@@ -268,25 +297,52 @@ __global__ void __launch_bounds__(64) summary_mix_kernel(const SummaryParams p) 
             off = 0;
           }
         }
-        for (int i = filled + lane; i < kChunk; i += 32) dst[i] = nan("");
+        for (int i = filled + lane; i < kChunk; i += 32) dst[i] = fill;
       }
       if (warp == 0 && lane == 0 && c > 0) {
+        // The dependent add chain, eight values per step with every shared
+        // load of the step issued before its first add.
         const double2* src = reinterpret_cast<const double2*>(ring[(c - 1) & 1]);
+        // software-pipelined: the next eight values are loaded while the
+        // current eight run through the chain
+        double2 a0 = src[0], a1 = src[1], a2 = src[2], a3 = src[3];
         if (pass == 0) {
-          for (int i = 0; i < kChunk / 2; ++i) {
-            const double2 v = src[i];
-            const bool a = !isnan(v.x), b = !isnan(v.y);
-            sum += a ? v.x : 0.0;  // sum >= +0, ratios >= 0: adding +0.0 is exact
-            sum += b ? v.y : 0.0;
-            cnt += a + b;
+#pragma unroll 1
+          for (int i = 4; i <= kChunk / 2; i += 4) {
+            const int k = i < kChunk / 2 ? i : 0;
+            const double2 b0 = src[k], b1 = src[k + 1], b2 = src[k + 2], b3 = src[k + 3];
+            sum += a0.x;
+            sum += a0.y;
+            sum += a1.x;
+            sum += a1.y;
+            sum += a2.x;
+            sum += a2.y;
+            sum += a3.x;
+            sum += a3.y;
+            a0 = b0;
+            a1 = b1;
+            a2 = b2;
+            a3 = b3;
           }
         } else {
-          for (int i = 0; i < kChunk / 2; ++i) {
-            const double2 v = src[i];
-            const double dx = isnan(v.x) ? 0.0 : (v.x - mean) * (v.x - mean);
-            const double dy = isnan(v.y) ? 0.0 : (v.y - mean) * (v.y - mean);
-            acc += dx;
-            acc += dy;
+#pragma unroll 1
+          for (int i = 4; i <= kChunk / 2; i += 4) {
+            const int k = i < kChunk / 2 ? i : 0;
+            const double2 b0 = src[k], b1 = src[k + 1], b2 = src[k + 2], b3 = src[k + 3];
+            const double e0 = a0.x - mean, e1 = a0.y - mean, e2 = a1.x - mean, e3 = a1.y - mean;
+            const double e4 = a2.x - mean, e5 = a2.y - mean, e6 = a3.x - mean, e7 = a3.y - mean;
+            acc += e0 * e0;
+            acc += e1 * e1;
+            acc += e2 * e2;
+            acc += e3 * e3;
+            acc += e4 * e4;
+            acc += e5 * e5;
+            acc += e6 * e6;
+            acc += e7 * e7;
+            a0 = b0;
+            a1 = b1;
+            a2 = b2;
+            a3 = b3;
           }
         }
       }
