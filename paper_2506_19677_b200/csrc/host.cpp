@@ -324,9 +324,13 @@ struct Scratch {
     if (rc != 0)
       return fail(SABER_ECUDA, "trajectory kernel configuration failed (" + std::to_string(rc) +
                                    "): " + cudaGetErrorString(cudaGetLastError()));
+    // one ledger / low-FIFO slice per resident group of the LARGEST grid any
+    // kernel variant launches with (the mode-specialised grids differ)
+    int64_t grid = launch.grid;
+    if (!launch.lane)
+      for (int v = 0; v < 3; ++v) grid = std::max<int64_t>(grid, launch.grid_sel[v]);
     const int64_t groups = launch.lane ? static_cast<int64_t>(launch.grid) * launch.block
-                                       : static_cast<int64_t>(launch.grid) * (kSimBlock / kWarp) *
-                                             (kWarp / launch.group);
+                                       : grid * (kSimBlock / kWarp) * (kWarp / launch.group);
     const size_t per = static_cast<size_t>(nmax);
     ALLOC_TRY(ledger, device, static_cast<size_t>(groups) * per * sizeof(double));
     ALLOC_TRY(low, device, static_cast<size_t>(groups) * per * sizeof(uint16_t));

@@ -48,6 +48,9 @@ using namespace simdev;
 #ifndef SABER_STATIC_MIN_BLOCKS
 #define SABER_STATIC_MIN_BLOCKS 6
 #endif
+#ifndef SABER_SABER_MIN_BLOCKS
+#define SABER_SABER_MIN_BLOCKS 4
+#endif
 
 // Scheduler-mode specialisation of the trajectory kernel:
 // kSel 0 = any trajectory, 1 = static only, 2 = SABER only.  The specialised
@@ -827,7 +830,8 @@ __device__ __forceinline__ void simulate_one(const SimParams& P, int ti, const S
 }
 
 template <int NW, int G, bool kTrace, bool kRecords, int kSel>
-__global__ void __launch_bounds__(kSimBlock, kSel == kSelStatic ? SABER_STATIC_MIN_BLOCKS
+__global__ void __launch_bounds__(kSimBlock, kSel == kSelStatic  ? SABER_STATIC_MIN_BLOCKS
+                                             : kSel == kSelSaber ? SABER_SABER_MIN_BLOCKS
                                                                  : SABER_SIM_MIN_BLOCKS)
     sim_kernel(const SimParams P) {
   extern __shared__ __align__(16) uint64_t smem[];
@@ -848,6 +852,10 @@ __global__ void __launch_bounds__(kSimBlock, kSel == kSelStatic ? SABER_STATIC_M
   S.col0 = grp * G;
   const int64_t group_id =
       (static_cast<int64_t>(blockIdx.x) * (kSimBlock / kWarp) + warp) * (kWarp / G) + grp;
+  if (group_id >= P.scratch.groups) {  // scratch sized for a smaller grid: loud, never silent
+    if (lane == 0) atomicCAS(P.out.error, kErrNone, kErrBadDesc);
+    return;
+  }
   double* LNEED = P.scratch.ledger_need + group_id * P.wl.nmax;
   uint16_t* LOW = P.scratch.low_fifo + group_id * P.wl.nmax;
   for (;;) {
