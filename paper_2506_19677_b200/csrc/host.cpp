@@ -343,6 +343,7 @@ struct Scratch {
 
 struct Workloads {
   DevBuf arr, dl, sla, mo, in, task, dem, hor, items, seed_base, th, tt, tl;
+  DevBuf ka, kd;  // tick-table indices of arrival / demote_after (launch_tick_index)
   WorkloadTables view(int nmax) const {
     WorkloadTables w;
     w.arrival = arr.as<double>();
@@ -353,6 +354,8 @@ struct Workloads {
     w.task = task.as<int8_t>();
     w.demote_after = dem.as<double>();
     w.horizon = hor.as<double>();
+    w.arr_tick = ka.p ? ka.as<int32_t>() : nullptr;
+    w.dem_tick = kd.p ? kd.as<int32_t>() : nullptr;
     w.nmax = nmax;
     return w;
   }
@@ -688,6 +691,10 @@ saber_status saber_cuda_sweep_plan_create(const saber_sweep_desc* desc, saber_sw
   tr.mark("h2d");
   if (saber_status s = P->ticktab.build(dev, desc->tick, hb_max)) return s;
   P->h2d_bytes += P->ticktab.bytes;
+  if (P->ticktab.view.len > 0) {
+    ALLOC_TRY(P->wl.ka, dev, static_cast<size_t>(P->n_items) * n * 4);
+    ALLOC_TRY(P->wl.kd, dev, static_cast<size_t>(P->n_items) * n * 4);
+  }
   tr.mark("tick table");
   if (saber_status s = P->all.init()) return s;
   if (saber_status s = P->sim.init()) return s;
@@ -734,6 +741,11 @@ saber_status saber_cuda_sweep_plan_run(saber_sweep_plan* P, void* stream) {
   wp.nmax = P->n;
   LAUNCH_TRY(launch_workloads(wp, s));
   ++P->launches;
+  if (P->wl.ka.p) {
+    LAUNCH_TRY(launch_tick_index(P->wl.view(P->n), static_cast<int64_t>(P->n_items) * P->n,
+                                 P->ticktab.view, P->wl.ka.as<int32_t>(), P->wl.kd.as<int32_t>(), s));
+    ++P->launches;
+  }
 
   if (d.with_saber) {
     RngGenParams rg{};
@@ -1157,6 +1169,10 @@ extern "C" saber_status saber_cuda_run_batch(const saber_run_batch_desc* desc,
       }
     if (best_n > 0)
       if (saber_status s = ticktab.build(dev, best_tick, best_hb)) return s;
+    if (ticktab.view.len > 0) {
+      ALLOC_TRY(wl.ka, dev, cells * 4);
+      ALLOC_TRY(wl.kd, dev, cells * 4);
+    }
   }
 
   CUDA_TRY(cudaMemcpy(wl.items.p, items.data(), items.size() * sizeof(WorkloadItem), cudaMemcpyHostToDevice));
@@ -1212,6 +1228,11 @@ extern "C" saber_status saber_cuda_run_batch(const saber_run_batch_desc* desc,
   wp.nmax = nmax;
   LAUNCH_TRY(launch_workloads(wp, st));
   ++launches;
+  if (wl.ka.p) {
+    LAUNCH_TRY(launch_tick_index(wl.view(nmax), static_cast<int64_t>(cells), ticktab.view,
+                                 wl.ka.as<int32_t>(), wl.kd.as<int32_t>(), st));
+    ++launches;
+  }
   if (!seeds.empty()) {
     RngGenParams rg{};
     rg.seeds = seeds_d.as<uint64_t>();
@@ -1597,6 +1618,10 @@ extern "C" saber_status saber_cuda_mc_sweep(const saber_mc_desc* desc, saber_mc_
     ++launches;
     CUDA_TRY(cudaMemcpy(&hm, hmax.p, 8, cudaMemcpyDeviceToHost));
     if (saber_status s = ticktab.build(dev, d.tick, hm + 1.0)) return s;
+    if (ticktab.view.len > 0) {
+      ALLOC_TRY(wl.ka, dev, static_cast<size_t>(chunk) * n * 4);
+      ALLOC_TRY(wl.kd, dev, static_cast<size_t>(chunk) * n * 4);
+    }
   }
   if (d.with_saber && mine > 0) {
     pool = static_cast<int32_t>(std::min<int64_t>(d.scheduler_seeds, d.n_traj));
@@ -1629,7 +1654,9 @@ extern "C" saber_status saber_cuda_mc_sweep(const saber_mc_desc* desc, saber_mc_
     mp.k0 = k0;
     mp.count = std::min<int64_t>(chunk, mine - k0);
     LAUNCH_TRY(launch_mc_workloads(mp, st));
-    CUDA_TRY(cudaMemsetAsync(rows.p, 0, static_cast<size_t>(mp.count) * sizeof(saber_traj_row), st));
+    if (wl.ka.p)
+      LAUNCH_TRY(launch_tick_index(wl.view(n), mp.count * n, ticktab.view, wl.ka.as<int32_t>(),
+                                   wl.kd.as<int32_t>(), st));    CUDA_TRY(cudaMemsetAsync(rows.p, 0, static_cast<size_t>(mp.count) * sizeof(saber_traj_row), st));
     CUDA_TRY(cudaMemsetAsync(cursor.p, 0, 16, st));
     LAUNCH_TRY(launch_fill_rows(comp.as<double>(), mp.count, n, 0, 1, st));
     SimParams sp{};

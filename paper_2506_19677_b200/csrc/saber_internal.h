@@ -30,6 +30,8 @@ struct WorkloadTables {
   const int8_t* task;      // [W][nmax]  catalog index or -1
   const double* demote_after;  // [W][nmax] safe lower bound on demotion time
   const double* horizon;   // [W]  last arrival + 10 * max sla (simloop.cpp:60-63)
+  const int32_t* arr_tick;  // [W][nmax] first tick-table index >= arrival, or null
+  const int32_t* dem_tick;  // [W][nmax] first tick-table index >= demote_after, or null
   int32_t nmax;
 };
 
@@ -135,6 +137,10 @@ struct SimLaunch {
 constexpr int kSimBlock = 128;
 int plan_sim(int nmax, int group, SimLaunch* out);
 int launch_sim(const SimParams& p, const SimLaunch& l, void* stream);
+// Tick-table indices of every request's arrival and demote_after (quiet
+// streak bounds without table searches on the trajectory's critical path).
+int launch_tick_index(const WorkloadTables& wl, int64_t cells, const TickTable& tt, int32_t* ka,
+                      int32_t* kd, void* stream);
 // Lane-per-trajectory lockstep kernel: n <= 128, max_output_tokens < 2^23.
 constexpr int kLaneMaxRequests = 128;
 constexpr double kLaneMaxOutput = 8388607.0;

@@ -52,6 +52,14 @@ using namespace simdev;
 #define SABER_SABER_MIN_BLOCKS 4
 #endif
 
+#ifdef SABER_STREAK_STATS
+#define SEC_BEGIN() const long long sec_t0_ = clock64()
+#define SEC_END(k) st_cyc[k] += clock64() - sec_t0_
+#else
+#define SEC_BEGIN()
+#define SEC_END(k)
+#endif
+
 // Scheduler-mode specialisation of the trajectory kernel:
 // kSel 0 = any trajectory, 1 = static only, 2 = SABER only.  The specialised
 // variants drop the other mode's code (smaller footprint in the instruction
@@ -84,12 +92,23 @@ __device__ __forceinline__ int floor_div_lb(double a, double b) {
   return static_cast<int>(fminf(q, 1073741824.0f));
 }
 
-// min{k : T[k] >= x} over the tick table (len if none; x may be +inf).
+// min{k : T[k] >= x} over the tick table (len if none; x may be +-inf;
+// NaN maps to len).
 __device__ __forceinline__ int tick_index(const TickTable& tt, double x) {
+  if (isnan(x)) return tt.len;
   int k = static_cast<int>(fmin(fmax(x * tt.inv_tick, 0.0), static_cast<double>(tt.len)));
   while (k > 0 && tt.T[k - 1] >= x) --k;
   while (k < tt.len && tt.T[k] < x) ++k;
   return k;
+}
+
+__global__ void tick_index_kernel(const WorkloadTables wl, int64_t cells, const TickTable tt,
+                                  int32_t* ka, int32_t* kd) {
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < cells;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    ka[i] = tick_index(tt, wl.arrival[i]);
+    kd[i] = tick_index(tt, wl.demote_after[i]);
+  }
 }
 
 // Quiet streak: K consecutive ticks k0 .. k0+K-1, each one
@@ -334,12 +353,19 @@ __device__ __forceinline__ void simulate_one(const SimParams& P, int ti, const S
 
   // Tick table: kh = first tick index at/after the horizon,
   // ka = first tick index at/after the next arrival (lazily, -1 = stale).
-  bool use_tab = !P.no_streak && P.ticks.len > 0 && tick == P.ticks.tick;
+  const int32_t* __restrict__ KA = P.wl.arr_tick ? P.wl.arr_tick + wo : nullptr;
+  const int32_t* __restrict__ KD = P.wl.dem_tick ? P.wl.dem_tick + wo : nullptr;
+  bool use_tab = !P.no_streak && P.ticks.len > 0 && tick == P.ticks.tick && KA != nullptr;
   const int kh = use_tab ? tick_index(P.ticks, horizon) : 0;
-  int ka = -1;
+  // tick index of the next arrival, and of min_td (tick_index is monotone, so
+  // it follows min_td's own updates: min at arrival, recomputed at a scan)
+  int ka = use_tab ? (n > 0 ? KA[0] : P.ticks.len) : 0;
+  int min_kd = 0x7FFFFFFF;
 #ifdef SABER_STREAK_STATS
   int st_ticks = 0, st_count = 0, st_quiet = 0, st_exact = 0;
   const long long st_t0 = clock64();
+  long long st_cyc[5] = {0, 0, 0, 0, 0};
+  int st_scans = 0;
 #endif
 
   double t = 0.0;
@@ -348,9 +374,10 @@ __device__ __forceinline__ void simulate_one(const SimParams& P, int ti, const S
     while (na_t <= t) {
       high.set(next);
       if (saber) min_td = dmin(min_td, DEM[next]);
+      if (saber && use_tab) min_kd = min(min_kd, KD[next]);
       ++next;
       na_t = next < n ? ARR[next] : kInf;
-      ka = -1;
+      if (use_tab) ka = next < n ? KA[next] : P.ticks.len;
     }
     ++ticks;
     const int load = A;
@@ -358,13 +385,21 @@ __device__ __forceinline__ void simulate_one(const SimParams& P, int ti, const S
     bool gate_idle = false;
     int gate_w = 0;
     double gate_pred = 0.0;
+#ifdef SABER_STREAK_STATS
+    const long long sched_t0 = clock64();
+#endif
     if (saber) {
       const int hc = high.count();
       refresh_entries += hc;
       // refresh_tiers (scheduler.cpp:38-55): scan in queue (= id) order only
       // when some entry may have crossed its demotion bound.
       if (hc > 0 && t >= min_td) {
+#ifdef SABER_STREAK_STATS
+        const long long scan_t0 = clock64();
+        st_scans += 1;
+#endif
         double nm = kInf;
+        int nkd = 0x7FFFFFFF;
         for (int i = 0; i < NW; ++i) {
           uint64_t b = high.word(i);
           while (b) {
@@ -385,10 +420,17 @@ __device__ __forceinline__ void simulate_one(const SimParams& P, int ti, const S
                 if (kRecords && DEMO && leader) DEMO[id] = 1;
               }
             }
-            if (!demote) nm = dmin(nm, T);
+            if (!demote) {
+              nm = dmin(nm, T);
+              if (use_tab) nkd = min(nkd, KD[id]);
+            }
           }
         }
         min_td = nm;
+        min_kd = nkd;
+#ifdef SABER_STREAK_STATS
+        st_cyc[4] += clock64() - scan_t0;
+#endif
       }
       if (high.any()) {
         // admission_step, high tier (scheduler.cpp:58-95).
@@ -526,6 +568,9 @@ __device__ __forceinline__ void simulate_one(const SimParams& P, int ti, const S
       }
     }
 
+#ifdef SABER_STREAK_STATS
+    st_cyc[2] += clock64() - sched_t0;
+#endif
     if (t >= horizon) break;
 
     // Quiet streak: from this tick on, consecutive ticks
@@ -561,30 +606,39 @@ __device__ __forceinline__ void simulate_one(const SimParams& P, int ti, const S
       if (Kb < 2) sblock = true;
       int K = 0;
       if (Kb >= 2) {
-        if (ka < 0) ka = tick_index(P.ticks, na_t);
         K = min(Kb, min(ka - k0, kh - 1 - k0));
         if (gate_streak) {
           // no refresh scan (t < min_td) and enough scheduler draws
-          K = min(K, tick_index(P.ticks, min_td) - k0);
+          K = min(K, min_kd - k0);
           if (gate_w > 1)
             K = static_cast<int>(min(static_cast<int64_t>(K),
                                      1 + (draw_len - draw_pos) / (gate_w - 1)));
         }
       }
       if (K >= 2) {
-        if (P.ticks.T[k0] != t || clock != t) {  // invariant: loud, never silent
+#ifdef SABER_DEBUG_CHECKS
+        if (P.ticks.T[k0] != t || clock != t) {  // invariant t_k == T[k] at a tick start
           if (leader) atomicCAS(P.out.error, kErrNone, kErrTickTable);
           use_tab = false;
-        } else {
+        } else
+#endif
+        {
+          const double t_after = P.ticks.T[k0 + K];  // issued early, used after the sweep
           const double* __restrict__ DTk = P.ticks.DT + k0;
           // min_pf stays exact: the same per-pass chain min_pf -= dt
-          min_pf = streak_slots<G>(S, sub, A, speed_A, DTk, K, min_pf);
+          {
+            SEC_BEGIN();
+            min_pf = streak_slots<G>(S, sub, A, speed_A, DTk, K, min_pf);
+            SEC_END(1);
+          }
           if (A > npre) rem_lb = rem_lb - static_cast<double>(K) * delta;
           rem_exact = false;
           if (gate_streak) {
             const int hc = high.count();
+            SEC_BEGIN();
             gate_streak_decisions<G, kTrace, NW>(P, S, sub, gmask, high, MO, DL, draws, draw_pos,
                                                  k0, K, gate_w, A, gate_pred, L, tr, INV);
+            SEC_END(0);
             const int64_t extra = K - 1;
             draw_pos += extra * (gate_w - 1);
             rng_draws += static_cast<int32_t>(extra * (gate_w - 1));
@@ -600,7 +654,7 @@ __device__ __forceinline__ void simulate_one(const SimParams& P, int ti, const S
           passes += K;
           prefill_updates += K * npre;
           decode_updates += K * (A - npre);
-          t = P.ticks.T[k0 + K];
+          t = t_after;
           clock = t;
           continue;
         }
@@ -609,6 +663,9 @@ __device__ __forceinline__ void simulate_one(const SimParams& P, int ti, const S
     const double nt = (horizon < t + tick) ? horizon : t + tick;
 
     // Engine::advance_to(nt) (engine.cpp:51-127).
+#ifdef SABER_STREAK_STATS
+    const long long eng_t0 = clock64();
+#endif
     while (clock < nt) {
       if (A == 0) {
         clock = nt;
@@ -793,6 +850,9 @@ __device__ __forceinline__ void simulate_one(const SimParams& P, int ti, const S
       }
       clock = nclock;
     }
+#ifdef SABER_STREAK_STATS
+    st_cyc[3] += clock64() - eng_t0;
+#endif
     t = nt;
     if (completed == n) break;
   }
@@ -823,6 +883,9 @@ __device__ __forceinline__ void simulate_one(const SimParams& P, int ti, const S
     R->horizon = st_count;
     R->ratio_mean = static_cast<double>(clock64() - st_t0);  // overwritten by row metrics
     R->n_kind[4] = clock64() - st_t0;
+    for (int q = 0; q < 4; ++q) R->n_kind[q] = st_cyc[q];
+    R->rng_draws = st_cyc[4];
+    R->gate_candidates = st_scans;
     R->decision_hash = (static_cast<uint64_t>(st_quiet) << 32) | static_cast<uint32_t>(st_exact);
 #endif
     if (kTrace && P.out.trace_count) P.out.trace_count[d.row] = L.n;
@@ -1017,6 +1080,16 @@ int launch_sim(const SimParams& p, const SimLaunch& l, void* stream) {
                           static_cast<cudaStream_t>(stream)) == cudaSuccess
              ? 0
              : 1;
+}
+
+int launch_tick_index(const WorkloadTables& wl, int64_t cells, const TickTable& tt, int32_t* ka,
+                      int32_t* kd, void* stream) {
+  if (cells == 0 || tt.len == 0) return 0;
+  const int block = 256;
+  const int64_t want = (cells + block - 1) / block;
+  const int grid = static_cast<int>(want < 4096 ? want : 4096);
+  tick_index_kernel<<<grid, block, 0, static_cast<cudaStream_t>(stream)>>>(wl, cells, tt, ka, kd);
+  return cudaGetLastError() == cudaSuccess ? 0 : 1;
 }
 
 int launch_row_metrics(const RowMetricsParams& p, void* stream) {

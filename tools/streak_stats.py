@@ -79,5 +79,34 @@ def durations():
             print(f"{mode:6s} {m} max kcyc by rps 1..20: {line}")
 
 
-if __name__ == "__main__" and len(sys.argv) > 1:
+if __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "dur":
     durations()
+
+
+def sections():
+    """Cycle split (stats build): n_kind[0] gate-streak decisions, [1] streak
+    slot sweeps, [2] scheduler step of normal ticks, [3] normal engine passes,
+    [4] whole trajectory."""
+    grid = S.SweepGrid(bench.MIXES, bench.RPS, bench.CAPS, True)
+    base = S.SimConfig()
+    base.workload.num_requests = bench.N_REQ
+    base.model = S.SpeedModel(S.ModelFamily.Usl, bench.CAL_USL)
+    base.repeats = bench.SEEDS_PER_GPU
+    base.seed = bench.BASE_SEED
+    p = S.SweepPlan(grid, base)
+    p.run()
+    p.run()
+    rows, _, _, _ = p.fetch(summary=False)
+    keys = S.sweep_row_keys(grid, base)
+    saber = np.array([k[2] == S.SchedulerMode.Saber for k in keys])
+    nk = rows["n_kind"].astype(np.float64)
+    for name, m in [("static", ~saber), ("saber", saber)]:
+        tot = nk[m, 4].sum()
+        parts = [nk[m, q].sum() / tot for q in range(4)]
+        print(f"{name}: kcyc/traj {tot / m.sum() / 1e3:.0f}  gate-streak {parts[0]:.3f}  slot-streak {parts[1]:.3f}"
+              f"  sched-step {parts[2]:.3f} (refresh scans {rows['rng_draws'][m].sum() / tot:.3f},"
+              f" {rows['gate_candidates'][m].mean():.0f}/traj)  engine {parts[3]:.3f}  rest {1 - sum(parts):.3f}")
+
+
+if __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "sec":
+    sections()
