@@ -74,6 +74,7 @@ template <int G>
 struct Slots {
   double* g;     // fluid progress (>= 0) or -prefill_left (< 0); kDoneMark when done
   uint64_t* m;   // bits(max_output_tokens) | request id (low 16 bits are free)
+  uint32_t* dbuf;  // this group's staging buffer for scheduler draws, G * (kMaxWindow - 1)
   int col0;      // grp * G
   static_assert((G & (G - 1)) == 0, "G must be a power of two");
   __device__ __forceinline__ int idx(int k) const {
@@ -201,22 +202,27 @@ __device__ __forceinline__ void gate_streak_decisions(
     const bool live = j < K;
     const double tj = live ? P.ticks.T[k0 + j] : 0.0;
     const uint64_t tb = dbits(tj);
-    const uint32_t* __restrict__ dq = draws + draw_pos + static_cast<int64_t>(j - 1) * (w - 1);
-    uint32_t xq[kMaxWindow - 1];
-#pragma unroll
-    for (int q = 0; q < kMaxWindow - 1; ++q) xq[q] = (live && q < w - 1) ? dq[q] : 0u;
+    // This round's draws (ticks jb .. jb+G-1, w-1 each, consecutive in the
+    // stream) are staged through shared memory with coalesced loads, then
+    // every lane runs its tick's Fisher-Yates from there (a rolled loop keeps
+    // the kernel's instruction footprint small).
+    const int nd = min(G, K - jb) * (w - 1);
+    const uint32_t* __restrict__ src = draws + draw_pos + static_cast<int64_t>(jb - 1) * (w - 1);
+    for (int q = sub; q < nd; q += G) S.dbuf[q] = src[q];
+    __syncwarp(gmask);
+    const uint32_t* my = S.dbuf + sub * (w - 1);
     uint64_t ord = 0xFEDCBA9876543210ull;
-#pragma unroll
-    for (int q = 0; q < kMaxWindow - 1; ++q) {
-      if (q < w - 1) {
-        const uint32_t i = static_cast<uint32_t>(w - 1 - q);
-        const uint32_t jj = xq[q] - __umulhi(xq[q], INV[i + 1]) * (i + 1);
-        const uint64_t a = (ord >> (4 * i)) & 15ull;
-        const uint64_t bb = (ord >> (4 * jj)) & 15ull;
-        const uint64_t x2 = a ^ bb;
-        ord ^= (x2 << (4 * i)) | (x2 << (4 * jj));
-      }
+#pragma unroll 1
+    for (int q = 0; q < w - 1; ++q) {
+      const uint32_t x = live ? my[q] : 0u;
+      const uint32_t i = static_cast<uint32_t>(w - 1 - q);
+      const uint32_t jj = x - __umulhi(x, INV[i + 1]) * (i + 1);
+      const uint64_t a = (ord >> (4 * i)) & 15ull;
+      const uint64_t bb = (ord >> (4 * jj)) & 15ull;
+      const uint64_t x2 = a ^ bb;
+      ord ^= (x2 << (4 * i)) | (x2 << (4 * jj));
     }
+    __syncwarp(gmask);  // the buffer is refilled next round
     for (int c = 0; c < w; ++c) {
       const int p = static_cast<int>((ord >> (4 * c)) & 15ull);
       const int id = __shfl_sync(gmask, wid, S.col0 + p);
@@ -444,9 +450,6 @@ __device__ __forceinline__ void simulate_one(const SimParams& P, int ti, const S
         // Draws are stored mod lcm(1..16); x % d is exact via the reciprocal
         // table (x < 2^20).  All w-1 draws are independent
         // loads, issued before anything consumes them.
-        uint32_t xq[kMaxWindow - 1];
-#pragma unroll
-        for (int q = 0; q < kMaxWindow - 1; ++q) xq[q] = q < w - 1 ? draws[draw_pos + q] : 0u;
         const double pred = MT[load + 1];
         const bool violates = pred < ledger_max;  // ActiveLedger::violates
         unsigned okmask = 0;
@@ -457,18 +460,22 @@ __device__ __forceinline__ void simulate_one(const SimParams& P, int ti, const S
         int cid[kQ];
         double cneed[kQ];
         if constexpr (G >= kMaxWindow) {
-          // Lane c owns shuffled position c.  The element FY leaves at c is
-          // tau_{w-1}(...tau_1(c)) with tau_i = (i j_i): walked forward over
+          // Lane q holds draw q, which serves swap i = w-1-q.  Lane c owns
+          // shuffled position c: the element FY leaves at c is
+          // tau_{w-1}(...tau_1(c)) with tau_i = (i j_i), walked over
           // i = 1..w-1 with compares and selects, all lanes at once.
+          int jl = 0;
+          if (sub < w - 1) {
+            const uint32_t x = draws[draw_pos + sub];
+            const uint32_t d1 = static_cast<uint32_t>(w - sub);  // i + 1
+            jl = static_cast<int>(x - __umulhi(x, INV[d1]) * d1);
+          }
           int pos = sub;
-#pragma unroll
-          for (int q = kMaxWindow - 2; q >= 0; --q) {
-            if (q < w - 1) {
-              const int i = w - 1 - q;  // draw q serves swap i
-              const uint32_t d1 = static_cast<uint32_t>(i + 1);
-              const int j = static_cast<int>(xq[q] - __umulhi(xq[q], INV[d1]) * d1);
-              pos = pos == i ? j : (pos == j ? i : pos);
-            }
+#pragma unroll 1
+          for (int q = w - 2; q >= 0; --q) {
+            const int i = w - 1 - q;
+            const int j = __shfl_sync(gmask, jl, S.col0 + q);
+            pos = pos == i ? j : (pos == j ? i : pos);
           }
           cid[0] = 0;
           cneed[0] = 0.0;
@@ -478,6 +485,9 @@ __device__ __forceinline__ void simulate_one(const SimParams& P, int ti, const S
             if (!(pred < cneed[0]) && !violates) okmask = 1u << sub;
           }
         } else {
+          uint32_t xq[kMaxWindow - 1];
+#pragma unroll
+          for (int q = 0; q < kMaxWindow - 1; ++q) xq[q] = q < w - 1 ? draws[draw_pos + q] : 0u;
           uint64_t ord = 0xFEDCBA9876543210ull;  // window positions as nibbles
 #pragma unroll
           for (int q = 0; q < kMaxWindow - 1; ++q) {
@@ -912,6 +922,8 @@ __global__ void __launch_bounds__(kSimBlock, kSel == kSelStatic  ? SABER_STATIC_
   Slots<G> S;
   S.g = reinterpret_cast<double*>(tile);
   S.m = tile + static_cast<size_t>(rows) * kWarp;
+  S.dbuf = reinterpret_cast<uint32_t*>(smem + static_cast<size_t>(kSimBlock / kWarp) * rows * kWarp * 2) +
+           static_cast<size_t>(warp) * kWarp * (kMaxWindow - 1) + grp * G * (kMaxWindow - 1);
   S.col0 = grp * G;
   const int64_t group_id =
       (static_cast<int64_t>(blockIdx.x) * (kSimBlock / kWarp) + warp) * (kWarp / G) + grp;
@@ -1038,6 +1050,8 @@ int plan_sim(int nmax, int group, SimLaunch* out) {
     if (l.smem <= kTileBudget || group >= 32) break;
     group *= 2;
   }
+  // + per-warp staging for scheduler draws (gate streaks)
+  l.smem += static_cast<size_t>(kSimBlock / kWarp) * kWarp * (kMaxWindow - 1) * 4;
   void* k = pick_kernel(l.nwords, group, false, false);
   if (!k) return 1;
   int dev = 0, sms = 0, per_sm = 0;
