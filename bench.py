@@ -163,6 +163,16 @@ def algorithmic_fp64_ops(rows):
                         r["ledger_scanned"]))
 
 
+def issue_roofline(prof):
+    """The issue-slot roofline of K1 from the committed ncu capture
+    (sm__inst_issued % of peak, time-weighted over the two kernels)."""
+    if not prof or "issue_active_pct_weighted" not in prof:
+        return None
+    return {"frac": prof["issue_active_pct_weighted"] / 100.0,
+            "per_kernel": {k: v.get("issue_active_pct") for k, v in prof.get("kernels", {}).items()},
+            "source": "ncu sm__inst_issued.avg.pct_of_peak_sustained_active, profiles/sim_kernel_traffic.json"}
+
+
 def load_profile_traffic():
     p = os.path.join(ROOT, "profiles", "sim_kernel_traffic.json")
     try:
@@ -295,12 +305,14 @@ def engine_arm(args):
             "gpu_launches": launches_per_step * args.steps,
             "roofline": {"bound": "fp64", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                          "frac": achieved / peak if peak else None, "traffic": traffic,
-                         "kernel": "sim_kernel (K1)", "kernel_ms": sim_avg_ms,
+                         "kernel": "sim_kernel<SABER> + sim_kernel<static> (K1, concurrent)",
+                         "kernel_ms": sim_avg_ms,
                          "share_of_step": sim_avg_ms / (total_ms / args.steps),
                          "algorithmic_fp64_ops_per_launch": fp64_ops,
                          "peak_source": "measured live: DFMA microbenchmark (saber_cuda_fp64_peak)",
                          "note": "K1 is issue/latency-bound (DESIGN.md §4); FP64 pipe is the "
-                                 "algorithmic roofline SURVEY §8(d) names"},
+                                 "algorithmic roofline SURVEY §8(d) names",
+                         "issue": issue_roofline(prof)},
             "clocks": clk,
             "summary": {m: {"delta": summ[i].delta, "saber_mean_goodput": summ[i].saber_mean_goodput,
                             "best_static_mean_goodput": summ[i].best_static_mean_goodput}
