@@ -470,6 +470,11 @@ struct saber_sweep_plan {
 
 namespace {
 
+// Every row of the sweep has the same scheduler mode.
+bool desc_all_one_mode(const saber_sweep_desc& d) {
+  return (d.with_saber && d.n_caps == 0) || (!d.with_saber && d.n_caps > 0);
+}
+
 saber_status validate_sweep(const saber_sweep_desc& d) {
   if (d.n_mixes < 1 || d.n_rps < 1 || (d.n_caps < 1 && !d.with_saber))
     return fail(SABER_EINVAL, "sweep: empty grid");
@@ -816,6 +821,9 @@ saber_status saber_cuda_sweep_plan_run(saber_sweep_plan* P, void* stream) {
     CUDA_TRY(cudaStreamWaitEvent(s, P->join, 0));
     P->launches += 2;
   } else {
+    // one class only: its specialised kernel (falls back to the generic one
+    // off the G = 32 path inside launch_sim)
+    if (desc_all_one_mode(d)) sp.mode_sel = d.with_saber ? 2 : 1;
     LAUNCH_TRY(launch_sim(sp, P->scratch.launch, s));
     ++P->launches;
   }
@@ -1263,6 +1271,11 @@ extern "C" saber_status saber_cuda_run_batch(const saber_run_batch_desc* desc,
   sp.out.error = err_d.as<int32_t>();
   sp.next_traj = cursor_d.as<int32_t>();
   sp.ticks = ticktab.view;
+  {
+    bool any_saber = false, any_static = false;
+    for (const TrajDesc& dd : descs) (dd.mode == SABER_MODE_SABER ? any_saber : any_static) = true;
+    if (any_saber != any_static) sp.mode_sel = any_saber ? 2 : 1;
+  }
   LAUNCH_TRY(launch_sim(sp, scratch.launch, st));
   ++launches;
   RowMetricsParams rm{};
@@ -1650,13 +1663,54 @@ extern "C" saber_status saber_cuda_mc_sweep(const saber_mc_desc* desc, saber_mc_
   }
   std::vector<saber_traj_row> host_rows;
   if (out->rows) host_rows.resize(static_cast<size_t>(chunk));
+  // split launches (SABER-only + static-only kernels) need both classes
+  const bool split_ok = d.with_saber && d.n_caps > 0 && scratch.launch.group == 32 &&
+                        !scratch.launch.lane && std::getenv("SABER_NO_SPLIT") == nullptr;
+  std::vector<int32_t> ord_h;
+  DevBuf order_d;
+  cudaStream_t side = nullptr;
+  cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
+  struct StreamGuard {
+    cudaStream_t* s;
+    cudaEvent_t* a;
+    cudaEvent_t* b;
+    ~StreamGuard() {
+      if (*s) cudaStreamDestroy(*s);
+      if (*a) cudaEventDestroy(*a);
+      if (*b) cudaEventDestroy(*b);
+    }
+  } sguard{&side, &fork_ev, &join_ev};
+  if (split_ok) {
+    ord_h.resize(static_cast<size_t>(chunk));
+    ALLOC_TRY(order_d, dev, static_cast<size_t>(chunk) * 4);
+    CUDA_TRY(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
+    CUDA_TRY(cudaEventCreateWithFlags(&fork_ev, cudaEventDisableTiming));
+    CUDA_TRY(cudaEventCreateWithFlags(&join_ev, cudaEventDisableTiming));
+  }
   for (int64_t k0 = 0; k0 < mine; k0 += chunk) {
     mp.k0 = k0;
     mp.count = std::min<int64_t>(chunk, mine - k0);
     LAUNCH_TRY(launch_mc_workloads(mp, st));
     if (wl.ka.p)
       LAUNCH_TRY(launch_tick_index(wl.view(n), mp.count * n, ticktab.view, wl.ka.as<int32_t>(),
-                                   wl.kd.as<int32_t>(), st));    CUDA_TRY(cudaMemsetAsync(rows.p, 0, static_cast<size_t>(mp.count) * sizeof(saber_traj_row), st));
+                                   wl.kd.as<int32_t>(), st));
+    // SABER trajectories of the chunk first (their cell is k % cells, the
+    // variant (k % cells) % (caps + 1), as mc.cu cell_of), run on the
+    // SABER-only kernel while the static ones run on theirs.
+    int32_t ns = 0;
+    if (split_ok) {
+      const int per_rps = d.n_caps + 1;
+      int32_t lo = 0, hi = static_cast<int32_t>(mp.count);
+      for (int64_t i = 0; i < mp.count; ++i) {
+        const int64_t k = d.shard_index + (k0 + i) * d.shard_count;
+        const bool sab = (k % cells) % per_rps == d.n_caps;
+        if (sab) ord_h[static_cast<size_t>(lo++)] = static_cast<int32_t>(i);
+        else ord_h[static_cast<size_t>(--hi)] = static_cast<int32_t>(i);
+      }
+      ns = lo;
+      CUDA_TRY(cudaMemcpyAsync(order_d.p, ord_h.data(), static_cast<size_t>(mp.count) * 4,
+                               cudaMemcpyHostToDevice, st));
+    }    CUDA_TRY(cudaMemsetAsync(rows.p, 0, static_cast<size_t>(mp.count) * sizeof(saber_traj_row), st));
     CUDA_TRY(cudaMemsetAsync(cursor.p, 0, 16, st));
     LAUNCH_TRY(launch_fill_rows(comp.as<double>(), mp.count, n, 0, 1, st));
     SimParams sp{};
@@ -1675,7 +1729,24 @@ extern "C" saber_status saber_cuda_mc_sweep(const saber_mc_desc* desc, saber_mc_
     sp.next_traj = cursor.as<int32_t>();
     sp.ticks = ticktab.view;
     CUDA_TRY(cudaEventRecord(simt.a, st));
-    LAUNCH_TRY(launch_sim(sp, scratch.launch, st));
+    if (split_ok && ns > 0 && ns < mp.count) {
+      SimParams sa = sp, sb = sp;
+      sa.order = sb.order = order_d.as<int32_t>();
+      sa.mode_sel = 2;
+      sa.n_traj = ns;
+      sb.mode_sel = 1;
+      sb.first_traj = ns;
+      sb.next_traj = cursor.as<int32_t>() + 1;
+      CUDA_TRY(cudaEventRecord(fork_ev, st));
+      CUDA_TRY(cudaStreamWaitEvent(side, fork_ev, 0));
+      LAUNCH_TRY(launch_sim(sa, scratch.launch, st));
+      LAUNCH_TRY(launch_sim(sb, scratch.launch, side));
+      CUDA_TRY(cudaEventRecord(join_ev, side));
+      CUDA_TRY(cudaStreamWaitEvent(st, join_ev, 0));
+      launches += 1;
+    } else {
+      LAUNCH_TRY(launch_sim(sp, scratch.launch, st));
+    }
     CUDA_TRY(cudaEventRecord(simt.b, st));
     RowMetricsParams rm{};
     rm.rows = rows.as<saber_traj_row>();
