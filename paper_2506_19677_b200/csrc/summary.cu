@@ -16,6 +16,7 @@
 
 #include <climits>
 #include <cmath>
+#include <cstdlib>
 
 #include "saber_internal.h"
 
@@ -371,6 +372,101 @@ __global__ void __launch_bounds__(64) summary_mix_kernel(const SummaryParams p) 
   }
 }
 
+// The same pooled sums on ONE warp, no shared memory and no barrier: every
+// lane loads a strided slice of the next 128 pooled values into registers
+// (two batches in flight), and the dependent add chain takes them in
+// sequence through shuffles — 2 SHFL + 1 DADD per value, which the scheduler
+// issues in the shadow of the 8-cycle DADD chain.  Never-completed requests
+// contribute an exact +0 (0 to the sum, a zero term to the deviations), and
+// are counted with a ballot.  Every lane carries the same chain value.
+constexpr int kStream = 4;  // values per lane per batch (a batch = 128 values)
+
+__device__ __forceinline__ double pooled_chain(const SummaryParams& p, int mi, int variant,
+                                               int pass, double mean, int64_t* cnt) {
+  const int lane = threadIdx.x & 31;
+  double acc = 0.0;
+  int64_t c = 0;
+  SegmentWalk walk;
+  const double* sp = nullptr;
+  int64_t slen = 0;
+  const double pad = nan("");  // beyond a segment: skipped like a never-completed request
+  while (walk.next(p, mi, variant, &sp, &slen)) {
+    double cur[kStream], nxt[kStream];
+#pragma unroll
+    for (int u = 0; u < kStream; ++u) {
+      const int64_t i = static_cast<int64_t>(u) * 32 + lane;
+      cur[u] = i < slen ? sp[i] : pad;
+    }
+    for (int64_t base = 0; base < slen; base += 32 * kStream) {
+      const int64_t nb = base + 32 * kStream;
+#pragma unroll
+      for (int u = 0; u < kStream; ++u) {  // next batch, issued before this one's chain
+        const int64_t i = nb + static_cast<int64_t>(u) * 32 + lane;
+        nxt[u] = i < slen ? sp[i] : pad;
+      }
+#pragma unroll
+      for (int u = 0; u < kStream; ++u) {
+        const double v = cur[u];
+        const bool ok = !isnan(v);
+        double term;
+        if (pass == 0) {
+          term = ok ? v : 0.0;
+          c += __popc(__ballot_sync(kFull, ok));
+        } else {
+          const double e = v - mean;
+          term = ok ? e * e : 0.0;
+        }
+        // all 32 shuffles first (their ~30-cycle latency overlaps), then the
+        // chain of 32 dependent adds
+        double w[32];
+#pragma unroll
+        for (int k = 0; k < 32; ++k) w[k] = __shfl_sync(kFull, term, k);
+#pragma unroll
+        for (int k = 0; k < 32; ++k) acc += w[k];
+      }
+#pragma unroll
+      for (int u = 0; u < kStream; ++u) cur[u] = nxt[u];
+    }
+  }
+  if (cnt) *cnt = c;
+  return acc;
+}
+
+__global__ void __launch_bounds__(32) summary_mix_warp_kernel(const SummaryParams p) {
+  const int mi = blockIdx.x >> 1;
+  const int variant = blockIdx.x & 1;  // 0 = saber, 1 = best static
+  const double* sc = p.scratch + static_cast<int64_t>(mi) * p.n_rps * kCellScratch;
+  const bool present = variant == 0 ? p.with_saber != 0 : p.n_caps > 0;
+  const double nanv = nan("");
+  double mean_goodput = nanv, pooled = nanv, rps_cv = nanv;
+  if (present) {
+    int64_t cnt = 0;
+    const double sum = pooled_chain(p, mi, variant, 0, 0.0, &cnt);
+    if (cnt > 0) {
+      const double mean = sum / static_cast<double>(cnt);
+      if (mean != 0.0) {
+        const double acc = pooled_chain(p, mi, variant, 1, mean, nullptr);
+        pooled = sqrt(acc / static_cast<double>(cnt)) / mean;
+      }
+    }
+    double s = 0.0;
+    for (int ri = 0; ri < p.n_rps; ++ri) s += sc[ri * kCellScratch + (variant == 0 ? 0 : 1)];
+    mean_goodput = s / static_cast<double>(p.n_rps);
+    rps_cv = cv_cells(sc, p.n_rps, variant == 0 ? 2 : 3, variant == 0 ? 4 : 5);
+  }
+  if (threadIdx.x != 0) return;
+  saber_mix_summary* out = p.summary + mi;
+  if (variant == 0) {
+    out->saber_mean_goodput = mean_goodput;
+    out->saber_pooled_cv = pooled;
+    out->saber_rps_mean_cv = rps_cv;
+  } else {
+    out->best_static_mean_goodput = mean_goodput;
+    out->best_static_pooled_cv = pooled;
+    out->best_static_rps_mean_cv = rps_cv;
+  }
+}
+
 // delta = saber - best static (simloop.cpp:262), after both variants wrote.
 __global__ void summary_delta_kernel(const SummaryParams p) {
   const int mi = blockIdx.x * blockDim.x + threadIdx.x;
@@ -387,7 +483,10 @@ int launch_summary(const SummaryParams& p, void* stream) {
   if (cells == 0) return 0;
   ratios_kernel<<<1184, 256, 0, s>>>(p);
   summary_cells_kernel<<<(cells * 32 + 127) / 128, 128, 0, s>>>(p);
-  summary_mix_kernel<<<2 * p.n_mixes, 64, 0, s>>>(p);
+  if (std::getenv("SABER_SUMMARY_RING"))
+    summary_mix_kernel<<<2 * p.n_mixes, 64, 0, s>>>(p);
+  else
+    summary_mix_warp_kernel<<<2 * p.n_mixes, 32, 0, s>>>(p);
   summary_delta_kernel<<<1, 32, 0, s>>>(p);
   return cudaGetLastError() == cudaSuccess ? 0 : 1;
 }
