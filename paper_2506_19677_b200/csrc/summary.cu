@@ -372,17 +372,20 @@ __global__ void __launch_bounds__(64) summary_mix_kernel(const SummaryParams p) 
   }
 }
 
-// The same pooled sums on ONE warp, no shared memory and no barrier: every
-// lane loads a strided slice of the next 128 pooled values into registers
-// (two batches in flight), and the dependent add chain takes them in
-// sequence through shuffles — 2 SHFL + 1 DADD per value, which the scheduler
-// issues in the shadow of the 8-cycle DADD chain.  Never-completed requests
-// contribute an exact +0 (0 to the sum, a zero term to the deviations), and
-// are counted with a ballot.  Every lane carries the same chain value.
-constexpr int kStream = 4;  // values per lane per batch (a batch = 128 values)
+// The same pooled sums on ONE warp, no block barrier: every lane loads a
+// strided slice of the next 256 pooled values into registers (two batches in
+// flight), writes this batch's terms to a warp-private shared buffer, and the
+// dependent add chain reads them back in pool order with broadcast 16-byte
+// loads (half an LDS per value, in the shadow of the 8-cycle DADD chain;
+// shuffles cost 11 cycles per value, profiles/latency_probe_b200.txt).
+// Never-completed requests contribute an exact +0 (0 to the sum, a zero term
+// to the deviations) and are counted with a ballot.  Every lane carries the
+// same chain value.
+constexpr int kStream = 8;  // values per lane per batch (a batch = 256 values)
 
 __device__ __forceinline__ double pooled_chain(const SummaryParams& p, int mi, int variant,
-                                               int pass, double mean, int64_t* cnt) {
+                                               int pass, double mean, int64_t* cnt,
+                                               double* buf /* [2][32 * kStream] shared */) {
   const int lane = threadIdx.x & 31;
   double acc = 0.0;
   int64_t c = 0;
@@ -390,6 +393,7 @@ __device__ __forceinline__ double pooled_chain(const SummaryParams& p, int mi, i
   const double* sp = nullptr;
   int64_t slen = 0;
   const double pad = nan("");  // beyond a segment: skipped like a never-completed request
+  int parity = 0;
   while (walk.next(p, mi, variant, &sp, &slen)) {
     double cur[kStream], nxt[kStream];
 #pragma unroll
@@ -404,6 +408,8 @@ __device__ __forceinline__ double pooled_chain(const SummaryParams& p, int mi, i
         const int64_t i = nb + static_cast<int64_t>(u) * 32 + lane;
         nxt[u] = i < slen ? sp[i] : pad;
       }
+      // this batch's terms, in pool order, into the shared buffer
+      double* bb = buf + parity * (32 * kStream);
 #pragma unroll
       for (int u = 0; u < kStream; ++u) {
         const double v = cur[u];
@@ -416,14 +422,18 @@ __device__ __forceinline__ double pooled_chain(const SummaryParams& p, int mi, i
           const double e = v - mean;
           term = ok ? e * e : 0.0;
         }
-        // all 32 shuffles first (their ~30-cycle latency overlaps), then the
-        // chain of 32 dependent adds
-        double w[32];
-#pragma unroll
-        for (int k = 0; k < 32; ++k) w[k] = __shfl_sync(kFull, term, k);
-#pragma unroll
-        for (int k = 0; k < 32; ++k) acc += w[k];
+        bb[u * 32 + lane] = term;
       }
+      __syncwarp();
+      // the chain: every lane reads the same words (broadcast), two per load
+      const double2* b2 = reinterpret_cast<const double2*>(bb);
+#pragma unroll 8
+      for (int k = 0; k < 16 * kStream; ++k) {
+        const double2 x = b2[k];
+        acc += x.x;
+        acc += x.y;
+      }
+      parity ^= 1;  // the other half is written next; this one is read by then
 #pragma unroll
       for (int u = 0; u < kStream; ++u) cur[u] = nxt[u];
     }
@@ -433,6 +443,7 @@ __device__ __forceinline__ double pooled_chain(const SummaryParams& p, int mi, i
 }
 
 __global__ void __launch_bounds__(32) summary_mix_warp_kernel(const SummaryParams p) {
+  __shared__ __align__(16) double buf[2 * 32 * kStream];
   const int mi = blockIdx.x >> 1;
   const int variant = blockIdx.x & 1;  // 0 = saber, 1 = best static
   const double* sc = p.scratch + static_cast<int64_t>(mi) * p.n_rps * kCellScratch;
@@ -441,11 +452,12 @@ __global__ void __launch_bounds__(32) summary_mix_warp_kernel(const SummaryParam
   double mean_goodput = nanv, pooled = nanv, rps_cv = nanv;
   if (present) {
     int64_t cnt = 0;
-    const double sum = pooled_chain(p, mi, variant, 0, 0.0, &cnt);
+    const double sum = pooled_chain(p, mi, variant, 0, 0.0, &cnt, buf);
     if (cnt > 0) {
       const double mean = sum / static_cast<double>(cnt);
       if (mean != 0.0) {
-        const double acc = pooled_chain(p, mi, variant, 1, mean, nullptr);
+        __syncwarp();
+        const double acc = pooled_chain(p, mi, variant, 1, mean, nullptr, buf);
         pooled = sqrt(acc / static_cast<double>(cnt)) / mean;
       }
     }

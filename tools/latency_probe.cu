@@ -27,6 +27,24 @@ __global__ void chain(double* out, long long* cyc, double a, double b, int n) {
   out[threadIdx.x] = x + f + u;
 }
 
+// The summary's pooled chain (summary.cu pooled_chain): 32 values per step,
+// broadcast by shuffles, added in sequence.  Reports cycles per added value.
+__global__ void pooled(const double* v, double* out, long long* cyc, int n) {
+  double acc = 0.0;
+  long long t0 = clock64();
+  for (int b = 0; b < n; ++b) {
+    const double term = v[(b * 32 + threadIdx.x) & 4095];
+    double w[32];
+#pragma unroll
+    for (int k = 0; k < 32; ++k) w[k] = __shfl_sync(0xffffffffu, term, k);
+#pragma unroll
+    for (int k = 0; k < 32; ++k) acc += w[k];
+  }
+  long long t1 = clock64();
+  if (threadIdx.x == 0) cyc[0] = t1 - t0;
+  out[threadIdx.x] = acc;
+}
+
 int main() {
   double* out; long long* cyc;
   cudaMalloc(&out, 1024 * 8); cudaMalloc(&cyc, 8);
@@ -48,6 +66,17 @@ int main() {
     }
     long long c; cudaMemcpy(&c, cyc, 8, cudaMemcpyDeviceToHost);
     printf("%-16s %.2f cycles/op (1 warp, dependent chain)\n", names[op], (double)c / (n * 16));
+  }
+  {
+    double* v;
+    cudaMalloc(&v, 4096 * 8);
+    cudaMemset(v, 0, 4096 * 8);
+    for (int rep = 0; rep < 2; ++rep) {
+      pooled<<<1, 32>>>(v, out, cyc, n);
+      cudaDeviceSynchronize();
+    }
+    long long c; cudaMemcpy(&c, cyc, 8, cudaMemcpyDeviceToHost);
+    printf("%-16s %.2f cycles/value (summary pooled chain)\n", "SHFLx32+DADDx32", (double)c / (n * 32));
   }
   return 0;
 }
