@@ -206,54 +206,88 @@ def engine_arm(args):
     base.model = S.SpeedModel(S.ModelFamily.Usl, CAL_USL)
     base.repeats = SEEDS_PER_GPU * world
     base.seed = BASE_SEED
-    plan = S.SweepPlan(grid, base, device=device, shard_index=rank, shard_count=world)
-    bufs = plan.buffers()
-    rows_t = comp_t = None
-    if world > 1:
-        # zero-copy int64 views of the plan's row/completion buffers for NCCL
-        rows_t = torch.as_tensor(_CudaView(bufs.rows, bufs.rows_bytes), device=f"cuda:{device}")
-        comp_t = torch.as_tensor(_CudaView(bufs.completion_times, bufs.completion_bytes),
-                                 device=f"cuda:{device}")
+    # Two plans, so consecutive sweeps pipeline: the summary of sweep k (its
+    # sequential pooled sums, on a side stream) overlaps the simulation of
+    # sweep k+1.  --no-pipeline runs them back to back.
+    n_plans = 1 if args.no_pipeline else 2
+    plans = [S.SweepPlan(grid, base, device=device, shard_index=rank, shard_count=world)
+             for _ in range(n_plans)]
+    views = []
+    for pl in plans:
+        bufs = pl.buffers()
+        if world > 1:
+            # zero-copy int64 views of the plan's row/completion buffers for NCCL
+            views.append((torch.as_tensor(_CudaView(bufs.rows, bufs.rows_bytes), device=f"cuda:{device}"),
+                          torch.as_tensor(_CudaView(bufs.completion_times, bufs.completion_bytes),
+                                          device=f"cuda:{device}")))
+        else:
+            views.append(None)
+    side = torch.cuda.Stream(device=device, priority=-1)  # high priority: summary blocks go first
+    summary_done = [None] * n_plans
 
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.int32, device=device)
 
-    def step():
-        plan.run(stream.cuda_stream)
+    def gather(i):
         if world > 1:
             # NCCL final statistics reduce: shards are disjoint (other ranks'
             # rows are 0), so an integer sum of the raw bits is an exact gather
-            dist.all_reduce(rows_t)
-            dist.all_reduce(comp_t)
-        plan.summarize(stream.cuda_stream)
+            dist.all_reduce(views[i][0])
+            dist.all_reduce(views[i][1])
 
-    for _ in range(args.warmup):
-        step()
+    def step(k, sync):
+        i = k % n_plans
+        pl = plans[i]
+        if sync:
+            pl.run(stream.cuda_stream)
+            gather(i)
+            pl.summarize(stream.cuda_stream)
+            return
+        if summary_done[i] is not None:
+            stream.wait_event(summary_done[i])  # plan i's buffers are free again
+        pl.launch(stream.cuda_stream)
+        sim_done = torch.cuda.Event()
+        sim_done.record(stream)
+        side.wait_event(sim_done)
+        with torch.cuda.stream(side):
+            gather(i)
+            pl.summarize_launch(side.cuda_stream)
+        e = torch.cuda.Event()
+        e.record(side)
+        summary_done[i] = e
+
+    for k in range(args.warmup):
+        step(k, sync=True)  # synchronous: every warm-up sweep is error-checked
     torch.cuda.synchronize()
 
     clocks = ClockSampler(device)
     clocks.start()
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-          for _ in range(args.steps)]
-    sim_ms = []
+    t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     if dist:
         dist.barrier()
     torch.cuda.synchronize()
+    t_start.record(stream)
     for k in range(args.steps):
-        flush.fill_(k)  # evict L2 (256 MB > 126 MB) between timed steps
-        ev[k][0].record(stream)
-        step()
-        ev[k][1].record(stream)
-        sim_ms.append(plan.stats()[1])
+        if not os.environ.get("BENCH_NO_FLUSH"):
+            flush.fill_(k)  # evict L2 (256 MB > 126 MB) between timed steps
+        step(k, sync=args.no_pipeline)
+    for e in summary_done:
+        if e is not None:
+            stream.wait_event(e)
+    t_end.record(stream)
     torch.cuda.synchronize()
+    for pl in plans:
+        pl.wait()  # error flags of the last sweeps, stats
     if dist:
         dist.barrier()
     clk = clocks.stop()
-    total_ms = sum(a.elapsed_time(b) for a, b in ev)
+    total_ms = t_start.elapsed_time(t_end)
     if dist:
         t = torch.tensor([total_ms], dtype=torch.float64, device=device)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         total_ms = float(t.item())
+    plan = plans[(args.steps - 1) % n_plans]
     launches_per_step = plan.stats()[2]
+    sim_ms = [pl.stats()[1] for pl in plans]
 
     rows, _, summ, best = plan.fetch(completion=False, summary=True)
     total_rows = plan.n_rows
@@ -297,7 +331,9 @@ def engine_arm(args):
                     f"seeds {BASE_SEED}..{BASE_SEED + base.repeats - 1})",
             "config": {"workload": WORKLOAD, "trajectories_per_step": total_rows,
                        "seeds": base.repeats, "l2": "flushed between steps (256 MB write)",
-                       "parallelism": f"rows strided over {world} GPU(s)"},
+                       "parallelism": f"rows strided over {world} GPU(s)",
+                       "pipelining": "none" if args.no_pipeline else
+                       "2 plans: summary of sweep k overlaps the simulation of sweep k+1"},
             "decisions_per_s": decisions * args.steps / (total_ms / 1e3),
             "decisions_per_step": decisions,
             "e2e": {"value": e2e_value, "unit": "traj/s", "h2d_bytes_per_step": h2d,
@@ -320,7 +356,8 @@ def engine_arm(args):
         }
         if cpu is not None:
             line["cpu_baseline"] = cpu
-    plan.close()
+    for pl in plans:
+        pl.close()
     if line is not None:
         print(json.dumps(line), flush=True)
     if dist:
@@ -412,6 +449,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="engine", choices=["engine", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-pipeline", action="store_true",
+                    help="run each sweep's summary after it instead of overlapping the next sweep")
     args = ap.parse_args()
     if args.impl == "reference":
         return reference_arm(args)

@@ -194,6 +194,13 @@ typedef struct {
 saber_status saber_cuda_sweep_plan_create(const saber_sweep_desc* desc, saber_sweep_plan** plan);
 saber_status saber_cuda_sweep_plan_run(saber_sweep_plan* plan, void* cuda_stream);
 saber_status saber_cuda_sweep_plan_summarize(saber_sweep_plan* plan, void* cuda_stream);
+/* Asynchronous halves of run / summarize: enqueue on the stream and return;
+ * saber_cuda_sweep_plan_wait synchronises, checks the kernels' error flag and
+ * updates the stats.  Lets a caller pipeline sweeps (the summary of one plan
+ * overlapping the simulation of another on a second stream). */
+saber_status saber_cuda_sweep_plan_launch(saber_sweep_plan* plan, void* cuda_stream);
+saber_status saber_cuda_sweep_plan_summarize_launch(saber_sweep_plan* plan, void* cuda_stream);
+saber_status saber_cuda_sweep_plan_wait(saber_sweep_plan* plan);
 saber_status saber_cuda_sweep_plan_buffers(saber_sweep_plan* plan, saber_sweep_buffers* out);
 saber_status saber_cuda_sweep_plan_fetch(saber_sweep_plan* plan, saber_sweep_out* out);
 /* CUDA-event time and launches of the last plan_run (+ summarize). */

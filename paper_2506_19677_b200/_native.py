@@ -183,6 +183,9 @@ SYMBOLS = [
     ("saber_cuda_sweep_plan_create", C.c_int, [_P(saber_sweep_desc), _P(C.c_void_p)]),
     ("saber_cuda_sweep_plan_run", C.c_int, [C.c_void_p, C.c_void_p]),
     ("saber_cuda_sweep_plan_summarize", C.c_int, [C.c_void_p, C.c_void_p]),
+    ("saber_cuda_sweep_plan_launch", C.c_int, [C.c_void_p, C.c_void_p]),
+    ("saber_cuda_sweep_plan_summarize_launch", C.c_int, [C.c_void_p, C.c_void_p]),
+    ("saber_cuda_sweep_plan_wait", C.c_int, [C.c_void_p]),
     ("saber_cuda_sweep_plan_buffers", C.c_int, [C.c_void_p, _P(saber_sweep_buffers)]),
     ("saber_cuda_sweep_plan_fetch", C.c_int, [C.c_void_p, _P(saber_sweep_out)]),
     ("saber_cuda_sweep_plan_stats", C.c_int, [C.c_void_p, _P(C.c_double), _P(C.c_double),

@@ -485,6 +485,18 @@ class SweepPlan:
     def summarize(self, stream: int = 0):
         _check(N.lib().saber_cuda_sweep_plan_summarize(self.handle, C.c_void_p(stream)))
 
+    def launch(self, stream: int = 0):
+        """Enqueue run() without waiting (pair with wait())."""
+        _check(N.lib().saber_cuda_sweep_plan_launch(self.handle, C.c_void_p(stream)))
+
+    def summarize_launch(self, stream: int = 0):
+        """Enqueue summarize() without waiting (pair with wait())."""
+        _check(N.lib().saber_cuda_sweep_plan_summarize_launch(self.handle, C.c_void_p(stream)))
+
+    def wait(self):
+        """Synchronise the enqueued work, check the kernels' error flag."""
+        _check(N.lib().saber_cuda_sweep_plan_wait(self.handle))
+
     def buffers(self) -> N.saber_sweep_buffers:
         b = N.saber_sweep_buffers()
         _check(N.lib().saber_cuda_sweep_plan_buffers(self.handle, C.byref(b)))

@@ -461,7 +461,8 @@ struct saber_sweep_plan {
     if (fork) cudaEventDestroy(fork);
     if (join) cudaEventDestroy(join);
   }
-  Timer all, sim;
+  Timer all, sim, summ;
+  bool run_pending = false, summary_pending = false;
   double last_ms = 0.0, sim_ms = 0.0;
   int launches = 0;
   bool summarized = false;
@@ -703,6 +704,7 @@ saber_status saber_cuda_sweep_plan_create(const saber_sweep_desc* desc, saber_sw
   tr.mark("tick table");
   if (saber_status s = P->all.init()) return s;
   if (saber_status s = P->sim.init()) return s;
+  if (saber_status s = P->summ.init()) return s;
   if (P->n_saber_first > 0 && P->n_saber_first < P->rows_shard) {
     CUDA_TRY(cudaStreamCreateWithFlags(&P->side, cudaStreamNonBlocking));
     CUDA_TRY(cudaEventCreateWithFlags(&P->fork, cudaEventDisableTiming));
@@ -713,13 +715,14 @@ saber_status saber_cuda_sweep_plan_create(const saber_sweep_desc* desc, saber_sw
   return SABER_OK;
 }
 
-saber_status saber_cuda_sweep_plan_run(saber_sweep_plan* P, void* stream) {
+saber_status saber_cuda_sweep_plan_launch(saber_sweep_plan* P, void* stream) {
   if (!P) return fail(SABER_EINVAL, "null plan");
   CUDA_TRY(cudaSetDevice(P->device));
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const saber_sweep_desc& d = P->desc;
   P->launches = 0;
   P->summarized = false;
+  P->summary_pending = false;
   CUDA_TRY(cudaEventRecord(P->all.a, s));
   CUDA_TRY(cudaMemsetAsync(P->rows.p, 0, P->rows.bytes, s));
   CUDA_TRY(cudaMemsetAsync(P->cursor.p, 0, 16, s));
@@ -838,21 +841,44 @@ saber_status saber_cuda_sweep_plan_run(saber_sweep_plan* P, void* stream) {
   LAUNCH_TRY(launch_row_metrics(rm, s));
   ++P->launches;
   CUDA_TRY(cudaEventRecord(P->all.b, s));
-  CUDA_TRY(cudaEventSynchronize(P->all.b));
-  float ms = 0.f, ms2 = 0.f;
-  CUDA_TRY(cudaEventElapsedTime(&ms, P->all.a, P->all.b));
-  CUDA_TRY(cudaEventElapsedTime(&ms2, P->sim.a, P->sim.b));
-  P->last_ms = ms;
-  P->sim_ms = ms2;
-  int32_t err = 0;
-  CUDA_TRY(cudaMemcpy(&err, P->err.p, 4, cudaMemcpyDeviceToHost));
-  if (err == kErrRngExhausted)
-    return fail(SABER_EINTERNAL, "scheduler RNG stream exhausted (draw bound violated)");
-  if (err != 0) return fail(SABER_EINTERNAL, "trajectory kernel error " + std::to_string(err));
+  P->run_pending = true;
   return SABER_OK;
 }
 
-saber_status saber_cuda_sweep_plan_summarize(saber_sweep_plan* P, void* stream) {
+saber_status saber_cuda_sweep_plan_wait(saber_sweep_plan* P) {
+  if (!P) return fail(SABER_EINVAL, "null plan");
+  CUDA_TRY(cudaSetDevice(P->device));
+  if (P->run_pending) {
+    CUDA_TRY(cudaEventSynchronize(P->all.b));
+    float ms = 0.f, ms2 = 0.f;
+    CUDA_TRY(cudaEventElapsedTime(&ms, P->all.a, P->all.b));
+    CUDA_TRY(cudaEventElapsedTime(&ms2, P->sim.a, P->sim.b));
+    P->last_ms = ms;
+    P->sim_ms = ms2;
+    P->run_pending = false;
+    int32_t err = 0;
+    CUDA_TRY(cudaMemcpy(&err, P->err.p, 4, cudaMemcpyDeviceToHost));
+    if (err == kErrRngExhausted)
+      return fail(SABER_EINTERNAL, "scheduler RNG stream exhausted (draw bound violated)");
+    if (err != 0) return fail(SABER_EINTERNAL, "trajectory kernel error " + std::to_string(err));
+  }
+  if (P->summary_pending) {
+    CUDA_TRY(cudaEventSynchronize(P->summ.b));
+    float ms = 0.f;
+    CUDA_TRY(cudaEventElapsedTime(&ms, P->summ.a, P->summ.b));
+    P->last_ms += ms;
+    P->summary_pending = false;
+    P->summarized = true;
+  }
+  return SABER_OK;
+}
+
+saber_status saber_cuda_sweep_plan_run(saber_sweep_plan* P, void* stream) {
+  if (saber_status s = saber_cuda_sweep_plan_launch(P, stream)) return s;
+  return saber_cuda_sweep_plan_wait(P);
+}
+
+static saber_status summarize_launch_impl(saber_sweep_plan* P, void* stream, bool narrow) {
   if (!P) return fail(SABER_EINVAL, "null plan");
   CUDA_TRY(cudaSetDevice(P->device));
   cudaStream_t s = static_cast<cudaStream_t>(stream);
@@ -872,16 +898,22 @@ saber_status saber_cuda_sweep_plan_summarize(saber_sweep_plan* P, void* stream) 
   sp.best_cap = P->best_cap.as<int32_t>();
   sp.scratch = P->cell_scratch.as<double>();
   sp.ratios = P->ratios.as<double>();
-  CUDA_TRY(cudaEventRecord(P->all.a, s));
+  sp.narrow = narrow ? 1 : 0;
+  CUDA_TRY(cudaEventRecord(P->summ.a, s));
   LAUNCH_TRY(launch_summary(sp, s));
-  CUDA_TRY(cudaEventRecord(P->all.b, s));
-  CUDA_TRY(cudaEventSynchronize(P->all.b));
-  float ms = 0.f;
-  CUDA_TRY(cudaEventElapsedTime(&ms, P->all.a, P->all.b));
-  P->last_ms += ms;
+  CUDA_TRY(cudaEventRecord(P->summ.b, s));
   P->launches += 4;
-  P->summarized = true;
+  P->summary_pending = true;
   return SABER_OK;
+}
+
+saber_status saber_cuda_sweep_plan_summarize_launch(saber_sweep_plan* P, void* stream) {
+  return summarize_launch_impl(P, stream, true);
+}
+
+saber_status saber_cuda_sweep_plan_summarize(saber_sweep_plan* P, void* stream) {
+  if (saber_status s = summarize_launch_impl(P, stream, false)) return s;
+  return saber_cuda_sweep_plan_wait(P);
 }
 
 saber_status saber_cuda_sweep_plan_buffers(saber_sweep_plan* P, saber_sweep_buffers* out) {

@@ -224,6 +224,7 @@ struct SummaryParams {
   int32_t* best_cap;            // [n_mixes][n_rps]
   double* scratch;              // [n_mixes][n_rps][6] cell-level means/flags
   double* ratios;               // [n_rows][n] latency/SLA ratios (NaN = never completed)
+  int32_t narrow;               // 1 = few small blocks (runs beside the trajectory kernels)
 };
 int launch_summary(const SummaryParams& p, void* stream);
 

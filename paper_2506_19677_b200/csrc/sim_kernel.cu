@@ -1072,6 +1072,10 @@ int plan_sim(int nmax, int group, SimLaunch* out) {
     if (per_sm < 1) return 3;
     l.grid_sel[sel] = sms * per_sm;
   }
+  // The SABER kernel fills the register file of every SM (4 x 128 threads x
+  // 128 registers); leave 8 SMs one block short so a concurrent sweep summary
+  // (single-warp blocks on a side stream) finds room (bench.py pipelining).
+  if (l.grid_sel[kSelSaber] > 16 * kSimBlock / kWarp) l.grid_sel[kSelSaber] -= 8;
   l.grid = l.grid_sel[0];
   l.lane = 0;
   l.block = kSimBlock;

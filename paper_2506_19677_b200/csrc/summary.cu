@@ -26,7 +26,7 @@ namespace {
 constexpr int kCellScratch = 6;
 constexpr unsigned kFull = 0xFFFFFFFFu;
 
-__global__ void ratios_kernel(const SummaryParams p) {
+__global__ void __launch_bounds__(256) ratios_kernel(const SummaryParams p) {
   const int64_t total = static_cast<int64_t>(p.n_mixes) * p.n_rps *
                         (static_cast<int64_t>(p.n_caps) * p.repeats + (p.with_saber ? p.repeats : 0)) *
                         p.n;
@@ -493,8 +493,17 @@ int launch_summary(const SummaryParams& p, void* stream) {
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const int cells = p.n_mixes * p.n_rps;
   if (cells == 0) return 0;
-  ratios_kernel<<<1184, 256, 0, s>>>(p);
-  summary_cells_kernel<<<(cells * 32 + 127) / 128, 128, 0, s>>>(p);
+  // narrow: the summary of one sweep overlapping the next sweep's trajectory
+  // kernels (bench.py pipelining) — small blocks that fit in the register
+  // file those kernels leave free (the static kernel leaves 4,096 registers
+  // per SM: one warp of the cells kernel or two of the ratios kernel fit)
+  if (p.narrow) {
+    ratios_kernel<<<148, 64, 0, s>>>(p);
+    summary_cells_kernel<<<cells, 32, 0, s>>>(p);
+  } else {
+    ratios_kernel<<<1184, 256, 0, s>>>(p);
+    summary_cells_kernel<<<(cells * 32 + 127) / 128, 128, 0, s>>>(p);
+  }
   if (std::getenv("SABER_SUMMARY_RING"))
     summary_mix_kernel<<<2 * p.n_mixes, 64, 0, s>>>(p);
   else
