@@ -655,21 +655,40 @@ saber_status saber_cuda_sweep_plan_create(const saber_sweep_desc* desc, saber_sw
     const int per_rps = desc->n_caps * R + (desc->with_saber ? R : 0);
     const char* om = std::getenv("SABER_ORDER");
     const int order_mode = om ? std::atoi(om) : 1;
-    std::vector<std::pair<double, int32_t>> key(static_cast<size_t>(P->rows_shard));
+    // The key depends only on (rps index, scheduler class): a stable counting
+    // sort over those 2 x n_rps buckets (no comparison sort of the rows).
+    auto key_of = [&](int ri, bool sab) {
+      double kk = -(n / P->rps[static_cast<size_t>(ri)]) - (sab ? 1.0 : 0.0);
+      if (order_mode == 1) kk = (sab ? -1e18 : 0.0) - n / P->rps[static_cast<size_t>(ri)];
+      if (order_mode == 2) kk = 0.0;
+      return kk;
+    };
+    std::vector<double> distinct;
+    for (int ri = 0; ri < n_rps; ++ri)
+      for (int c = 0; c < 2; ++c) distinct.push_back(key_of(ri, c != 0));
+    std::sort(distinct.begin(), distinct.end());
+    distinct.erase(std::unique(distinct.begin(), distinct.end()), distinct.end());
+    std::vector<int32_t> bucket_of(static_cast<size_t>(2 * n_rps));
+    for (int ri = 0; ri < n_rps; ++ri)
+      for (int c = 0; c < 2; ++c)
+        bucket_of[static_cast<size_t>(2 * ri + c)] = static_cast<int32_t>(
+            std::lower_bound(distinct.begin(), distinct.end(), key_of(ri, c != 0)) -
+            distinct.begin());
+    std::vector<int32_t> bucket(static_cast<size_t>(P->rows_shard));
+    std::vector<int64_t> start(distinct.size() + 1, 0);
     for (int64_t k = 0; k < P->rows_shard; ++k) {
       const int64_t r = desc->shard_index + k * desc->shard_count;
       const int ri = static_cast<int>((r / per_rps) % n_rps);
       const bool sab = (r % per_rps) >= desc->n_caps * R;
-      double kk = -(n / P->rps[static_cast<size_t>(ri)]) - (sab ? 1.0 : 0.0);
-      if (order_mode == 1) kk = (sab ? -1e18 : 0.0) - n / P->rps[static_cast<size_t>(ri)];
-      if (order_mode == 2) kk = 0.0;
-      key[static_cast<size_t>(k)] = {kk, static_cast<int32_t>(k)};
+      const int32_t bk = bucket_of[static_cast<size_t>(2 * ri + (sab ? 1 : 0))];
+      bucket[static_cast<size_t>(k)] = bk;
+      ++start[static_cast<size_t>(bk) + 1];
       if (order_mode == 1 && sab) ++P->n_saber_first;
     }
-    std::stable_sort(key.begin(), key.end(),
-                     [](const auto& a, const auto& b) { return a.first < b.first; });
-    std::vector<int32_t> ord(key.size());
-    for (size_t k = 0; k < key.size(); ++k) ord[k] = key[k].second;
+    for (size_t b = 1; b < start.size(); ++b) start[b] += start[b - 1];
+    std::vector<int32_t> ord(bucket.size());
+    for (size_t k = 0; k < bucket.size(); ++k)
+      ord[static_cast<size_t>(start[static_cast<size_t>(bucket[k])]++)] = static_cast<int32_t>(k);
     ALLOC_TRY(P->order, dev, std::max<size_t>(1, ord.size()) * 4);
     if (!ord.empty())
       CUDA_TRY(cudaMemcpy(P->order.p, ord.data(), ord.size() * 4, cudaMemcpyHostToDevice));
@@ -705,11 +724,11 @@ saber_status saber_cuda_sweep_plan_create(const saber_sweep_desc* desc, saber_sw
   if (saber_status s = P->all.init()) return s;
   if (saber_status s = P->sim.init()) return s;
   if (saber_status s = P->summ.init()) return s;
-  if (P->n_saber_first > 0 && P->n_saber_first < P->rows_shard) {
-    CUDA_TRY(cudaStreamCreateWithFlags(&P->side, cudaStreamNonBlocking));
-    CUDA_TRY(cudaEventCreateWithFlags(&P->fork, cudaEventDisableTiming));
-    CUDA_TRY(cudaEventCreateWithFlags(&P->join, cudaEventDisableTiming));
-  }
+  // side stream: the static half of a split launch, and the one-shot
+  // summary overlapping the row download
+  CUDA_TRY(cudaStreamCreateWithFlags(&P->side, cudaStreamNonBlocking));
+  CUDA_TRY(cudaEventCreateWithFlags(&P->fork, cudaEventDisableTiming));
+  CUDA_TRY(cudaEventCreateWithFlags(&P->join, cudaEventDisableTiming));
   tr.mark("events");
   *out = guard.release();
   return SABER_OK;
@@ -805,7 +824,8 @@ saber_status saber_cuda_sweep_plan_launch(saber_sweep_plan* P, void* stream) {
   sp.order = P->order.as<int32_t>();
   sp.ticks = P->ticktab.view;
   CUDA_TRY(cudaEventRecord(P->sim.a, s));
-  const bool split = P->side != nullptr && P->scratch.launch.group == 32 && !P->scratch.launch.lane &&
+  const bool split = P->n_saber_first > 0 && P->n_saber_first < P->rows_shard &&
+                     P->scratch.launch.group == 32 && !P->scratch.launch.lane &&
                      std::getenv("SABER_NO_SPLIT") == nullptr;
   if (split) {
     // SABER rows [0, ns) on the SABER-only kernel, static rows [ns, N) on the
@@ -980,15 +1000,32 @@ saber_status saber_cuda_sweep(const saber_sweep_desc* desc, saber_sweep_out* out
   if (saber_status s = saber_cuda_sweep_plan_create(desc, &P)) return s;
   std::unique_ptr<saber_sweep_plan, void (*)(saber_sweep_plan*)> guard(P, saber_cuda_sweep_plan_destroy);
   if (saber_status s = saber_cuda_sweep_plan_run(P, nullptr)) return s;
-  const double run_ms = P->last_ms;
-  if (out->summary || out->best_cap_by_rps) {
+  const bool want_summary = out->summary || out->best_cap_by_rps;
+  if (want_summary) {
     if (desc->shard_count != 1)
       return fail(SABER_EINVAL, "summary of a sharded sweep needs the rows of every shard "
                                 "(all-reduce the plan buffers, then summarize)");
-    if (saber_status s = saber_cuda_sweep_plan_summarize(P, nullptr)) return s;
+    // the summary runs on the side stream while the rows download
+    if (saber_status s = summarize_launch_impl(P, P->side, false)) return s;
   }
-  if (saber_status s = saber_cuda_sweep_plan_fetch(P, out)) return s;
-  (void)run_ms;
+  saber_sweep_out rows_part = *out;
+  rows_part.summary = nullptr;
+  rows_part.best_cap_by_rps = nullptr;
+  if (saber_status s = saber_cuda_sweep_plan_fetch(P, &rows_part)) return s;
+  int64_t d2h = rows_part.d2h_bytes;
+  if (want_summary) {
+    if (saber_status s = saber_cuda_sweep_plan_wait(P)) return s;
+    saber_sweep_out summ_part{};
+    summ_part.summary = out->summary;
+    summ_part.best_cap_by_rps = out->best_cap_by_rps;
+    if (saber_status s = saber_cuda_sweep_plan_fetch(P, &summ_part)) return s;
+    d2h += summ_part.d2h_bytes;
+  }
+  out->n_rows = P->n_rows;
+  out->h2d_bytes = P->h2d_bytes;
+  out->d2h_bytes = d2h;
+  out->device_ms = P->last_ms;
+  out->kernel_launches = P->launches;
   return SABER_OK;
 }
 
