@@ -163,3 +163,47 @@ def test_sweep_rows_and_summary_match_reference(engine, ref):
         for a, b in zip(vals, r["summary"][k]):
             assert same_float(a, b), (m, vals, list(r["summary"][k]))
         assert [s.best_cap_by_rps[float(x)] for x in grid.rps_list] == list(r["best_cap"][k])
+
+
+def test_pipelined_plans_match_synchronous(engine):
+    """The asynchronous plan API (launch / summarize_launch / wait) on two
+    plans and two streams, as bench.py pipelines sweeps, gives exactly the
+    synchronous rows and summary; the narrow summary grids included."""
+    import torch
+    import paper_2506_19677_b200 as S
+    grid = S.SweepGrid(["w1", "w3"], [1.0, 4.0, 15.0], [10, 40], True)
+    base = sim_config("w1", 1.0, 100, 42)
+    base.repeats = 8
+    ref_plan = S.SweepPlan(grid, base)
+    ref_plan.run()
+    ref_plan.summarize()
+    rows0, _, summ0, best0 = ref_plan.fetch(summary=True)
+    ref_plan.close()
+
+    plans = [S.SweepPlan(grid, base) for _ in range(2)]
+    main = torch.cuda.current_stream()
+    side = torch.cuda.Stream(priority=-1)
+    done = [None, None]
+    for k in range(5):
+        i = k % 2
+        if done[i] is not None:
+            main.wait_event(done[i])
+        plans[i].launch(main.cuda_stream)
+        e = torch.cuda.Event()
+        e.record(main)
+        side.wait_event(e)
+        plans[i].summarize_launch(side.cuda_stream)
+        d = torch.cuda.Event()
+        d.record(side)
+        done[i] = d
+    torch.cuda.synchronize()
+    for pl in plans:
+        pl.wait()
+        rows, _, summ, best = pl.fetch(summary=True)
+        assert rows.tobytes() == rows0.tobytes()
+        assert np.array_equal(best, best0)
+        for a, b in zip(summ, summ0):
+            for f in ("saber_mean_goodput", "best_static_mean_goodput", "delta", "saber_pooled_cv",
+                      "best_static_pooled_cv", "saber_rps_mean_cv", "best_static_rps_mean_cv"):
+                assert same_float(getattr(a, f), getattr(b, f)), f
+        pl.close()
