@@ -648,19 +648,23 @@ saber_status saber_cuda_sweep_plan_create(const saber_sweep_desc* desc, saber_sw
 
   // Execution order: every SABER trajectory first (they are
   // ~4x the work of a static one, and keeping the two code paths apart in
-  // time keeps the instruction cache warm: measured 21.9 vs 25.8 ms on config
-  // 2), each class longest arrival span n / rps first.  SABER_ORDER=0 orders
-  // by n / rps only, SABER_ORDER=2 keeps row order (A/B runs).
+  // time keeps the instruction cache warm: 21.9 vs 25.8 ms on config 2),
+  // SABER at high rates first (their gates dominate; low-rate SABER runs are
+  // mostly streaks), static rows longest arrival span n / rps first.
+  // SABER_ORDER=0 orders by n / rps only, 1 = SABER first by n / rps,
+  // 2 = row order (A/B runs).
   {
     const int per_rps = desc->n_caps * R + (desc->with_saber ? R : 0);
     const char* om = std::getenv("SABER_ORDER");
-    const int order_mode = om ? std::atoi(om) : 1;
+    const int order_mode = om ? std::atoi(om) : 3;
     // The key depends only on (rps index, scheduler class): a stable counting
     // sort over those 2 x n_rps buckets (no comparison sort of the rows).
     auto key_of = [&](int ri, bool sab) {
       double kk = -(n / P->rps[static_cast<size_t>(ri)]) - (sab ? 1.0 : 0.0);
       if (order_mode == 1) kk = (sab ? -1e18 : 0.0) - n / P->rps[static_cast<size_t>(ri)];
       if (order_mode == 2) kk = 0.0;
+      if (order_mode == 3)  // SABER first, high rates first (the heavy gates); static longest first
+        kk = sab ? -1e18 + n / P->rps[static_cast<size_t>(ri)] : -(n / P->rps[static_cast<size_t>(ri)]);
       return kk;
     };
     std::vector<double> distinct;
@@ -683,7 +687,7 @@ saber_status saber_cuda_sweep_plan_create(const saber_sweep_desc* desc, saber_sw
       const int32_t bk = bucket_of[static_cast<size_t>(2 * ri + (sab ? 1 : 0))];
       bucket[static_cast<size_t>(k)] = bk;
       ++start[static_cast<size_t>(bk) + 1];
-      if (order_mode == 1 && sab) ++P->n_saber_first;
+      if ((order_mode == 1 || order_mode == 3) && sab) ++P->n_saber_first;
     }
     for (size_t b = 1; b < start.size(); ++b) start[b] += start[b - 1];
     std::vector<int32_t> ord(bucket.size());
