@@ -567,10 +567,10 @@ def sweep(grid: SweepGrid, base: SimConfig, jobs: int = 0, device: int = 0,
         dev_ms = plan.stats()[0]
     finally:
         plan.close()
-    out_rows = []
-    for (m, r, mode, cap, seed), row in zip(sweep_row_keys(grid, base), rows):
-        out_rows.append(SweepRow(m, r, mode, cap, seed, float(row["goodput"]), float(row["ratio_mean"]),
-                                 float(row["ratio_std"]), float(row["cv"])))
+    # column-wise (numpy -> Python floats in bulk), then one object per row
+    cols = [rows[f].tolist() for f in ("goodput", "ratio_mean", "ratio_std", "cv")]
+    out_rows = [SweepRow(m, r, mode, cap, seed, g, rm, rs, cv)
+                for (m, r, mode, cap, seed), g, rm, rs, cv in zip(sweep_row_keys(grid, base), *cols)]
     summary = {}
     for k, m in enumerate(grid.mixes):
         s = summ[k]
