@@ -190,11 +190,19 @@ def engine_arm(args):
     world = env_int("WORLD_SIZE", 1)
     rank = env_int("RANK", 0)
     local = env_int("LOCAL_RANK", 0)
+    # Test hooks for the N > 1 path on a single-GPU box (never set by the
+    # driver): every rank on one device, gloo instead of NCCL.
+    if os.environ.get("SABER_BENCH_DEVICE") is not None:
+        local = env_int("SABER_BENCH_DEVICE", 0)
+    backend = os.environ.get("SABER_BENCH_BACKEND", "nccl")
     dist = None
     if world > 1:
         import torch.distributed as dist  # noqa: F811
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     else:
         torch.cuda.set_device(local)
     device = torch.cuda.current_device()
