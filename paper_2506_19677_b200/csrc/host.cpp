@@ -445,7 +445,9 @@ struct saber_sweep_plan {
   int n_items = 0;
   int model_tab = -1, gt_tab = 0;
   double ceiling = 0.0;
-  std::vector<int64_t> stream_len;
+  std::vector<int64_t> stream_len;   // generated draws per seed stream (<= stream_full)
+  std::vector<int64_t> stream_full;  // the provable bound (draw_bound)
+  int64_t stream_cap = 0;            // current cap on stream_len (grows on exhaustion)
   int64_t total_draws = 0;
 
   Workloads wl;
@@ -463,6 +465,7 @@ struct saber_sweep_plan {
   }
   Timer all, sim, summ;
   bool run_pending = false, summary_pending = false;
+  bool rerun = false;  // the draw streams were grown after an exhaustion
   double last_ms = 0.0, sim_ms = 0.0;
   int launches = 0;
   bool summarized = false;
@@ -512,6 +515,24 @@ saber_status validate_sweep(const saber_sweep_desc& d) {
 }
 
 }  // namespace
+
+// (Re)size the per-seed scheduler draw streams to min(bound, cap).
+saber_status set_stream_lengths(saber_sweep_plan* P, int dev) {
+  const size_t ns = P->stream_full.size();
+  if (ns == 0) return SABER_OK;
+  std::vector<int64_t> off(ns);
+  P->stream_len.assign(ns, 0);
+  P->total_draws = 0;
+  for (size_t i = 0; i < ns; ++i) {
+    P->stream_len[i] = std::min(P->stream_full[i], P->stream_cap);
+    off[i] = P->total_draws;
+    P->total_draws += P->stream_len[i];
+  }
+  ALLOC_TRY(P->draws, dev, static_cast<size_t>(std::max<int64_t>(1, P->total_draws)) * 4);
+  CUDA_TRY(cudaMemcpy(P->s_off.p, off.data(), ns * 8, cudaMemcpyHostToDevice));
+  CUDA_TRY(cudaMemcpy(P->s_len.p, P->stream_len.data(), ns * 8, cudaMemcpyHostToDevice));
+  return SABER_OK;
+}
 
 extern "C" {
 
@@ -592,7 +613,6 @@ saber_status saber_cuda_sweep_plan_create(const saber_sweep_desc* desc, saber_sw
 
   // Scheduler RNG streams, one per seed, sized by the horizon bound.
   std::vector<uint64_t> seeds;
-  std::vector<int64_t> off;
   if (desc->with_saber) {
     double rmin = P->rps[0];
     for (double r : P->rps) rmin = std::min(rmin, r);
@@ -601,9 +621,7 @@ saber_status saber_cuda_sweep_plan_create(const saber_sweep_desc* desc, saber_sw
       const double hb = desc->has_horizon ? desc->horizon : last + 10.0 * 12.0 + 1.0;
       const int64_t len = draw_bound(hb, desc->tick, desc->window_size, n);
       seeds.push_back((desc->seed + static_cast<uint64_t>(i)) ^ kSchedulerSeedSalt);
-      off.push_back(P->total_draws);
-      P->stream_len.push_back(len);
-      P->total_draws += len;
+      P->stream_full.push_back(len);
     }
   }
 
@@ -638,9 +656,8 @@ saber_status saber_cuda_sweep_plan_create(const saber_sweep_desc* desc, saber_sw
   ALLOC_TRY(P->ratios, dev, static_cast<size_t>(P->n_rows) * n * 8);
   if (desc->with_saber) {
     ALLOC_TRY(P->seeds, dev, seeds.size() * 8);
-    ALLOC_TRY(P->s_off, dev, off.size() * 8);
-    ALLOC_TRY(P->s_len, dev, off.size() * 8);
-    ALLOC_TRY(P->draws, dev, static_cast<size_t>(std::max<int64_t>(1, P->total_draws)) * 4);
+    ALLOC_TRY(P->s_off, dev, P->stream_full.size() * 8);
+    ALLOC_TRY(P->s_len, dev, P->stream_full.size() * 8);
   }
   tr.mark("device buffers");
   if (saber_status s = P->scratch.alloc(dev, n)) return s;
@@ -711,12 +728,18 @@ saber_status saber_cuda_sweep_plan_create(const saber_sweep_desc* desc, saber_sw
     CUDA_TRY(cudaMemcpy(P->caps_d.p, P->caps.data(), P->caps.size() * 4, cudaMemcpyHostToDevice));
   if (desc->with_saber) {
     CUDA_TRY(cudaMemcpy(P->seeds.p, seeds.data(), seeds.size() * 8, cudaMemcpyHostToDevice));
-    CUDA_TRY(cudaMemcpy(P->s_off.p, off.data(), off.size() * 8, cudaMemcpyHostToDevice));
-    CUDA_TRY(cudaMemcpy(P->s_len.p, P->stream_len.data(), off.size() * 8, cudaMemcpyHostToDevice));
+    // Scheduler draw streams are generated up to a cap far below the provable
+    // bound (config 2 uses <= 19K of ~150K); a trajectory that exhausts its
+    // stream raises kErrRngExhausted, and the plan grows the cap (up to the
+    // bound) and reruns — never a silent draw (saber_cuda_sweep_plan_wait).
+    P->stream_cap = 32768;
+    if (const char* e = std::getenv("SABER_DRAW_CAP")) P->stream_cap = std::max(1, std::atoi(e));
+    if (saber_status s = set_stream_lengths(P, dev)) return s;
   }
   P->h2d_bytes += static_cast<int64_t>(items.size() * sizeof(WorkloadItem) + base.size() * 8 +
                                       th.size() * 8 + tt.size() + tlast.size() + tab.size() * 8 +
-                                      P->caps.size() * 4 + seeds.size() * 8 + off.size() * 16);
+                                      P->caps.size() * 4 + seeds.size() * 8 +
+                                      P->stream_full.size() * 16);
   tr.mark("h2d");
   if (saber_status s = P->ticktab.build(dev, desc->tick, hb_max)) return s;
   P->h2d_bytes += P->ticktab.bytes;
@@ -882,8 +905,17 @@ saber_status saber_cuda_sweep_plan_wait(saber_sweep_plan* P) {
     P->run_pending = false;
     int32_t err = 0;
     CUDA_TRY(cudaMemcpy(&err, P->err.p, 4, cudaMemcpyDeviceToHost));
-    if (err == kErrRngExhausted)
+    if (err == kErrRngExhausted) {
+      int64_t full = 0;
+      for (int64_t f : P->stream_full) full = std::max(full, f);
+      if (P->stream_cap < full) {
+        P->stream_cap = std::min(full, P->stream_cap * 4);
+        if (saber_status s = set_stream_lengths(P, P->device)) return s;
+        P->rerun = true;
+        return fail(SABER_EINTERNAL, "scheduler RNG streams grown; rerun the sweep");
+      }
       return fail(SABER_EINTERNAL, "scheduler RNG stream exhausted (draw bound violated)");
+    }
     if (err != 0) return fail(SABER_EINTERNAL, "trajectory kernel error " + std::to_string(err));
   }
   if (P->summary_pending) {
@@ -898,8 +930,12 @@ saber_status saber_cuda_sweep_plan_wait(saber_sweep_plan* P) {
 }
 
 saber_status saber_cuda_sweep_plan_run(saber_sweep_plan* P, void* stream) {
-  if (saber_status s = saber_cuda_sweep_plan_launch(P, stream)) return s;
-  return saber_cuda_sweep_plan_wait(P);
+  for (;;) {
+    if (saber_status s = saber_cuda_sweep_plan_launch(P, stream)) return s;
+    const saber_status s = saber_cuda_sweep_plan_wait(P);
+    if (s == SABER_OK || !P->rerun) return s;  // grown draw streams: run again
+    P->rerun = false;
+  }
 }
 
 static saber_status summarize_launch_impl(saber_sweep_plan* P, void* stream, bool narrow) {

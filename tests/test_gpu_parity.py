@@ -207,3 +207,17 @@ def test_pipelined_plans_match_synchronous(engine):
                       "best_static_pooled_cv", "saber_rps_mean_cv", "best_static_rps_mean_cv"):
                 assert same_float(getattr(a, f), getattr(b, f)), f
         pl.close()
+
+
+def test_draw_streams_grow_on_exhaustion(engine, monkeypatch):
+    """Scheduler draw streams start far below the provable bound and grow
+    (rerunning the sweep) when a trajectory exhausts one: a tiny initial cap
+    gives exactly the rows of the default one."""
+    import paper_2506_19677_b200 as S
+    grid = S.SweepGrid(["w1", "w2"], [2.0, 12.0], [20], True)
+    base = sim_config("w1", 1.0, 80, 42)
+    base.repeats = 4
+    a = S.sweep(grid, base)
+    monkeypatch.setenv("SABER_DRAW_CAP", "16")
+    b = S.sweep(grid, base)
+    assert a.traj_rows.tobytes() == b.traj_rows.tobytes()
