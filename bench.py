@@ -264,6 +264,7 @@ def engine_arm(args):
         summary_done[i] = e
 
     for k in range(args.warmup):
+        flush.fill_(k)  # (also loads the fill kernel before the timed region)
         step(k, sync=True)  # synchronous: every warm-up sweep is error-checked
     torch.cuda.synchronize()
 
@@ -453,7 +454,7 @@ def cpu_baseline(gpu_rows, grid, base):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="engine", choices=["engine", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")

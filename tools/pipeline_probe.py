@@ -29,7 +29,11 @@ def main():
     t0 = ev()
     t0.record(main_s)
     marks = []
-    for k in range(8):
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.int32, device="cuda")
+    nsteps = int(os.environ.get("PROBE_STEPS", "8"))
+    for k in range(nsteps):
+        if os.environ.get("PROBE_FLUSH"):
+            flush.fill_(k)
         i = k % 2
         if done[i] is not None:
             main_s.wait_event(done[i])
