@@ -997,6 +997,78 @@ __global__ void __launch_bounds__(128) row_metrics_kernel(const RowMetricsParams
   R->cv = mean == 0.0 ? nan("") : R->ratio_std / mean;
 }
 
+// K2 with one warp per row: the per-request tests and counts are
+// lane-parallel (ballots), and the two sequential sums of compute_metrics run
+// as one dependent chain fed by shuffles, in request-id order; requests that
+// never completed contribute an exact +0 (sums of non-negative terms).
+__global__ void __launch_bounds__(128) row_metrics_warp_kernel(const RowMetricsParams p) {
+  const int lane = threadIdx.x & 31;
+  const int64_t i = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  if (i >= p.n_traj) return;  // uniform per warp
+  const TrajDesc d = p.traj[i];
+  const int nmax = p.wl.nmax;
+  const int64_t wo = static_cast<int64_t>(d.workload) * nmax;
+  const double* C = p.completion + d.row * nmax;
+  const double* ARR = p.wl.arrival + wo;
+  const double* SLA = p.wl.sla + wo;
+  const int8_t* TASK = p.wl.task + wo;
+  int64_t met = 0, comp = 0;
+  int64_t issued[4] = {0, 0, 0, 0}, metk[4] = {0, 0, 0, 0};
+  double sum = 0.0;
+  for (int base = 0; base < d.n; base += kWarp) {
+    const int q = base + lane;
+    const bool valid = q < d.n;
+    const double c = valid ? C[q] : nan("");
+    const bool has = valid && !isnan(c);
+    const double a = has ? ARR[q] : 0.0, sl = has ? SLA[q] : 1.0;
+    const bool m = has && c - a <= sl;
+    const int tk = valid ? TASK[q] : -1;
+    met += __popc(__ballot_sync(0xFFFFFFFFu, m));
+    comp += __popc(__ballot_sync(0xFFFFFFFFu, has));
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      issued[k] += __popc(__ballot_sync(0xFFFFFFFFu, tk == k));
+      metk[k] += __popc(__ballot_sync(0xFFFFFFFFu, m && tk == k));
+    }
+    const double v = has ? (c - a) / sl : 0.0;
+#pragma unroll
+    for (int k = 0; k < kWarp; ++k) sum += __shfl_sync(0xFFFFFFFFu, v, k);
+  }
+  saber_traj_row* R = p.rows + d.row;
+  if (lane == 0) {
+    R->goodput = static_cast<double>(met) / static_cast<double>(d.n);
+    R->completed = comp;
+    R->met = met;
+    for (int k = 0; k < 4; ++k) {
+      R->issued_by_task[k] = issued[k];
+      R->met_by_task[k] = metk[k];
+    }
+  }
+  if (comp == 0) {
+    if (lane == 0) R->ratio_mean = R->ratio_std = R->cv = nan("");
+    return;
+  }
+  const double mean = sum / static_cast<double>(comp);
+  double var = 0.0;
+  for (int base = 0; base < d.n; base += kWarp) {
+    const int q = base + lane;
+    const double c = q < d.n ? C[q] : nan("");
+    double t = 0.0;
+    if (!isnan(c)) {
+      const double v = (c - ARR[q]) / SLA[q];
+      t = (v - mean) * (v - mean);
+    }
+#pragma unroll
+    for (int k = 0; k < kWarp; ++k) var += __shfl_sync(0xFFFFFFFFu, t, k);
+  }
+  if (lane == 0) {
+    var /= static_cast<double>(comp);
+    R->ratio_mean = mean;
+    R->ratio_std = sqrt(var);
+    R->cv = mean == 0.0 ? nan("") : R->ratio_std / mean;
+  }
+}
+
 template <int NW, int G, bool kTrace, bool kRecords, int kSel = kSelAny>
 void* kernel_ptr() {
   return reinterpret_cast<void*>(&sim_kernel<NW, G, kTrace, kRecords, kSel>);
@@ -1113,8 +1185,14 @@ int launch_tick_index(const WorkloadTables& wl, int64_t cells, const TickTable& 
 int launch_row_metrics(const RowMetricsParams& p, void* stream) {
   if (p.n_traj == 0) return 0;
   const int block = 128;
-  const int grid = (p.n_traj + block - 1) / block;
-  row_metrics_kernel<<<grid, block, 0, static_cast<cudaStream_t>(stream)>>>(p);
+  if (std::getenv("SABER_ROW_METRICS_THREAD")) {
+    const int grid = (p.n_traj + block - 1) / block;
+    row_metrics_kernel<<<grid, block, 0, static_cast<cudaStream_t>(stream)>>>(p);
+  } else {
+    const int64_t grid = (static_cast<int64_t>(p.n_traj) * kWarp + block - 1) / block;
+    row_metrics_warp_kernel<<<static_cast<unsigned>(grid), block, 0,
+                              static_cast<cudaStream_t>(stream)>>>(p);
+  }
   return cudaGetLastError() == cudaSuccess ? 0 : 1;
 }
 
