@@ -252,7 +252,8 @@ def engine_arm(args):
             return
         if summary_done[i] is not None:
             stream.wait_event(summary_done[i])  # plan i's buffers are free again
-        pl.launch(stream.cuda_stream)
+        pl.launch(stream.cuda_stream)  # per-row metrics stay on this stream: narrow
+        # metrics blocks on the side stream displaced trajectory blocks (14.8 vs 13.6 ms)
         sim_done = torch.cuda.Event()
         sim_done.record(stream)
         side.wait_event(sim_done)

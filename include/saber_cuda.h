@@ -98,6 +98,12 @@ typedef struct {
   int64_t refresh_entries, gate_candidates, ledger_scanned, rng_draws;
   double last_arrival;
   double horizon;
+  /* Latency percentiles p50, p90, p99 of completion - arrival over the
+   * trajectory's issued requests, read off the reference's cdf
+   * (metrics.cpp:61-85, all tasks): the smallest latency x whose fraction
+   * (#latencies <= x) / issued is >= p; NaN when that fraction is never
+   * reached (too few completions).  Exact (an order statistic). */
+  double latency_q[3];
 } saber_traj_row;
 
 /* Decision record (scheduler.hpp:48-55). Absent speeds: has_* = 0. */
@@ -201,6 +207,11 @@ saber_status saber_cuda_sweep_plan_summarize(saber_sweep_plan* plan, void* cuda_
 saber_status saber_cuda_sweep_plan_launch(saber_sweep_plan* plan, void* cuda_stream);
 saber_status saber_cuda_sweep_plan_summarize_launch(saber_sweep_plan* plan, void* cuda_stream);
 saber_status saber_cuda_sweep_plan_wait(saber_sweep_plan* plan);
+/* launch = launch_sim + metrics_launch on one stream.  Split, the per-row
+ * metrics (which feed the summary and the fetched rows) can run on the
+ * summary's stream; multi-GPU: before the gather (each rank owns its rows). */
+saber_status saber_cuda_sweep_plan_launch_sim(saber_sweep_plan* plan, void* cuda_stream);
+saber_status saber_cuda_sweep_plan_metrics_launch(saber_sweep_plan* plan, void* cuda_stream);
 saber_status saber_cuda_sweep_plan_buffers(saber_sweep_plan* plan, saber_sweep_buffers* out);
 saber_status saber_cuda_sweep_plan_fetch(saber_sweep_plan* plan, saber_sweep_out* out);
 /* CUDA-event time and launches of the last plan_run (+ summarize). */

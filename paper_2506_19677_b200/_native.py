@@ -36,6 +36,7 @@ class saber_traj_row(C.Structure):
         ("prefill_updates", C.c_int64), ("refresh_entries", C.c_int64),
         ("gate_candidates", C.c_int64), ("ledger_scanned", C.c_int64), ("rng_draws", C.c_int64),
         ("last_arrival", C.c_double), ("horizon", C.c_double),
+        ("latency_q", C.c_double * 3),
     ]
 
 
@@ -186,6 +187,8 @@ SYMBOLS = [
     ("saber_cuda_sweep_plan_launch", C.c_int, [C.c_void_p, C.c_void_p]),
     ("saber_cuda_sweep_plan_summarize_launch", C.c_int, [C.c_void_p, C.c_void_p]),
     ("saber_cuda_sweep_plan_wait", C.c_int, [C.c_void_p]),
+    ("saber_cuda_sweep_plan_launch_sim", C.c_int, [C.c_void_p, C.c_void_p]),
+    ("saber_cuda_sweep_plan_metrics_launch", C.c_int, [C.c_void_p, C.c_void_p]),
     ("saber_cuda_sweep_plan_buffers", C.c_int, [C.c_void_p, _P(saber_sweep_buffers)]),
     ("saber_cuda_sweep_plan_fetch", C.c_int, [C.c_void_p, _P(saber_sweep_out)]),
     ("saber_cuda_sweep_plan_stats", C.c_int, [C.c_void_p, _P(C.c_double), _P(C.c_double),

@@ -489,6 +489,14 @@ class SweepPlan:
         """Enqueue run() without waiting (pair with wait())."""
         _check(N.lib().saber_cuda_sweep_plan_launch(self.handle, C.c_void_p(stream)))
 
+    def launch_sim(self, stream: int = 0):
+        """launch() without the per-row metrics (pair with metrics_launch())."""
+        _check(N.lib().saber_cuda_sweep_plan_launch_sim(self.handle, C.c_void_p(stream)))
+
+    def metrics_launch(self, stream: int = 0):
+        """Enqueue the per-row metrics of the last launch_sim()."""
+        _check(N.lib().saber_cuda_sweep_plan_metrics_launch(self.handle, C.c_void_p(stream)))
+
     def summarize_launch(self, stream: int = 0):
         """Enqueue summarize() without waiting (pair with wait())."""
         _check(N.lib().saber_cuda_sweep_plan_summarize_launch(self.handle, C.c_void_p(stream)))

@@ -516,6 +516,21 @@ saber_status validate_sweep(const saber_sweep_desc& d) {
 
 }  // namespace
 
+// K2 (per-row metrics) of the plan's shard on `s` (narrow: few single-warp
+// blocks, to run beside another sweep's trajectory kernels).
+static saber_status metrics_launch_impl(saber_sweep_plan* P, cudaStream_t s, bool narrow) {
+  RowMetricsParams rm{};
+  rm.rows = P->rows.as<saber_traj_row>();
+  rm.completion = P->comp.as<double>();
+  rm.wl = P->wl.view(P->n);
+  rm.traj = P->descs.as<TrajDesc>();
+  rm.n_traj = static_cast<int32_t>(P->rows_shard);
+  rm.narrow = narrow ? 1 : 0;
+  LAUNCH_TRY(launch_row_metrics(rm, s));
+  ++P->launches;
+  return SABER_OK;
+}
+
 // (Re)size the per-seed scheduler draw streams to min(bound, cap).
 saber_status set_stream_lengths(saber_sweep_plan* P, int dev) {
   const size_t ns = P->stream_full.size();
@@ -761,7 +776,7 @@ saber_status saber_cuda_sweep_plan_create(const saber_sweep_desc* desc, saber_sw
   return SABER_OK;
 }
 
-saber_status saber_cuda_sweep_plan_launch(saber_sweep_plan* P, void* stream) {
+static saber_status plan_launch_impl(saber_sweep_plan* P, void* stream, bool with_metrics) {
   if (!P) return fail(SABER_EINVAL, "null plan");
   CUDA_TRY(cudaSetDevice(P->device));
   cudaStream_t s = static_cast<cudaStream_t>(stream);
@@ -878,18 +893,26 @@ saber_status saber_cuda_sweep_plan_launch(saber_sweep_plan* P, void* stream) {
     ++P->launches;
   }
   CUDA_TRY(cudaEventRecord(P->sim.b, s));
-
-  RowMetricsParams rm{};
-  rm.rows = P->rows.as<saber_traj_row>();
-  rm.completion = P->comp.as<double>();
-  rm.wl = sp.wl;
-  rm.traj = sp.traj;
-  rm.n_traj = sp.n_traj;
-  LAUNCH_TRY(launch_row_metrics(rm, s));
-  ++P->launches;
+  if (with_metrics) {
+    if (saber_status st = metrics_launch_impl(P, s, false)) return st;
+  }
   CUDA_TRY(cudaEventRecord(P->all.b, s));
   P->run_pending = true;
   return SABER_OK;
+}
+
+saber_status saber_cuda_sweep_plan_launch(saber_sweep_plan* P, void* stream) {
+  return plan_launch_impl(P, stream, true);
+}
+
+saber_status saber_cuda_sweep_plan_launch_sim(saber_sweep_plan* P, void* stream) {
+  return plan_launch_impl(P, stream, false);
+}
+
+saber_status saber_cuda_sweep_plan_metrics_launch(saber_sweep_plan* P, void* stream) {
+  if (!P) return fail(SABER_EINVAL, "null plan");
+  CUDA_TRY(cudaSetDevice(P->device));
+  return metrics_launch_impl(P, static_cast<cudaStream_t>(stream), true);
 }
 
 saber_status saber_cuda_sweep_plan_wait(saber_sweep_plan* P) {

@@ -210,6 +210,7 @@ struct RowMetricsParams {
   WorkloadTables wl;
   const TrajDesc* traj;
   int32_t n_traj;
+  int32_t narrow;  // 1 = a few single-warp blocks (beside the trajectory kernels)
 };
 int launch_row_metrics(const RowMetricsParams& p, void* stream);
 

@@ -943,69 +943,18 @@ __global__ void __launch_bounds__(kSimBlock, kSel == kSelStatic  ? SABER_STATIC_
   }
 }
 
-// K2: per-row metrics (make_record + compute_metrics, metrics.cpp:17-140).
-// Sequential sums in request-id order, exactly as the reference.
-__global__ void __launch_bounds__(128) row_metrics_kernel(const RowMetricsParams p) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= p.n_traj) return;
-  const TrajDesc d = p.traj[i];
-  const int nmax = p.wl.nmax;
-  const int64_t wo = static_cast<int64_t>(d.workload) * nmax;
-  const double* C = p.completion + d.row * nmax;
-  const double* ARR = p.wl.arrival + wo;
-  const double* SLA = p.wl.sla + wo;
-  const int8_t* TASK = p.wl.task + wo;
-  int64_t met = 0, comp = 0;
-  int64_t issued[4] = {0, 0, 0, 0}, metk[4] = {0, 0, 0, 0};
-  double sum = 0.0;
-  for (int q = 0; q < d.n; ++q) {
-    const double c = C[q];
-    const bool has = !isnan(c);
-    const bool m = has && c - ARR[q] <= SLA[q];
-    met += m;
-    comp += has;
-    const int tk = TASK[q];
-    if (tk >= 0 && tk < 4) {
-      issued[tk] += 1;
-      metk[tk] += m;
-    }
-    if (has) sum += (c - ARR[q]) / SLA[q];
-  }
-  saber_traj_row* R = p.rows + d.row;
-  R->goodput = static_cast<double>(met) / static_cast<double>(d.n);
-  R->completed = comp;
-  R->met = met;
-  for (int k = 0; k < 4; ++k) {
-    R->issued_by_task[k] = issued[k];
-    R->met_by_task[k] = metk[k];
-  }
-  if (comp == 0) {
-    R->ratio_mean = R->ratio_std = R->cv = nan("");
-    return;
-  }
-  const double mean = sum / static_cast<double>(comp);
-  double var = 0.0;
-  for (int q = 0; q < d.n; ++q) {
-    const double c = C[q];
-    if (isnan(c)) continue;
-    const double v = (c - ARR[q]) / SLA[q];
-    var += (v - mean) * (v - mean);
-  }
-  var /= static_cast<double>(comp);
-  R->ratio_mean = mean;
-  R->ratio_std = sqrt(var);
-  R->cv = mean == 0.0 ? nan("") : R->ratio_std / mean;
-}
+// K2: per-row metrics (make_record + compute_metrics, metrics.cpp:17-140),
+// one warp per row: the per-request tests and counts are lane-parallel
+// (ballots), and the two sequential sums of compute_metrics run as one
+// dependent chain fed by shuffles, in request-id order; requests that never
+// completed contribute an exact +0 (sums of non-negative terms).  Then the
+// latency percentiles off the reference's cdf (metrics.cpp:61-85) as exact
+// order statistics (rank counting over the row's latencies in shared memory).
+constexpr int kQuantiles = 3;
+__device__ const double kQuantileP[kQuantiles] = {0.5, 0.9, 0.99};
 
-// K2 with one warp per row: the per-request tests and counts are
-// lane-parallel (ballots), and the two sequential sums of compute_metrics run
-// as one dependent chain fed by shuffles, in request-id order; requests that
-// never completed contribute an exact +0 (sums of non-negative terms).
-__global__ void __launch_bounds__(128) row_metrics_warp_kernel(const RowMetricsParams p) {
-  const int lane = threadIdx.x & 31;
-  const int64_t i = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-  if (i >= p.n_traj) return;  // uniform per warp
-  const TrajDesc d = p.traj[i];
+__device__ __forceinline__ void row_metrics_one(const RowMetricsParams& p, const TrajDesc d,
+                                                int lane, double* lat) {
   const int nmax = p.wl.nmax;
   const int64_t wo = static_cast<int64_t>(d.workload) * nmax;
   const double* C = p.completion + d.row * nmax;
@@ -1035,6 +984,50 @@ __global__ void __launch_bounds__(128) row_metrics_warp_kernel(const RowMetricsP
     for (int k = 0; k < kWarp; ++k) sum += __shfl_sync(0xFFFFFFFFu, v, k);
   }
   saber_traj_row* R = p.rows + d.row;
+  // latency percentiles: the k-th smallest latency, k = min{i : (i+1)/n >= p}
+  {
+    __syncwarp();  // the previous row's reads of lat are done
+    for (int q = lane; q < d.n; q += kWarp) {
+      const double c = C[q];
+      lat[q] = isnan(c) ? kInf : c - ARR[q];
+    }
+    __syncwarp();
+    int kq[kQuantiles];
+#pragma unroll
+    for (int t = 0; t < kQuantiles; ++t) {
+      const double pq = kQuantileP[t];
+      int k = static_cast<int>(pq * d.n) - 2;
+      if (k < 0) k = 0;
+      while (static_cast<double>(k + 1) / static_cast<double>(d.n) < pq) ++k;
+      kq[t] = k;
+    }
+    unsigned hit[kQuantiles] = {0u, 0u, 0u};
+    double val[kQuantiles] = {0.0, 0.0, 0.0};
+    for (int q = lane; q < d.n; q += kWarp) {
+      const double x = lat[q];
+      int less = 0, le = 0;
+      for (int r = 0; r < d.n; ++r) {
+        const double y = lat[r];
+        less += y < x;
+        le += y <= x;
+      }
+#pragma unroll
+      for (int t = 0; t < kQuantiles; ++t)
+        if (x < kInf && less <= kq[t] && kq[t] < le) {
+          hit[t] = 1u;
+          val[t] = x;
+        }
+    }
+#pragma unroll
+    for (int t = 0; t < kQuantiles; ++t) {
+      const unsigned who = __ballot_sync(0xFFFFFFFFu, hit[t] != 0u);
+      if (who == 0u) {
+        if (lane == 0) R->latency_q[t] = nan("");
+      } else if (lane == __ffs(who) - 1) {
+        R->latency_q[t] = val[t];
+      }
+    }
+  }
   if (lane == 0) {
     R->goodput = static_cast<double>(met) / static_cast<double>(d.n);
     R->completed = comp;
@@ -1066,6 +1059,16 @@ __global__ void __launch_bounds__(128) row_metrics_warp_kernel(const RowMetricsP
     R->ratio_mean = mean;
     R->ratio_std = sqrt(var);
     R->cv = mean == 0.0 ? nan("") : R->ratio_std / mean;
+  }
+}
+
+__global__ void __launch_bounds__(128) row_metrics_warp_kernel(const RowMetricsParams p) {
+  __shared__ double lat_all[128 / kWarp][kMaxRequests];
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  for (int64_t i = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; i < p.n_traj;
+       i += warps) {  // uniform per warp
+    row_metrics_one(p, p.traj[i], lane, lat_all[threadIdx.x >> 5]);
   }
 }
 
@@ -1185,9 +1188,8 @@ int launch_tick_index(const WorkloadTables& wl, int64_t cells, const TickTable& 
 int launch_row_metrics(const RowMetricsParams& p, void* stream) {
   if (p.n_traj == 0) return 0;
   const int block = 128;
-  if (std::getenv("SABER_ROW_METRICS_THREAD")) {
-    const int grid = (p.n_traj + block - 1) / block;
-    row_metrics_kernel<<<grid, block, 0, static_cast<cudaStream_t>(stream)>>>(p);
+  if (p.narrow) {  // one warp per block, so a block fits beside the trajectory kernels
+    row_metrics_warp_kernel<<<296, kWarp, 0, static_cast<cudaStream_t>(stream)>>>(p);
   } else {
     const int64_t grid = (static_cast<int64_t>(p.n_traj) * kWarp + block - 1) / block;
     row_metrics_warp_kernel<<<static_cast<unsigned>(grid), block, 0,

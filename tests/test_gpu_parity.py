@@ -188,10 +188,11 @@ def test_pipelined_plans_match_synchronous(engine):
         i = k % 2
         if done[i] is not None:
             main.wait_event(done[i])
-        plans[i].launch(main.cuda_stream)
+        plans[i].launch_sim(main.cuda_stream)
         e = torch.cuda.Event()
         e.record(main)
         side.wait_event(e)
+        plans[i].metrics_launch(side.cuda_stream)  # narrow row metrics, as bench.py
         plans[i].summarize_launch(side.cuda_stream)
         d = torch.cuda.Event()
         d.record(side)
@@ -221,3 +222,32 @@ def test_draw_streams_grow_on_exhaustion(engine, monkeypatch):
     monkeypatch.setenv("SABER_DRAW_CAP", "16")
     b = S.sweep(grid, base)
     assert a.traj_rows.tobytes() == b.traj_rows.tobytes()
+
+
+def _quantiles_from_records(records):
+    """The reference's cdf (metrics.cpp:61-85) over all issued requests:
+    smallest latency x with (#latencies <= x) / issued >= p."""
+    issued = len(records)
+    lat = sorted(r.completion_time - r.arrival_time for r in records if not math.isnan(r.completion_time))
+    out = []
+    for p in (0.5, 0.9, 0.99):
+        got = float("nan")
+        for i, x in enumerate(lat):
+            if (i + 1) / issued >= p:
+                got = x
+                break
+        out.append(got)
+    return out
+
+
+def test_latency_percentiles_match_restatement(engine, orc):
+    cfgs = random_configs(160, seed=4242)
+    res = engine.run_batch(cfgs)
+    bad = []
+    for k, cfg in enumerate(cfgs):
+        o = orc.run(orc_config(cfg), records=True)
+        want = _quantiles_from_records(o.records)
+        got = list(res.rows[k]["latency_q"])
+        if not all(same_float(a, b) for a, b in zip(got, want)):
+            bad.append((k, got, want))
+    assert bad == []
