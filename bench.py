@@ -51,6 +51,69 @@ def env_int(k, d):
 
 
 # ------------------------------------------------------------------ clocks --
+class NvmlClockSampler:
+    """SM clock and clock-event reasons sampled through NVML every ~2 ms on a
+    background thread (the nvidia-smi loop below samples at ~10 Hz at best,
+    i.e. once or twice in a ~140 ms timed region)."""
+
+    def __init__(self, device):
+        import pynvml as nv
+        self.nv = nv
+        nv.nvmlInit()
+        self.h = nv.nvmlDeviceGetHandleByIndex(device)
+        self.max_mhz = nv.nvmlDeviceGetMaxClockInfo(self.h, nv.NVML_CLOCK_SM)
+        self.samples = []
+        self.skip = 0
+        self.run = False
+        self.thread = None
+
+    def _loop(self):
+        import time as _t
+        nv = self.nv
+        get_reasons = getattr(nv, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
+            nv.nvmlDeviceGetCurrentClocksThrottleReasons
+        while self.run:
+            try:
+                sm = nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM)
+                reasons = get_reasons(self.h)
+                util = nv.nvmlDeviceGetUtilizationRates(self.h).gpu
+                self.samples.append((sm, reasons, util))
+            except Exception:  # noqa: BLE001 (sampling is best effort)
+                pass
+            _t.sleep(0.002)
+
+    def start(self):
+        import threading
+        self.run = True
+        self.thread = threading.Thread(target=self._loop, daemon=True)
+        self.thread.start()
+
+    def mark(self):
+        self.skip = len(self.samples)
+
+    def stop(self):
+        self.run = False
+        if self.thread:
+            self.thread.join(timeout=5)
+        nv = self.nv
+        names = {"hw_slowdown": nv.nvmlClocksThrottleReasonHwSlowdown,
+                 "hw_thermal_slowdown": nv.nvmlClocksThrottleReasonHwThermalSlowdown,
+                 "sw_thermal_slowdown": nv.nvmlClocksThrottleReasonSwThermalSlowdown,
+                 "sw_power_cap": nv.nvmlClocksThrottleReasonSwPowerCap}
+        got = self.samples[self.skip:] or self.samples[-1:]
+        reasons = sorted({n for _, r, _ in got for n, bit in names.items() if r & bit})
+        sm = [c for c, _, _ in got]
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": self.max_mhz,
+                "reasons": reasons, "samples": len(got), "source": "NVML, ~2 ms period"}
+
+
+def make_clock_sampler(device):
+    try:
+        return NvmlClockSampler(device)
+    except Exception:  # noqa: BLE001 (no NVML: nvidia-smi loop)
+        return ClockSampler(device)
+
+
 class ClockSampler:
     QUERY = ("index,clocks.sm,clocks.max.sm,power.draw,utilization.gpu,"
              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
@@ -269,7 +332,7 @@ def engine_arm(args):
         step(k, sync=True)  # synchronous: every warm-up sweep is error-checked
     torch.cuda.synchronize()
 
-    clocks = ClockSampler(device)
+    clocks = make_clock_sampler(device)
     clocks.start()
     t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     if dist:
