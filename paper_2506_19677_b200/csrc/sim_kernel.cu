@@ -1003,20 +1003,34 @@ __device__ __forceinline__ void row_metrics_one(const RowMetricsParams& p, const
     }
     unsigned hit[kQuantiles] = {0u, 0u, 0u};
     double val[kQuantiles] = {0.0, 0.0, 0.0};
-    for (int q = lane; q < d.n; q += kWarp) {
-      const double x = lat[q];
-      int less = 0, le = 0;
+    // four of this lane's latencies ranked per pass over the row (one shared
+    // load serves four comparisons)
+    constexpr int kR = 4;
+    for (int q0 = lane; q0 < d.n; q0 += kR * kWarp) {
+      double x[kR];
+      int less[kR], le[kR];
+#pragma unroll
+      for (int u = 0; u < kR; ++u) {
+        const int q = q0 + u * kWarp;
+        x[u] = q < d.n ? lat[q] : kInf;
+        less[u] = le[u] = 0;
+      }
       for (int r = 0; r < d.n; ++r) {
         const double y = lat[r];
-        less += y < x;
-        le += y <= x;
+#pragma unroll
+        for (int u = 0; u < kR; ++u) {
+          less[u] += y < x[u];
+          le[u] += y <= x[u];
+        }
       }
 #pragma unroll
-      for (int t = 0; t < kQuantiles; ++t)
-        if (x < kInf && less <= kq[t] && kq[t] < le) {
-          hit[t] = 1u;
-          val[t] = x;
-        }
+      for (int u = 0; u < kR; ++u)
+#pragma unroll
+        for (int t = 0; t < kQuantiles; ++t)
+          if (x[u] < kInf && less[u] <= kq[t] && kq[t] < le[u]) {
+            hit[t] = 1u;
+            val[t] = x[u];
+          }
     }
 #pragma unroll
     for (int t = 0; t < kQuantiles; ++t) {
