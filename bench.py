@@ -385,7 +385,31 @@ def engine_arm(args):
             h2d, d2h = out
         e2e_value = total_rows * len(e2e_times) / sum(e2e_times)
     else:
-        e2e_value = None
+        # N > 1 through the staged public API: per step and
+        # rank, plan create (host prologue + H2D), run, NCCL gather, summary,
+        # D2H of every row and the summary; wall clock, max over ranks.
+        for k in range(args.warmup + args.steps):
+            torch.cuda.synchronize()
+            dist.barrier()
+            t0 = time.perf_counter()
+            pl = S.SweepPlan(grid, base, device=device, shard_index=rank, shard_count=world)
+            pl.run(stream.cuda_stream)
+            b = pl.buffers()
+            rt = torch.as_tensor(_CudaView(b.rows, b.rows_bytes), device=f"cuda:{device}")
+            ct = torch.as_tensor(_CudaView(b.completion_times, b.completion_bytes), device=f"cuda:{device}")
+            dist.all_reduce(rt)
+            dist.all_reduce(ct)
+            pl.summarize(stream.cuda_stream)
+            pl.fetch(completion=False, summary=True)
+            torch.cuda.synchronize()
+            dt = time.perf_counter() - t0
+            if k >= args.warmup:
+                e2e_times.append(dt)
+            h2d, d2h = pl.last_h2d_bytes, pl.last_d2h_bytes
+            pl.close()
+        t = torch.tensor([sum(e2e_times)], dtype=torch.float64, device=device)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_value = total_rows * len(e2e_times) / float(t.item())
 
     peak = S.fp64_peak_tflops(device)
     achieved = fp64_ops / (sim_avg_ms / 1e3) / 1e12

@@ -530,6 +530,7 @@ class SweepPlan:
             o.summary = summ
             o.best_cap_by_rps = best.ctypes.data_as(C.POINTER(C.c_int32))
         _check(N.lib().saber_cuda_sweep_plan_fetch(self.handle, C.byref(o)))
+        self.last_h2d_bytes, self.last_d2h_bytes = int(o.h2d_bytes), int(o.d2h_bytes)
         return rows, comp, summ, best
 
     def close(self):
