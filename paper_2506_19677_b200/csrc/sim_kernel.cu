@@ -120,7 +120,9 @@ __global__ void tick_index_kernel(const WorkloadTables wl, int64_t cells, const 
 // which is that same value.  The caller has proved that no pass of the streak
 // ends a prefill, binds the decode boundary or completes a slot.  Returns the
 // exact prefill minimum after the streak (the per-pass chain min_pf -= dt).
-template <int G, int kC>
+// kDec: no slot is in prefill (npre == 0, uniform), so every slot adds the
+// same fl(speed * dt) and the product is formed once per tick, not per slot.
+template <int G, int kC, bool kDec>
 __device__ __forceinline__ double streak_chunks(const Slots<G>& S, int sub, int A, double speed,
                                                const double* __restrict__ DT, int K, double pf) {
   // Chunk 0 runs on every lane of the group (it also carries the replicated
@@ -137,21 +139,27 @@ __device__ __forceinline__ double streak_chunks(const Slots<G>& S, int sub, int 
 #pragma unroll 1
     for (; j + 4 <= K; j += 4) {
       const double d0 = DT[j], d1 = DT[j + 1], d2 = DT[j + 2], d3 = DT[j + 3];
+      if (kDec) {
+        const double s0 = speed * d0, s1 = speed * d1, s2 = speed * d2, s3 = speed * d3;
 #pragma unroll
-      for (int i = 0; i < kC; ++i) {
-        g[i] = g[i] + mult[i] * d0;
-        g[i] = g[i] + mult[i] * d1;
-        g[i] = g[i] + mult[i] * d2;
-        g[i] = g[i] + mult[i] * d3;
+        for (int i = 0; i < kC; ++i) g[i] = (((g[i] + s0) + s1) + s2) + s3;
+      } else {
+#pragma unroll
+        for (int i = 0; i < kC; ++i) {
+          g[i] = g[i] + mult[i] * d0;
+          g[i] = g[i] + mult[i] * d1;
+          g[i] = g[i] + mult[i] * d2;
+          g[i] = g[i] + mult[i] * d3;
+        }
+        if (first) pf = (((pf - d0) - d1) - d2) - d3;
       }
-      if (first) pf = (((pf - d0) - d1) - d2) - d3;
     }
 #pragma unroll 1
     for (; j < K; ++j) {
       const double d0 = DT[j];
 #pragma unroll
-      for (int i = 0; i < kC; ++i) g[i] = g[i] + mult[i] * d0;
-      if (first) pf = pf - d0;
+      for (int i = 0; i < kC; ++i) g[i] = g[i] + mult[i] * d0;  // mult == speed when kDec
+      if (!kDec && first) pf = pf - d0;
     }
 #pragma unroll
     for (int i = 0; i < kC; ++i) {
@@ -163,11 +171,16 @@ __device__ __forceinline__ double streak_chunks(const Slots<G>& S, int sub, int 
 }
 
 template <int G>
-__device__ __forceinline__ double streak_slots(const Slots<G>& S, int sub, int A, double speed,
-                                               const double* __restrict__ DT, int K, double pf) {
-  if (A <= G) return streak_chunks<G, 1>(S, sub, A, speed, DT, K, pf);
-  if (A <= 2 * G) return streak_chunks<G, 2>(S, sub, A, speed, DT, K, pf);
-  return streak_chunks<G, 4>(S, sub, A, speed, DT, K, pf);
+__device__ __forceinline__ double streak_slots(const Slots<G>& S, int sub, int A, int npre,
+                                               double speed, const double* __restrict__ DT, int K,
+                                               double pf) {
+  if (A <= G) return streak_chunks<G, 1, false>(S, sub, A, speed, DT, K, pf);
+  if (npre == 0) {  // min_pf is +inf and stays so
+    if (A <= 2 * G) return streak_chunks<G, 2, true>(S, sub, A, speed, DT, K, pf);
+    return streak_chunks<G, 4, true>(S, sub, A, speed, DT, K, pf);
+  }
+  if (A <= 2 * G) return streak_chunks<G, 2, false>(S, sub, A, speed, DT, K, pf);
+  return streak_chunks<G, 4, false>(S, sub, A, speed, DT, K, pf);
 }
 
 // Gate streak decisions: ticks k0+1 .. k0+K-1 of a streak
@@ -638,7 +651,7 @@ __device__ __forceinline__ void simulate_one(const SimParams& P, int ti, const S
           // min_pf stays exact: the same per-pass chain min_pf -= dt
           {
             SEC_BEGIN();
-            min_pf = streak_slots<G>(S, sub, A, speed_A, DTk, K, min_pf);
+            min_pf = streak_slots<G>(S, sub, A, npre, speed_A, DTk, K, min_pf);
             SEC_END(1);
           }
           if (A > npre) rem_lb = rem_lb - static_cast<double>(K) * delta;
