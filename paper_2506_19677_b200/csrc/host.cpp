@@ -712,10 +712,19 @@ saber_status saber_cuda_sweep_plan_create(const saber_sweep_desc* desc, saber_sw
             distinct.begin());
     std::vector<int32_t> bucket(static_cast<size_t>(P->rows_shard));
     std::vector<int64_t> start(distinct.size() + 1, 0);
+    // walk row r = shard_index + k * shard_count incrementally (no divisions):
+    // rem = r % per_rps, ri = (r / per_rps) % n_rps
+    int64_t rem = desc->shard_index % per_rps;
+    int ri = static_cast<int>((desc->shard_index / per_rps) % n_rps);
     for (int64_t k = 0; k < P->rows_shard; ++k) {
-      const int64_t r = desc->shard_index + k * desc->shard_count;
-      const int ri = static_cast<int>((r / per_rps) % n_rps);
-      const bool sab = (r % per_rps) >= desc->n_caps * R;
+      if (k > 0) {
+        rem += desc->shard_count;
+        while (rem >= per_rps) {
+          rem -= per_rps;
+          if (++ri == n_rps) ri = 0;
+        }
+      }
+      const bool sab = rem >= static_cast<int64_t>(desc->n_caps) * R;
       const int32_t bk = bucket_of[static_cast<size_t>(2 * ri + (sab ? 1 : 0))];
       bucket[static_cast<size_t>(k)] = bk;
       ++start[static_cast<size_t>(bk) + 1];
