@@ -251,3 +251,28 @@ def test_latency_percentiles_match_restatement(engine, orc):
         if not all(same_float(a, b) for a, b in zip(got, want)):
             bad.append((k, got, want))
     assert bad == []
+
+
+@pytest.mark.parametrize("n", [200, 512])
+def test_large_trajectories_match_restatement(engine, orc, n):
+    """n up to the engine's limit (512): 4/8-word tier masks, multi-chunk
+    streak sweeps (more slots than 4 per lane), long demotion scans."""
+    import random
+    rng = random.Random(n)
+    cfgs = []
+    for i in range(24):
+        cfgs.append(sim_config(mix=rng.choice(["w1", "w2", "w3"]), rps=rng.choice([2.0, 8.0, 20.0, 40.0]),
+                               n=n, seed=rng.randrange(1 << 40), mode=rng.choice([0, 1]),
+                               cap=rng.choice([50, 200, 512]), window=rng.choice([3, 8, 16])))
+    res = engine.run_batch(cfgs)
+    bad = []
+    for k, cfg in enumerate(cfgs):
+        o = orc.run(orc_config(cfg), records=True)
+        errs = compare_row(res.rows[k], o.out)
+        for i, rec in enumerate(o.records):
+            if not same_float(res.completion_times[k, i], rec.completion_time):
+                errs.append(f"completion[{i}]")
+                break
+        if errs:
+            bad.append((k, errs[:4]))
+    assert bad == []
