@@ -20,6 +20,8 @@
  *   saber_cuda_profile_batch  <- profile(const EngineConfig&, const WorkloadSpec&, int l_max)
  *                                 calibration.hpp:29-31, calibration.cpp:58-135 (batched)
  *   saber_cuda_predict_table  <- double predict(const SpeedModel&, int)       estimator.hpp:39
+ *   saber_cuda_generate       <- std::vector<Request> generate(const WorkloadSpec&)
+ *                                 workload.hpp:31, workload.cpp:52-79 (batched)
  *
  * Conventions: plain C, POD structs, caller-owned memory, no exceptions.  Every
  * function returns a saber_status; on failure saber_cuda_last_error() holds a
@@ -41,7 +43,7 @@
 extern "C" {
 #endif
 
-#define SABER_CUDA_ABI_VERSION 1
+#define SABER_CUDA_ABI_VERSION 2
 
 typedef enum {
   SABER_OK = 0,
@@ -50,7 +52,11 @@ typedef enum {
   SABER_EFIT = 3,
   SABER_ECUDA = 4,
   SABER_ECAPACITY = 5, /* a caller-sized buffer (e.g. decision trace) is too small */
-  SABER_EINTERNAL = 6  /* an invariant the reference would throw logic_error on */
+  SABER_EINTERNAL = 6, /* an invariant the reference would throw logic_error on */
+  SABER_ERETRY = 7     /* recoverable: a sweep plan grew its scheduler draw streams
+                          (a trajectory exhausted one); the launched results are
+                          void — launch the plan again (saber_cuda_sweep_plan_run
+                          does this itself) */
 } saber_status;
 
 /* Task catalog (types.cpp:10-18), in catalog order. */
@@ -60,6 +66,9 @@ enum { SABER_TASK_QNA = 0, SABER_TASK_GENERATION = 1, SABER_TASK_SUMMARY = 2,
 enum { SABER_USL = 0, SABER_LOGISTIC = 1, SABER_LINEAR = 2 };
 /* SchedulerMode (types.hpp:76). */
 enum { SABER_MODE_SABER = 0, SABER_MODE_STATIC = 1 };
+/* RequestState (types.hpp:43). */
+enum { SABER_STATE_QUEUED_HIGH = 0, SABER_STATE_QUEUED_LOW = 1, SABER_STATE_EXECUTING = 2,
+       SABER_STATE_COMPLETED = 3 };
 /* DecisionKind (scheduler.hpp:46). */
 enum { SABER_ADMIT_HIGH = 0, SABER_ADMIT_LOW = 1, SABER_REJECT_OWN = 2,
        SABER_REJECT_ACTIVE = 3, SABER_DEMOTE = 4 };
@@ -217,6 +226,7 @@ saber_status saber_cuda_sweep_plan_fetch(saber_sweep_plan* plan, saber_sweep_out
 /* CUDA-event time and launches of the last plan_run (+ summarize). */
 saber_status saber_cuda_sweep_plan_stats(saber_sweep_plan* plan, double* device_ms,
                                          double* sim_kernel_ms, int32_t* launches);
+/* Waits for every piece of work the plan enqueued, then frees it. */
 void saber_cuda_sweep_plan_destroy(saber_sweep_plan* plan);
 
 /* --------------------------------------------------------------------------
@@ -224,6 +234,7 @@ void saber_cuda_sweep_plan_destroy(saber_sweep_plan* plan);
  * generated (generate(): WorkloadSpec + its seed) or replayed from explicit
  * requests (ids 0..n-1 in arrival order).
  * -------------------------------------------------------------------------- */
+/* The static fields of a Request (types.hpp:45-59); its id is its index. */
 typedef struct {
   double arrival_time;
   double sla_seconds;
@@ -231,8 +242,26 @@ typedef struct {
   int32_t input_tokens;
   int32_t max_output_tokens;
   int32_t task;            /* SABER_TASK_* (CUSTOM for non-catalog names) */
-  int32_t pad_;
+  int32_t group;           /* task group of the per-task metrics (MetricsReport::per_task,
+                              a std::map keyed by task name): requests with equal group
+                              share one CDF, groups ordered by value.  The engine numbers
+                              the catalog tasks by name rank (code_generation 0, code_qna 1,
+                              code_summary 2, code_translation 3); a replay caller numbers
+                              its task names in the same (sorted) order. */
 } saber_request;
+
+/* A request's mutable state at the end of a run (Request, types.hpp:45-59) and
+ * its RunRecord fields (make_record, metrics.cpp:17-30). */
+typedef struct {
+  double admit_time;               /* NaN = never admitted */
+  double completion_time;          /* NaN = never completed */
+  double generated_tokens;         /* fluid progress (max_output_tokens once completed) */
+  double recorded_required_speed;  /* required_speed at admission; NaN = never admitted */
+  int32_t state;                   /* SABER_STATE_* */
+  int32_t met_sla;                 /* completed and completion - arrival <= sla */
+  int32_t demoted;                 /* ever in the low tier (final_tier "low") */
+  int32_t pad_;
+} saber_request_state;
 
 typedef struct {
   /* WorkloadSpec (workload.hpp:15-21); ignored when `requests` is set */
@@ -279,9 +308,39 @@ typedef struct {
   int64_t* n_decisions;
   double device_ms;
   int32_t kernel_launches;
+  /* --- ABI 2: the full RunOutput (simloop.hpp:37-43) from the engine, each
+   * optional, row stride max_n (group counts: max_groups) --- */
+  saber_request* requests;         /* the workload: generate() output or the replay */
+  saber_request_state* states;     /* final request states + records */
+  /* Per task group g (saber_request::group) of trajectory k, the latency CDF
+   * of cdf() (metrics.cpp:61-85): the group's issued requests occupy positions
+   * [start_g, start_g + issued_g) of row k, start_g = #requests of smaller
+   * groups; the group's CDF points are the positions whose fraction is not
+   * NaN, in ascending latency order. */
+  double* cdf_latency;
+  double* cdf_fraction;
+  int32_t* group_issued;           /* [n_traj][max_groups]: TaskMetrics::issued */
+  int32_t* group_met;              /* [n_traj][max_groups]: met_sla count (goodput = met / issued) */
+  int32_t max_groups;              /* >= 4 when any trajectory is generated; > every replay group */
 } saber_run_batch_out;
 
 saber_status saber_cuda_run_batch(const saber_run_batch_desc* desc, saber_run_batch_out* out);
+
+/* --------------------------------------------------------------------------
+ * Workload generation <- std::vector<Request> generate(const WorkloadSpec&)
+ *   workload.hpp:31, workload.cpp:52-79.  Spec k's requests land at
+ *   out + k * max_n (num_requests entries); bit-identical to the reference.
+ * -------------------------------------------------------------------------- */
+typedef struct {
+  saber_mix mix;
+  double rps;
+  int32_t num_requests;
+  uint64_t seed;
+  double length_jitter;
+} saber_workload_spec;
+
+saber_status saber_cuda_generate(const saber_workload_spec* specs, int32_t n_specs, int32_t device,
+                                 saber_request* out, int32_t max_n);
 
 /* --------------------------------------------------------------------------
  * Monte-Carlo sweep with bursty arrivals (BASELINE config 5; no reference
@@ -416,6 +475,9 @@ saber_status saber_cuda_predict_table(const saber_model* model, int32_t max_load
  * Misc.
  * -------------------------------------------------------------------------- */
 const char* saber_cuda_last_error(void);
+/* Device blocks freed by finished calls are cached for reuse; this returns
+ * the cached blocks of `device` to the driver. */
+saber_status saber_cuda_release_cache(int32_t device);
 int32_t saber_cuda_abi_version(void);
 /* Number of usable sm_100 devices (0 on a CPU-only host). */
 int32_t saber_cuda_device_count(void);

@@ -8,11 +8,17 @@
 //     saber::sweep(grid, base, jobs)   ->  saber::cuda::sweep(grid, base, jobs)
 //     saber::run(cfg)                  ->  saber::cuda::run(cfg)
 //     saber::run_with_requests(cfg, r) ->  saber::cuda::run_with_requests(cfg, r)
+//     saber::generate(spec)            ->  saber::cuda::generate(spec)
+//     saber::fit / calibrate / profile ->  saber::cuda::fit / calibrate / profile
 //
+// Every value these functions return comes from the engine; the header only
+// converts between the reference's types and the C ABI's structs (it calls no
+// reference function).
 // Only this header depends on the reference; the engine itself (the C ABI in
 // saber_cuda.h) does not.
 #pragma once
 
+#include <algorithm>
 #include <cmath>
 #include <cstring>
 #include <map>
@@ -35,6 +41,7 @@ namespace saber::cuda {
 namespace detail {
 
 inline const char* kTask[4] = {"code_qna", "code_generation", "code_summary", "code_translation"};
+inline const char* kFamily[3] = {"usl", "logistic", "linear"};  // ModelFamily names
 
 inline int task_index(const std::string& name) {
   for (int t = 0; t < 4; ++t)
@@ -92,11 +99,45 @@ inline saber_traj_spec spec_of(const SimConfig& c) {
   return s;
 }
 
-inline RunOutput run_one(const SimConfig& cfg, std::vector<Request> requests, bool replay) {
+inline const std::string& task_name(int32_t t) {
+  static const std::string custom = "custom";
+  static const std::string names[4] = {kTask[0], kTask[1], kTask[2], kTask[3]};
+  return t >= 0 && t < 4 ? names[t] : custom;
+}
+
+inline RequestState state_of(int32_t s) {
+  switch (s) {
+    case SABER_STATE_QUEUED_LOW: return RequestState::QueuedLow;
+    case SABER_STATE_EXECUTING: return RequestState::Executing;
+    case SABER_STATE_COMPLETED: return RequestState::Completed;
+    default: return RequestState::QueuedHigh;
+  }
+}
+
+inline std::optional<double> opt(double v) {
+  if (std::isnan(v)) return std::nullopt;
+  return v;
+}
+
+// One trajectory through saber_cuda_run_batch; every field of the RunOutput
+// (requests, records, decisions, metrics) is read off the engine's outputs.
+// The engine's event trace (Engine::trace) is not produced.
+inline RunOutput run_one(const SimConfig& cfg, std::vector<Request> requests, bool replay,
+                         int device) {
   saber_traj_spec spec = spec_of(cfg);
   std::vector<saber_request> rq;
+  std::vector<std::string> group_name(kTask, kTask + 4);  // generated: name rank
+  std::sort(group_name.begin(), group_name.end());
   if (replay) {
     if (requests.empty()) throw std::invalid_argument("run: no requests");
+    // per-task metrics group by task name, in name order (std::map)
+    std::map<std::string, int32_t> rank;
+    for (const Request& r : requests) rank.emplace(r.task, 0);
+    group_name.clear();
+    for (auto& kv : rank) {
+      kv.second = static_cast<int32_t>(group_name.size());
+      group_name.push_back(kv.first);
+    }
     rq.resize(requests.size());
     for (size_t i = 0; i < requests.size(); ++i) {
       if (requests[i].id != i) throw std::invalid_argument("run: request ids must be 0..n-1");
@@ -106,46 +147,77 @@ inline RunOutput run_one(const SimConfig& cfg, std::vector<Request> requests, bo
       rq[i].input_tokens = requests[i].input_tokens;
       rq[i].max_output_tokens = requests[i].max_output_tokens;
       rq[i].task = task_index(requests[i].task);
+      rq[i].group = rank[requests[i].task];
     }
     spec.requests = rq.data();
     spec.num_requests = static_cast<int32_t>(rq.size());
-  } else {
-    requests = generate(cfg.workload);  // reference generator, for the Request records
   }
-  const int n = static_cast<int>(requests.size());
-  saber_run_batch_desc d{&spec, 1, 0};
+  const int n = spec.num_requests;
+  if (n < 1) throw std::invalid_argument("num_requests must be >= 1");
+  const int groups = std::max<int>(4, static_cast<int>(group_name.size()));
+  saber_run_batch_desc d{&spec, 1, device};
   saber_traj_row row{};
-  std::vector<double> arr(n), adm(n), comp(n);
-  std::vector<uint8_t> dem(n);
-  const int64_t cap = 1 << 22;
-  std::vector<saber_decision> decs(static_cast<size_t>(cap));
-  int64_t n_dec = 0;
-  saber_run_batch_out o{};
-  o.rows = &row;
-  o.arrival_times = arr.data();
-  o.admit_times = adm.data();
-  o.completion_times = comp.data();
-  o.demoted = dem.data();
-  o.max_n = n;
-  o.decisions = decs.data();
-  o.decision_cap = cap;
-  o.n_decisions = &n_dec;
-  check(saber_cuda_run_batch(&d, &o));
+  std::vector<saber_request> req(static_cast<size_t>(n));
+  std::vector<saber_request_state> st(static_cast<size_t>(n));
+  std::vector<double> cdf_l(static_cast<size_t>(n)), cdf_f(static_cast<size_t>(n));
+  std::vector<int32_t> g_issued(static_cast<size_t>(groups)), g_met(static_cast<size_t>(groups));
+  int64_t cap = 1 << 16, n_dec = 0;
+  std::vector<saber_decision> decs;
+  for (;;) {  // grow the decision buffer to the trajectory's count when it overflows
+    decs.resize(static_cast<size_t>(cap));
+    saber_run_batch_out o{};
+    o.rows = &row;
+    o.max_n = n;
+    o.decisions = decs.data();
+    o.decision_cap = cap;
+    o.n_decisions = &n_dec;
+    o.requests = req.data();
+    o.states = st.data();
+    o.cdf_latency = cdf_l.data();
+    o.cdf_fraction = cdf_f.data();
+    o.group_issued = g_issued.data();
+    o.group_met = g_met.data();
+    o.max_groups = groups;
+    const saber_status s = saber_cuda_run_batch(&d, &o);
+    if (s == SABER_ECAPACITY && row.decisions > cap) {
+      cap = row.decisions;
+      continue;
+    }
+    check(s);
+    break;
+  }
   RunOutput out;
+  if (!replay) requests.resize(static_cast<size_t>(n));
+  out.records.reserve(static_cast<size_t>(n));
   for (int i = 0; i < n; ++i) {
     Request& r = requests[static_cast<size_t>(i)];
-    if (!std::isnan(adm[i])) r.admit_time = adm[i];
-    if (!std::isnan(comp[i])) {
-      r.completion_time = comp[i];
-      r.generated_tokens = r.max_output_tokens;
-      r.state = RequestState::Completed;
-    } else if (!std::isnan(adm[i])) {
-      r.state = RequestState::Executing;
-    } else {
-      r.state = dem[i] ? RequestState::QueuedLow : RequestState::QueuedHigh;
+    const saber_request& q = req[static_cast<size_t>(i)];
+    const saber_request_state& x = st[static_cast<size_t>(i)];
+    if (!replay) {  // the generated workload (generate(), workload.cpp:52-79)
+      r.id = static_cast<std::uint64_t>(i);
+      r.task = task_name(q.task);
+      r.arrival_time = q.arrival_time;
+      r.input_tokens = q.input_tokens;
+      r.max_output_tokens = q.max_output_tokens;
+      r.sla_seconds = q.sla_seconds;
+      r.deadline = q.deadline;
     }
-    r.demoted = dem[i] != 0;
-    out.records.push_back(make_record(r));
+    r.generated_tokens = x.generated_tokens;
+    r.state = state_of(x.state);
+    r.admit_time = opt(x.admit_time);
+    r.completion_time = opt(x.completion_time);
+    r.recorded_required_speed = opt(x.recorded_required_speed);
+    r.demoted = x.demoted != 0;
+    RunRecord rec;
+    rec.request_id = r.id;
+    rec.task = r.task;
+    rec.arrival_time = r.arrival_time;
+    rec.admit_time = r.admit_time;
+    rec.completion_time = r.completion_time;
+    rec.sla = r.sla_seconds;
+    rec.met_sla = x.met_sla != 0;
+    rec.final_tier = x.demoted ? "low" : "high";
+    out.records.push_back(std::move(rec));
   }
   for (int64_t k = 0; k < n_dec; ++k) {
     const saber_decision& x = decs[static_cast<size_t>(k)];
@@ -158,7 +230,25 @@ inline RunOutput run_one(const SimConfig& cfg, std::vector<Request> requests, bo
     if (x.has_req) dd.req_speed = x.req_speed;
     out.decisions.push_back(dd);
   }
-  out.metrics = compute_metrics(out.records);
+  // MetricsReport: the row's scalars and, per task group, the engine's
+  // issued / met counts and CDF points.
+  out.metrics.goodput = row.goodput;
+  out.metrics.ratio_mean = row.ratio_mean;
+  out.metrics.ratio_std = row.ratio_std;
+  out.metrics.cv = row.cv;
+  int start = 0;
+  for (int g = 0; g < static_cast<int>(group_name.size()); ++g) {
+    const int issued = g_issued[static_cast<size_t>(g)];
+    if (issued == 0) continue;
+    TaskMetrics tm;
+    tm.issued = issued;
+    tm.goodput = static_cast<double>(g_met[static_cast<size_t>(g)]) / static_cast<double>(issued);
+    for (int p = start; p < start + issued; ++p)
+      if (!std::isnan(cdf_f[static_cast<size_t>(p)]))
+        tm.cdf_points.emplace_back(cdf_l[static_cast<size_t>(p)], cdf_f[static_cast<size_t>(p)]);
+    out.metrics.per_task[group_name[static_cast<size_t>(g)]] = std::move(tm);
+    start += issued;
+  }
   out.requests = std::move(requests);
   return out;
 }
@@ -166,11 +256,39 @@ inline RunOutput run_one(const SimConfig& cfg, std::vector<Request> requests, bo
 }  // namespace detail
 
 // simloop.hpp:49
-inline RunOutput run(const SimConfig& config) { return detail::run_one(config, {}, false); }
+inline RunOutput run(const SimConfig& config, int device = 0) {
+  return detail::run_one(config, {}, false, device);
+}
 
 // simloop.hpp:53-54
-inline RunOutput run_with_requests(const SimConfig& config, std::vector<Request> requests) {
-  return detail::run_one(config, std::move(requests), true);
+inline RunOutput run_with_requests(const SimConfig& config, std::vector<Request> requests,
+                                   int device = 0) {
+  return detail::run_one(config, std::move(requests), true, device);
+}
+
+// workload.hpp:31
+inline std::vector<Request> generate(const WorkloadSpec& spec, int device = 0) {
+  saber_workload_spec w{};
+  w.mix = detail::mix_of(spec.mix);
+  w.rps = spec.rps;
+  w.num_requests = spec.num_requests;
+  w.seed = spec.seed;
+  w.length_jitter = spec.length_jitter;
+  if (w.num_requests < 1) throw std::invalid_argument("num_requests must be >= 1");
+  std::vector<saber_request> q(static_cast<size_t>(w.num_requests));
+  detail::check(saber_cuda_generate(&w, 1, device, q.data(), w.num_requests));
+  std::vector<Request> out(q.size());
+  for (size_t i = 0; i < q.size(); ++i) {
+    Request& r = out[i];
+    r.id = i;
+    r.task = detail::task_name(q[i].task);
+    r.arrival_time = q[i].arrival_time;
+    r.input_tokens = q[i].input_tokens;
+    r.max_output_tokens = q[i].max_output_tokens;
+    r.sla_seconds = q[i].sla_seconds;
+    r.deadline = q[i].deadline;
+  }
+  return out;
 }
 
 // simloop.hpp:96-99.  `jobs` is accepted for signature parity; the device
@@ -279,7 +397,7 @@ inline SpeedModel fit(const std::vector<LoadSpeedSample>& samples, ModelFamily f
   detail::check(saber_cuda_fit_batch(&d, &o));
   const std::array<double, 3> p = {params[3 * f], params[3 * f + 1], params[3 * f + 2]};
   if (status[f] != 0)
-    throw FitError(std::string("fit failed for ") + to_string(family), family, p, r2[f]);
+    throw FitError(std::string("fit failed for ") + detail::kFamily[f], family, p, r2[f]);
   SpeedModel m;
   m.family = family;
   m.params = p;
@@ -317,7 +435,7 @@ inline CalibrationReport calibrate(const std::vector<LoadSpeedSample>& samples, 
       e.model.params = {params[3 * f], params[3 * f + 1], params[3 * f + 2]};
       e.model.fit_r2 = r2[f];
     } else {
-      e.error = std::string("fit failed for ") + to_string(e.family);
+      e.error = std::string("fit failed for ") + detail::kFamily[f];
     }
     rep.fits.push_back(e);
   }

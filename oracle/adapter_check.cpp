@@ -9,6 +9,7 @@
 // Built by oracle/Makefile into oracle/_ref/adapter_check (it links the
 // compiled reference); tests/test_adapter.py runs it.
 #include <cmath>
+#include <optional>
 #include <cstdio>
 #include <cstring>
 #include <exception>
@@ -34,7 +35,33 @@ saber::SpeedModel calibrated_usl() {
           {99.999999999997357, 0.049999999999992085, 0.0010000000000001078}, {}};
 }
 
+bool same_opt(const std::optional<double>& a, const std::optional<double>& b) {
+  return a.has_value() == b.has_value() && (!a || same(*a, *b));
+}
+
+void compare_requests(const std::vector<saber::Request>& a, const std::vector<saber::Request>& b,
+                      const std::string& tag) {
+  expect(a.size() == b.size(), tag + " request count");
+  for (size_t i = 0; i < a.size() && i < b.size(); ++i) {
+    const auto& x = a[i];
+    const auto& y = b[i];
+    const bool ok = x.id == y.id && x.task == y.task && same(x.arrival_time, y.arrival_time) &&
+                    x.input_tokens == y.input_tokens && x.max_output_tokens == y.max_output_tokens &&
+                    same(x.sla_seconds, y.sla_seconds) && same(x.deadline, y.deadline) &&
+                    same(x.generated_tokens, y.generated_tokens) && x.state == y.state &&
+                    same_opt(x.admit_time, y.admit_time) &&
+                    same_opt(x.completion_time, y.completion_time) &&
+                    same_opt(x.recorded_required_speed, y.recorded_required_speed) &&
+                    x.demoted == y.demoted;
+    if (!ok) {
+      expect(false, tag + " request " + std::to_string(i));
+      break;
+    }
+  }
+}
+
 void compare_runs(const saber::RunOutput& a, const saber::RunOutput& b, const std::string& tag) {
+  compare_requests(a.requests, b.requests, tag);
   expect(a.decisions.size() == b.decisions.size(), tag + " decision count");
   for (size_t i = 0; i < a.decisions.size() && i < b.decisions.size(); ++i) {
     const auto& x = a.decisions[i];
@@ -76,8 +103,38 @@ int main() {
     st.workload.rps = 8.0;
     compare_runs(saber::run(st), saber::cuda::run(st), "static");
     auto reqs = saber::generate(cfg.workload);
+    compare_requests(reqs, saber::cuda::generate(cfg.workload), "generate");
     compare_runs(saber::run_with_requests(cfg, reqs), saber::cuda::run_with_requests(cfg, reqs),
                  "replay");
+    // Horizon cut mid-run: executing requests keep their fluid progress,
+    // queued ones stay queued (some demoted) — every Request field compared.
+    saber::SimConfig cut = cfg;
+    cut.workload.rps = 30.0;
+    cut.workload.num_requests = 200;
+    cut.horizon = 4.0;
+    compare_runs(saber::run(cut), saber::cuda::run(cut), "horizon");
+    saber::SimConfig cut_st = st;
+    cut_st.horizon = 3.3;
+    cut_st.engine.prefill_rate = 400.0;  // slots caught in prefill
+    compare_runs(saber::run(cut_st), saber::cuda::run(cut_st), "horizon static");
+    // Replay with task names outside the catalog (the per-task metrics are
+    // keyed by name) and a heavy rate.
+    auto custom = saber::generate(cut.workload);
+    for (size_t i = 0; i < custom.size(); i += 3) custom[i].task = i % 2 ? "alpha" : "zeta";
+    compare_runs(saber::run_with_requests(cfg, custom),
+                 saber::cuda::run_with_requests(cfg, custom), "custom tasks");
+    // generate() across mixes, rates, sizes and jitters
+    for (const char* mx : {"w1", "w2", "w3"})
+      for (double rps : {0.5, 7.0, 1e6}) {
+        saber::WorkloadSpec w;
+        w.mix = saber::preset_mix(mx);
+        w.rps = rps;
+        w.num_requests = 333;
+        w.seed = 1234567;
+        w.length_jitter = rps > 1.0 ? 0.0 : 0.6;
+        compare_requests(saber::generate(w), saber::cuda::generate(w),
+                         std::string("generate ") + mx);
+      }
 
     // A config-2 shaped sweep.
     saber::SweepGrid grid;

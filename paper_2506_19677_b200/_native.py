@@ -13,9 +13,11 @@ import os
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("SABER_LIB", os.path.join(HERE, "libsaber_b200.so"))
 
-SABER_OK, SABER_EINVAL, SABER_EDOMAIN, SABER_EFIT, SABER_ECUDA, SABER_ECAPACITY, SABER_EINTERNAL = range(7)
+(SABER_OK, SABER_EINVAL, SABER_EDOMAIN, SABER_EFIT, SABER_ECUDA, SABER_ECAPACITY, SABER_EINTERNAL,
+ SABER_ERETRY) = range(8)
 STATUS_NAMES = ["SABER_OK", "SABER_EINVAL", "SABER_EDOMAIN", "SABER_EFIT", "SABER_ECUDA",
-                "SABER_ECAPACITY", "SABER_EINTERNAL"]
+                "SABER_ECAPACITY", "SABER_EINTERNAL", "SABER_ERETRY"]
+ABI_VERSION = 2
 
 
 class saber_model(C.Structure):
@@ -86,7 +88,19 @@ class saber_sweep_buffers(C.Structure):
 class saber_request(C.Structure):
     _fields_ = [("arrival_time", C.c_double), ("sla_seconds", C.c_double), ("deadline", C.c_double),
                 ("input_tokens", C.c_int32), ("max_output_tokens", C.c_int32), ("task", C.c_int32),
+                ("group", C.c_int32)]
+
+
+class saber_request_state(C.Structure):
+    _fields_ = [("admit_time", C.c_double), ("completion_time", C.c_double),
+                ("generated_tokens", C.c_double), ("recorded_required_speed", C.c_double),
+                ("state", C.c_int32), ("met_sla", C.c_int32), ("demoted", C.c_int32),
                 ("pad_", C.c_int32)]
+
+
+class saber_workload_spec(C.Structure):
+    _fields_ = [("mix", saber_mix), ("rps", C.c_double), ("num_requests", C.c_int32),
+                ("seed", C.c_uint64), ("length_jitter", C.c_double)]
 
 
 class saber_traj_spec(C.Structure):
@@ -115,6 +129,10 @@ class saber_run_batch_out(C.Structure):
         ("decisions", C.POINTER(saber_decision)), ("decision_cap", C.c_int64),
         ("n_decisions", C.POINTER(C.c_int64)),
         ("device_ms", C.c_double), ("kernel_launches", C.c_int32),
+        ("requests", C.POINTER(saber_request)), ("states", C.POINTER(saber_request_state)),
+        ("cdf_latency", C.POINTER(C.c_double)), ("cdf_fraction", C.POINTER(C.c_double)),
+        ("group_issued", C.POINTER(C.c_int32)), ("group_met", C.POINTER(C.c_int32)),
+        ("max_groups", C.c_int32),
     ]
 
 
@@ -203,6 +221,9 @@ SYMBOLS = [
     ("saber_cuda_mc_trace", C.c_int, [_P(saber_mc_desc), C.c_int64, _P(saber_request),
                                       _P(saber_traj_spec)]),
     ("saber_cuda_predict_table", C.c_int, [_P(saber_model), C.c_int32, _P(C.c_double)]),
+    ("saber_cuda_generate", C.c_int, [_P(saber_workload_spec), C.c_int32, C.c_int32,
+                                      _P(saber_request), C.c_int32]),
+    ("saber_cuda_release_cache", C.c_int, [C.c_int32]),
     ("saber_cuda_last_error", C.c_char_p, []),
     ("saber_cuda_abi_version", C.c_int32, []),
     ("saber_cuda_device_count", C.c_int32, []),
@@ -230,7 +251,7 @@ def lib():
 
 class SaberError(RuntimeError):
     def __init__(self, status: int, msg: str):
-        super().__init__(f"{STATUS_NAMES[status] if 0 <= status < 7 else status}: {msg}")
+        super().__init__(f"{STATUS_NAMES[status] if 0 <= status < len(STATUS_NAMES) else status}: {msg}")
         self.status = status
 
 

@@ -7,6 +7,7 @@ caller of the reference finds the same surface:
     sweep(grid, base, jobs=0)       -> SweepResult      simloop.hpp:96-99
     run(config)                     -> RunOutput        simloop.hpp:49
     run_with_requests(config, reqs) -> RunOutput        simloop.hpp:53-54
+    generate(spec)                  -> List[Request]    workload.hpp:31
     fit(samples, family)            -> SpeedModel       estimator.hpp:61
     calibrate(samples)              -> CalibrationReport calibration.hpp:54
     predict(model, load), max_speed(model)              estimator.hpp:39-42
@@ -152,8 +153,14 @@ class SimConfig:
     seed: int = 0
 
 
+class RequestState:
+    """types.hpp:43"""
+    QueuedHigh, QueuedLow, Executing, Completed = 0, 1, 2, 3
+
+
 @dataclass
 class Request:
+    """types.hpp:45-59 (id == index)."""
     id: int
     task: str
     arrival_time: float
@@ -161,6 +168,12 @@ class Request:
     max_output_tokens: int
     sla_seconds: float
     deadline: float
+    generated_tokens: float = 0.0
+    state: int = RequestState.QueuedHigh
+    admit_time: Optional[float] = None
+    completion_time: Optional[float] = None
+    recorded_required_speed: Optional[float] = None
+    demoted: bool = False
 
 
 @dataclass
@@ -186,7 +199,17 @@ class Decision:
 
 
 @dataclass
+class TaskMetrics:
+    """metrics.hpp:55-59"""
+    issued: int
+    goodput: float
+    cdf_points: List[Tuple[float, float]]
+
+
+@dataclass
 class MetricsReport:
+    """metrics.hpp:63-69 (goodput, ratio stats, per_task) plus the engine's
+    decision statistics and event counters."""
     goodput: float
     ratio_mean: float
     ratio_std: float
@@ -196,13 +219,16 @@ class MetricsReport:
     decision_kinds: List[int]
     decision_hash: int
     counters: Dict[str, int]
+    per_task: Dict[str, TaskMetrics] = field(default_factory=dict)
 
 
 @dataclass
 class RunOutput:
+    """simloop.hpp:37-43 (the engine event trace is not produced)."""
     records: List[RunRecord]
     decisions: Optional[List[Decision]]
     metrics: MetricsReport
+    requests: List[Request] = field(default_factory=list)
 
 
 @dataclass
@@ -300,6 +326,7 @@ def _spec_from_config(cfg: SimConfig, requests: Optional[Sequence[Request]] = No
     s.length_jitter = float(w.length_jitter)
     if requests is not None:
         arr = (N.saber_request * max(1, len(requests)))()
+        rank = {name: g for g, name in enumerate(sorted({r.task for r in requests}))}
         for i, r in enumerate(requests):
             if r.id != i:
                 raise InvalidArgument("run: request ids must be 0..n-1")
@@ -310,6 +337,7 @@ def _spec_from_config(cfg: SimConfig, requests: Optional[Sequence[Request]] = No
             q.input_tokens = r.input_tokens
             q.max_output_tokens = r.max_output_tokens
             q.task = TASK_INDEX.get(r.task, -1)
+            q.group = rank[r.task]
         s.requests = arr
         if keepalive is not None:
             keepalive.append(arr)
@@ -340,72 +368,135 @@ class BatchResult:
     decisions: Optional[List[np.ndarray]] = None
     device_ms: float = 0.0
     kernel_launches: int = 0
+    # full RunOutput from the engine (records=True)
+    requests: Optional[np.ndarray] = None      # REQUEST_DTYPE [n_traj][max_n]
+    states: Optional[np.ndarray] = None        # STATE_DTYPE [n_traj][max_n]
+    cdf_latency: Optional[np.ndarray] = None   # [n_traj][max_n]
+    cdf_fraction: Optional[np.ndarray] = None
+    group_issued: Optional[np.ndarray] = None  # [n_traj][max_groups]
+    group_met: Optional[np.ndarray] = None
 
 
 DECISION_DTYPE = np.dtype([("time", np.float64), ("request_id", np.uint64), ("kind", np.int32),
                            ("load_before", np.int32), ("has_pred", np.int32), ("has_req", np.int32),
                            ("pred_speed", np.float64), ("req_speed", np.float64)])
 assert DECISION_DTYPE.itemsize == C.sizeof(N.saber_decision)
+REQUEST_DTYPE = np.dtype([("arrival_time", np.float64), ("sla_seconds", np.float64),
+                          ("deadline", np.float64), ("input_tokens", np.int32),
+                          ("max_output_tokens", np.int32), ("task", np.int32), ("group", np.int32)])
+assert REQUEST_DTYPE.itemsize == C.sizeof(N.saber_request)
+STATE_DTYPE = np.dtype([("admit_time", np.float64), ("completion_time", np.float64),
+                        ("generated_tokens", np.float64), ("recorded_required_speed", np.float64),
+                        ("state", np.int32), ("met_sla", np.int32), ("demoted", np.int32),
+                        ("pad_", np.int32)])
+assert STATE_DTYPE.itemsize == C.sizeof(N.saber_request_state)
 
 
 def run_batch(configs: Sequence[SimConfig], requests: Optional[Sequence[Optional[Sequence[Request]]]] = None,
               records: bool = False, decisions: bool = False, decision_cap: int = 1 << 16,
               device: int = 0) -> BatchResult:
-    """Many independent run()/run_with_requests() trajectories in one launch."""
+    """Many independent run()/run_with_requests() trajectories in one launch.
+    records=True also returns every request's final state, its record and the
+    per-task-group CDFs, all computed on the device."""
     T = len(configs)
     if T == 0:
         raise InvalidArgument("run_batch: no trajectories")
     keep: list = []
     specs = (N.saber_traj_spec * T)()
+    max_group = 3
     for k, cfg in enumerate(configs):
         reqs = requests[k] if requests is not None else None
         specs[k] = _spec_from_config(cfg, reqs, keep)
+        if reqs is not None:
+            max_group = max(max_group, len({r.task for r in reqs}) - 1)
     max_n = max(int(s.num_requests) for s in specs)
-    rows = np.zeros(T, dtype=ROW_DTYPE)
-    comp = np.full((T, max_n), np.nan)
-    arr = np.full((T, max_n), np.nan) if records else None
-    adm = np.full((T, max_n), np.nan) if records else None
-    dem = np.zeros((T, max_n), dtype=np.uint8) if records else None
-    dec = np.zeros((T, decision_cap), dtype=DECISION_DTYPE) if decisions else None
-    ndec = np.zeros(T, dtype=np.int64) if decisions else None
-    d = N.saber_run_batch_desc()
-    d.specs = specs
-    d.n_traj = T
-    d.device = device
-    o = N.saber_run_batch_out()
-    P = C.POINTER
-    o.rows = rows.ctypes.data_as(P(N.saber_traj_row))
-    o.completion_times = comp.ctypes.data_as(P(C.c_double))
-    o.max_n = max_n
-    if records:
-        o.arrival_times = arr.ctypes.data_as(P(C.c_double))
-        o.admit_times = adm.ctypes.data_as(P(C.c_double))
-        o.demoted = dem.ctypes.data_as(P(C.c_uint8))
-    if decisions:
-        o.decisions = dec.ctypes.data_as(P(N.saber_decision))
-        o.decision_cap = decision_cap
-        o.n_decisions = ndec.ctypes.data_as(P(C.c_int64))
-    _check(N.lib().saber_cuda_run_batch(C.byref(d), C.byref(o)))
+    max_groups = max_group + 1
+    while True:
+        rows = np.zeros(T, dtype=ROW_DTYPE)
+        comp = np.full((T, max_n), np.nan)
+        arr = np.full((T, max_n), np.nan) if records else None
+        adm = np.full((T, max_n), np.nan) if records else None
+        dem = np.zeros((T, max_n), dtype=np.uint8) if records else None
+        dec = np.zeros((T, decision_cap), dtype=DECISION_DTYPE) if decisions else None
+        ndec = np.zeros(T, dtype=np.int64) if decisions else None
+        d = N.saber_run_batch_desc()
+        d.specs = specs
+        d.n_traj = T
+        d.device = device
+        o = N.saber_run_batch_out()
+        P = C.POINTER
+        o.rows = rows.ctypes.data_as(P(N.saber_traj_row))
+        o.completion_times = comp.ctypes.data_as(P(C.c_double))
+        o.max_n = max_n
+        ext = {}
+        if records:
+            o.arrival_times = arr.ctypes.data_as(P(C.c_double))
+            o.admit_times = adm.ctypes.data_as(P(C.c_double))
+            o.demoted = dem.ctypes.data_as(P(C.c_uint8))
+            ext = dict(requests=np.zeros((T, max_n), dtype=REQUEST_DTYPE),
+                       states=np.zeros((T, max_n), dtype=STATE_DTYPE),
+                       cdf_latency=np.full((T, max_n), np.nan),
+                       cdf_fraction=np.full((T, max_n), np.nan),
+                       group_issued=np.zeros((T, max_groups), dtype=np.int32),
+                       group_met=np.zeros((T, max_groups), dtype=np.int32))
+            o.requests = ext["requests"].ctypes.data_as(P(N.saber_request))
+            o.states = ext["states"].ctypes.data_as(P(N.saber_request_state))
+            o.cdf_latency = ext["cdf_latency"].ctypes.data_as(P(C.c_double))
+            o.cdf_fraction = ext["cdf_fraction"].ctypes.data_as(P(C.c_double))
+            o.group_issued = ext["group_issued"].ctypes.data_as(P(C.c_int32))
+            o.group_met = ext["group_met"].ctypes.data_as(P(C.c_int32))
+            o.max_groups = max_groups
+        if decisions:
+            o.decisions = dec.ctypes.data_as(P(N.saber_decision))
+            o.decision_cap = decision_cap
+            o.n_decisions = ndec.ctypes.data_as(P(C.c_int64))
+        st = N.lib().saber_cuda_run_batch(C.byref(d), C.byref(o))
+        if st == N.SABER_ECAPACITY and decisions and int(rows["decisions"].max()) > decision_cap:
+            decision_cap = int(rows["decisions"].max())  # exactly the longest log
+            continue
+        _check(st)
+        break
     decs = [dec[k, : ndec[k]].copy() for k in range(T)] if decisions else None
-    return BatchResult(rows, comp, arr, adm, dem, decs, o.device_ms, o.kernel_launches)
+    return BatchResult(rows, comp, arr, adm, dem, decs, o.device_ms, o.kernel_launches, **ext)
+
+
+def _opt(v) -> Optional[float]:
+    return None if math.isnan(v) else float(v)
 
 
 def _run_output(cfg: SimConfig, res: BatchResult, k: int, requests=None) -> RunOutput:
+    """RunOutput of trajectory k, every value read off the engine's outputs."""
     row = res.rows[k]
     n = int(row["n"])
-    recs = []
-    if res.arrival_times is not None:
-        names = [r.task for r in requests] if requests is not None else None
+    recs, reqs = [], []
+    per_task: Dict[str, TaskMetrics] = {}
+    if res.states is not None:
+        if requests is not None:
+            group_name = sorted({r.task for r in requests})
+        else:
+            group_name = sorted(TASK_NAMES)
         for i in range(n):
-            c = res.completion_times[k, i]
-            a = res.arrival_times[k, i]
-            ad = res.admit_times[k, i]
-            sla = requests[i].sla_seconds if requests is not None else None
-            recs.append(RunRecord(i, names[i] if names else "", float(a),
-                                  None if math.isnan(ad) else float(ad),
-                                  None if math.isnan(c) else float(c), sla if sla is not None else float("nan"),
-                                  (not math.isnan(c)) and sla is not None and (c - a) <= sla,
-                                  "low" if res.demoted[k, i] else "high"))
+            q = res.requests[k, i]
+            x = res.states[k, i]
+            task = requests[i].task if requests is not None else TASK_NAMES[int(q["task"])]
+            r = Request(i, task, float(q["arrival_time"]), int(q["input_tokens"]),
+                        int(q["max_output_tokens"]), float(q["sla_seconds"]), float(q["deadline"]),
+                        float(x["generated_tokens"]), int(x["state"]), _opt(x["admit_time"]),
+                        _opt(x["completion_time"]), _opt(x["recorded_required_speed"]),
+                        bool(x["demoted"]))
+            reqs.append(r)
+            recs.append(RunRecord(i, task, r.arrival_time, r.admit_time, r.completion_time,
+                                  r.sla_seconds, bool(x["met_sla"]), "low" if r.demoted else "high"))
+        start = 0
+        for g, name in enumerate(group_name):
+            issued = int(res.group_issued[k, g])
+            if issued == 0:
+                continue
+            seg = slice(start, start + issued)
+            lat, frac = res.cdf_latency[k, seg], res.cdf_fraction[k, seg]
+            pts = [(float(a), float(b)) for a, b in zip(lat, frac) if not math.isnan(b)]
+            per_task[name] = TaskMetrics(issued, float(res.group_met[k, g]) / float(issued), pts)
+            start += issued
     decs = None
     if res.decisions is not None:
         decs = [Decision(float(x["time"]), int(x["request_id"]), int(x["kind"]), int(x["load_before"]),
@@ -414,13 +505,13 @@ def _run_output(cfg: SimConfig, res: BatchResult, k: int, requests=None) -> RunO
     m = MetricsReport(float(row["goodput"]), float(row["ratio_mean"]), float(row["ratio_std"]),
                       float(row["cv"]), int(row["completed"]), int(row["decisions"]),
                       [int(v) for v in row["n_kind"]], int(row["decision_hash"]),
-                      {c: int(row[c]) for c in COUNTER_NAMES})
-    return RunOutput(recs, decs, m)
+                      {c: int(row[c]) for c in COUNTER_NAMES}, per_task)
+    return RunOutput(recs, decs, m, reqs)
 
 
 def run(config: SimConfig, decisions: bool = True, device: int = 0) -> RunOutput:
     """simloop.cpp:113-116: generate() then the tick loop, on the GPU."""
-    res = run_batch([config], records=True, decisions=decisions, decision_cap=1 << 20, device=device)
+    res = run_batch([config], records=True, decisions=decisions, device=device)
     return _run_output(config, res, 0)
 
 
@@ -429,9 +520,25 @@ def run_with_requests(config: SimConfig, requests: Sequence[Request], decisions:
     """simloop.cpp:50-111 over a caller-supplied workload (replay)."""
     if len(requests) == 0:
         raise InvalidArgument("run: no requests")
-    res = run_batch([config], [requests], records=True, decisions=decisions,
-                    decision_cap=1 << 20, device=device)
+    res = run_batch([config], [requests], records=True, decisions=decisions, device=device)
     return _run_output(config, res, 0, requests)
+
+
+def generate(spec: WorkloadSpec, device: int = 0) -> List[Request]:
+    """workload.cpp:52-79 on the device (bit-identical arrivals and lengths)."""
+    w = N.saber_workload_spec()
+    w.mix = _mix(spec.mix)
+    w.rps = float(spec.rps)
+    w.num_requests = int(spec.num_requests)
+    w.seed = int(spec.seed) & 0xFFFFFFFFFFFFFFFF
+    w.length_jitter = float(spec.length_jitter)
+    n = max(1, int(spec.num_requests))
+    out = np.zeros(n, dtype=REQUEST_DTYPE)
+    _check(N.lib().saber_cuda_generate(C.byref(w), 1, device,
+                                       out.ctypes.data_as(C.POINTER(N.saber_request)), n))
+    return [Request(i, TASK_NAMES[int(q["task"])], float(q["arrival_time"]), int(q["input_tokens"]),
+                    int(q["max_output_tokens"]), float(q["sla_seconds"]), float(q["deadline"]))
+            for i, q in enumerate(out)]
 
 
 # ---------------------------------------------------------------- sweep path

@@ -71,12 +71,15 @@ saber_status use_device(int device) {
     return fail(SABER_ECUDA, std::string("no CUDA device: ") + cudaGetErrorString(e));
   if (device < 0 || device >= count)
     return fail(SABER_EINVAL, "device ordinal " + std::to_string(device) + " out of range");
-  int major = 0;
+  // The library carries an arch-specific sm_100a cubin and no PTX, so only
+  // compute capability 10.0 can run it (sm_103 would fail at every launch).
+  int major = 0, minor = 0;
   CUDA_TRY(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, device));
-  if (major != 10) {
+  CUDA_TRY(cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, device));
+  if (major != 10 || minor != 0) {
     cudaDeviceProp prop;
     CUDA_TRY(cudaGetDeviceProperties(&prop, device));
-    return fail(SABER_ECUDA, std::string("device is not sm_100 (Blackwell): ") + prop.name);
+    return fail(SABER_ECUDA, std::string("device is not sm_100 (B200): ") + prop.name);
   }
   CUDA_TRY(cudaSetDevice(device));
   std::lock_guard<std::mutex> lk(mu);
@@ -104,11 +107,12 @@ struct HostTrace {
   }
 };
 
-// -------------------------------------------------- grow-only device cache --
-struct Block {
-  void* p;
-  size_t bytes;
-};
+// ------------------------------------------------------- device block cache --
+// Freed blocks are kept per device for reuse (cudaMalloc/cudaFree would sit in
+// every one-shot call's timed region).  A block goes back on the list only
+// after the work that used it has finished: every owner synchronises its
+// streams before releasing (SyncOnExit, saber_cuda_sweep_plan_destroy).
+// saber_cuda_release_cache() returns the cached blocks to the driver.
 std::mutex g_pool_mu;
 std::map<int, std::multimap<size_t, void*>> g_free;  // device -> size -> ptr
 
@@ -163,6 +167,20 @@ struct DevBuf {
   }
 };
 
+// Declared after the DevBufs of a call (so destroyed before them): waits for
+// the call's stream on every exit path once work was enqueued, so no kernel
+// still running can touch a block that went back to the cache.
+struct SyncOnExit {
+  const cudaStream_t* s[2] = {nullptr, nullptr};
+  explicit SyncOnExit(const cudaStream_t* a, const cudaStream_t* b = nullptr) : s{a, b} {}
+  SyncOnExit(const SyncOnExit&) = delete;
+  SyncOnExit& operator=(const SyncOnExit&) = delete;
+  ~SyncOnExit() {
+    if (s[0]) cudaStreamSynchronize(*s[0]);
+    if (s[1] && *s[1]) cudaStreamSynchronize(*s[1]);
+  }
+};
+
 #define ALLOC_TRY(buf, dev, n)                                                         \
   do {                                                                                 \
     if (!(buf).alloc((dev), (n)))                                                      \
@@ -176,6 +194,8 @@ const double kSlaH[4] = {1.0, 8.0, 1.0, 12.0};
 // std::map<std::string,...> order: code_generation, code_qna, code_summary, code_translation
 const int kAlphaH[4] = {SABER_TASK_GENERATION, SABER_TASK_QNA, SABER_TASK_SUMMARY,
                         SABER_TASK_TRANSLATION};
+// std::map order of the catalog names (records.cu kNameRank), by catalog id
+const int32_t kNameRankH[4] = {1, 0, 2, 3};
 constexpr uint64_t kSchedulerSeedSalt = 0x9e3779b97f4a7c15ull;  // scheduler.cpp:14
 
 // estimator.cpp:16-31 (eval), restated with libstdc++'s min/max/clamp.
@@ -312,25 +332,17 @@ struct Scratch {
   DevBuf ledger, low;
   SimLaunch launch{};
   GroupScratch view{};
-  // Kernel choice: the G-lane group kernel; SABER_KERNEL=lane
-  // selects the lane-per-trajectory lockstep kernel when the trajectory fits
-  // it (n <= 128, max_output_tokens < 2^23).  Measured slower on config 2
-  // (DESIGN.md §4), kept as a parity-tested alternative.
-  saber_status alloc(int device, int nmax, bool lane_ok = true) {
-    const char* e = std::getenv("SABER_KERNEL");
-    const bool lane = lane_ok && nmax <= kLaneMaxRequests && e && std::string(e) == "lane";
-    int rc = lane ? plan_sim_lane(nmax, &launch) : plan_sim(nmax, group_size(), &launch);
-    if (rc != 0 && lane) rc = plan_sim(nmax, group_size(), &launch);
+  // Kernel configuration: G lanes per trajectory.
+  saber_status alloc(int device, int nmax) {
+    const int rc = plan_sim(nmax, group_size(), &launch);
     if (rc != 0)
       return fail(SABER_ECUDA, "trajectory kernel configuration failed (" + std::to_string(rc) +
                                    "): " + cudaGetErrorString(cudaGetLastError()));
     // one ledger / low-FIFO slice per resident group of the LARGEST grid any
     // kernel variant launches with (the mode-specialised grids differ)
     int64_t grid = launch.grid;
-    if (!launch.lane)
-      for (int v = 0; v < 3; ++v) grid = std::max<int64_t>(grid, launch.grid_sel[v]);
-    const int64_t groups = launch.lane ? static_cast<int64_t>(launch.grid) * launch.block
-                                       : grid * (kSimBlock / kWarp) * (kWarp / launch.group);
+    for (int v = 0; v < 3; ++v) grid = std::max<int64_t>(grid, launch.grid_sel[v]);
+    const int64_t groups = grid * (kSimBlock / kWarp) * (kWarp / launch.group);
     const size_t per = static_cast<size_t>(nmax);
     ALLOC_TRY(ledger, device, static_cast<size_t>(groups) * per * sizeof(double));
     ALLOC_TRY(low, device, static_cast<size_t>(groups) * per * sizeof(uint16_t));
@@ -458,10 +470,15 @@ struct saber_sweep_plan {
   int32_t n_saber_first = 0;  // SABER rows lead the order: split launch
   cudaStream_t side = nullptr;
   cudaEvent_t fork = nullptr, join = nullptr;
+  // Recorded on the caller's stream at every exit of an enqueueing call
+  // (success or error), so destroy can wait for all of the plan's work.
+  cudaEvent_t tail_run = nullptr, tail_summ = nullptr;
   ~saber_sweep_plan() {
     if (side) cudaStreamDestroy(side);
     if (fork) cudaEventDestroy(fork);
     if (join) cudaEventDestroy(join);
+    if (tail_run) cudaEventDestroy(tail_run);
+    if (tail_summ) cudaEventDestroy(tail_summ);
   }
   Timer all, sim, summ;
   bool run_pending = false, summary_pending = false;
@@ -780,16 +797,27 @@ saber_status saber_cuda_sweep_plan_create(const saber_sweep_desc* desc, saber_sw
   CUDA_TRY(cudaStreamCreateWithFlags(&P->side, cudaStreamNonBlocking));
   CUDA_TRY(cudaEventCreateWithFlags(&P->fork, cudaEventDisableTiming));
   CUDA_TRY(cudaEventCreateWithFlags(&P->join, cudaEventDisableTiming));
+  CUDA_TRY(cudaEventCreateWithFlags(&P->tail_run, cudaEventDisableTiming));
+  CUDA_TRY(cudaEventCreateWithFlags(&P->tail_summ, cudaEventDisableTiming));
   tr.mark("events");
   *out = guard.release();
   return SABER_OK;
 }
 
+// Records `e` on `s` when the enqueueing call returns, on every path.
+struct TailMark {
+  cudaEvent_t e;
+  cudaStream_t s;
+  ~TailMark() { cudaEventRecord(e, s); }
+};
+
 static saber_status plan_launch_impl(saber_sweep_plan* P, void* stream, bool with_metrics) {
   if (!P) return fail(SABER_EINVAL, "null plan");
   CUDA_TRY(cudaSetDevice(P->device));
   cudaStream_t s = static_cast<cudaStream_t>(stream);
+  TailMark tail{P->tail_run, s};
   const saber_sweep_desc& d = P->desc;
+  P->rerun = false;
   P->launches = 0;
   P->summarized = false;
   P->summary_pending = false;
@@ -876,7 +904,7 @@ static saber_status plan_launch_impl(saber_sweep_plan* P, void* stream, bool wit
   sp.ticks = P->ticktab.view;
   CUDA_TRY(cudaEventRecord(P->sim.a, s));
   const bool split = P->n_saber_first > 0 && P->n_saber_first < P->rows_shard &&
-                     P->scratch.launch.group == 32 && !P->scratch.launch.lane &&
+                     P->scratch.launch.group == 32 &&
                      std::getenv("SABER_NO_SPLIT") == nullptr;
   if (split) {
     // SABER rows [0, ns) on the SABER-only kernel, static rows [ns, N) on the
@@ -944,7 +972,7 @@ saber_status saber_cuda_sweep_plan_wait(saber_sweep_plan* P) {
         P->stream_cap = std::min(full, P->stream_cap * 4);
         if (saber_status s = set_stream_lengths(P, P->device)) return s;
         P->rerun = true;
-        return fail(SABER_EINTERNAL, "scheduler RNG streams grown; rerun the sweep");
+        return fail(SABER_ERETRY, "scheduler RNG streams grown; rerun the sweep");
       }
       return fail(SABER_EINTERNAL, "scheduler RNG stream exhausted (draw bound violated)");
     }
@@ -965,8 +993,7 @@ saber_status saber_cuda_sweep_plan_run(saber_sweep_plan* P, void* stream) {
   for (;;) {
     if (saber_status s = saber_cuda_sweep_plan_launch(P, stream)) return s;
     const saber_status s = saber_cuda_sweep_plan_wait(P);
-    if (s == SABER_OK || !P->rerun) return s;  // grown draw streams: run again
-    P->rerun = false;
+    if (s != SABER_ERETRY) return s;  // grown draw streams: run again
   }
 }
 
@@ -974,6 +1001,7 @@ static saber_status summarize_launch_impl(saber_sweep_plan* P, void* stream, boo
   if (!P) return fail(SABER_EINVAL, "null plan");
   CUDA_TRY(cudaSetDevice(P->device));
   cudaStream_t s = static_cast<cudaStream_t>(stream);
+  TailMark tail{P->tail_summ, s};
   const saber_sweep_desc& d = P->desc;
   SummaryParams sp{};
   sp.rows = P->rows.as<saber_traj_row>();
@@ -1063,7 +1091,21 @@ saber_status saber_cuda_sweep_plan_stats(saber_sweep_plan* P, double* device_ms,
 void saber_cuda_sweep_plan_destroy(saber_sweep_plan* P) {
   if (!P) return;
   cudaSetDevice(P->device);
+  // Wait for everything the plan enqueued (its buffers go back to the cache).
+  if (P->tail_run) cudaEventSynchronize(P->tail_run);
+  if (P->tail_summ) cudaEventSynchronize(P->tail_summ);
+  if (P->side) cudaStreamSynchronize(P->side);
   delete P;
+}
+
+saber_status saber_cuda_release_cache(int32_t device) {
+  std::lock_guard<std::mutex> lk(g_pool_mu);
+  auto it = g_free.find(device);
+  if (it == g_free.end()) return SABER_OK;
+  CUDA_TRY(cudaSetDevice(device));
+  for (auto& kv : it->second) cudaFree(kv.second);
+  g_free.erase(it);
+  return SABER_OK;
 }
 
 saber_status saber_cuda_sweep(const saber_sweep_desc* desc, saber_sweep_out* out) {
@@ -1110,7 +1152,7 @@ int32_t saber_cuda_device_count(void) {
   int usable = 0;
   for (int i = 0; i < count; ++i) {
     cudaDeviceProp p;
-    if (cudaGetDeviceProperties(&p, i) == cudaSuccess && p.major == 10) ++usable;
+    if (cudaGetDeviceProperties(&p, i) == cudaSuccess && p.major == 10 && p.minor == 0) ++usable;
   }
   return usable;
 }
@@ -1173,9 +1215,29 @@ extern "C" saber_status saber_cuda_run_batch(const saber_run_batch_desc* desc,
     if (saber_status s = validate_spec(desc->specs[k])) return s;
     nmax = std::max(nmax, desc->specs[k].num_requests);
   }
-  if ((out->arrival_times || out->admit_times || out->completion_times || out->demoted) &&
+  const bool want_states = out->states || out->cdf_latency || out->cdf_fraction ||
+                           out->group_issued || out->group_met;
+  if ((out->arrival_times || out->admit_times || out->completion_times || out->demoted ||
+       out->requests || want_states) &&
       out->max_n < nmax)
     return fail(SABER_EINVAL, "run_batch: max_n smaller than the largest trajectory");
+  if ((out->cdf_latency == nullptr) != (out->cdf_fraction == nullptr) ||
+      (out->group_issued == nullptr) != (out->group_met == nullptr))
+    return fail(SABER_EINVAL, "run_batch: cdf_latency/cdf_fraction and group_issued/group_met "
+                              "come in pairs");
+  if (out->group_issued) {
+    for (int k = 0; k < T; ++k) {
+      const saber_traj_spec& s = desc->specs[k];
+      if (!s.requests) {
+        if (out->max_groups < 4)
+          return fail(SABER_EINVAL, "run_batch: max_groups < 4 with a generated trajectory");
+        continue;
+      }
+      for (int i = 0; i < s.num_requests; ++i)
+        if (s.requests[i].group < 0 || s.requests[i].group >= out->max_groups)
+          return fail(SABER_EINVAL, "run_batch: request group outside [0, max_groups)");
+    }
+  }
   if (saber_status s = use_device(desc->device)) return s;
   const int dev = desc->device;
 
@@ -1187,6 +1249,8 @@ extern "C" saber_status saber_cuda_run_batch(const saber_run_batch_desc* desc,
   const size_t cells = static_cast<size_t>(T) * nmax;
   std::vector<double> arr(cells, 0.0), dl(cells, 0.0), sla(cells, 1.0), mo(cells, 1.0), in(cells, 1.0);
   std::vector<int8_t> task(cells, -1);
+  std::vector<int32_t> group(cells, -1);  // -1: generated (the task's name rank)
+  bool any_replay = false;
   const int tl = nmax + 2;
   std::vector<double> tab(static_cast<size_t>(T) * 2 * tl);
   std::vector<TrajDesc> descs(static_cast<size_t>(T));
@@ -1215,6 +1279,7 @@ extern "C" saber_status saber_cuda_run_batch(const saber_run_batch_desc* desc,
     double last_bound = 0.0, max_sla = 12.0;
     if (s.requests) {
       it.kind = 1;
+      any_replay = true;
       max_sla = 0.0;
       for (int i = 0; i < n; ++i) {
         const saber_request& q = s.requests[i];
@@ -1225,6 +1290,7 @@ extern "C" saber_status saber_cuda_run_batch(const saber_run_batch_desc* desc,
         mo[o] = static_cast<double>(q.max_output_tokens);
         in[o] = static_cast<double>(q.input_tokens);
         task[o] = static_cast<int8_t>(q.task >= 0 && q.task < 4 ? q.task : -1);
+        group[o] = q.group < 0 ? 0 : q.group;
         max_sla = std::max(max_sla, q.sla_seconds);
       }
       last_bound = s.requests[n - 1].arrival_time;
@@ -1263,7 +1329,7 @@ extern "C" saber_status saber_cuda_run_batch(const saber_run_batch_desc* desc,
 
   Workloads wl;
   DevBuf tables, seeds_d, off_d, len_d, draws_d, descs_d, rows_d, comp_d, admit_d, demo_d, cursor_d,
-      err_d, trace_d, tcount_d;
+      err_d, trace_d, tcount_d, gen_d, group_d, req_d, state_d, cdfl_d, cdff_d, gi_d, gm_d;
   Scratch scratch;
   if (saber_status s = wl.alloc(dev, T, nmax)) return s;
   ALLOC_TRY(wl.items, dev, items.size() * sizeof(WorkloadItem));
@@ -1277,11 +1343,26 @@ extern "C" saber_status saber_cuda_run_batch(const saber_run_batch_desc* desc,
   ALLOC_TRY(comp_d, dev, cells * 8);
   ALLOC_TRY(cursor_d, dev, 16);
   ALLOC_TRY(err_d, dev, 16);
-  const bool records = out->admit_times || out->demoted;
+  const bool records = out->admit_times || out->demoted || want_states;
   if (records) {
     ALLOC_TRY(admit_d, dev, cells * 8);
     ALLOC_TRY(demo_d, dev, cells);
   }
+  const int max_groups = out->group_issued ? out->max_groups : 0;
+  if (want_states) {
+    ALLOC_TRY(gen_d, dev, cells * 8);
+    ALLOC_TRY(state_d, dev, cells * sizeof(saber_request_state));
+    if (any_replay) ALLOC_TRY(group_d, dev, cells * 4);
+    if (out->cdf_latency) {
+      ALLOC_TRY(cdfl_d, dev, cells * 8);
+      ALLOC_TRY(cdff_d, dev, cells * 8);
+    }
+    if (max_groups > 0) {
+      ALLOC_TRY(gi_d, dev, static_cast<size_t>(T) * max_groups * 4);
+      ALLOC_TRY(gm_d, dev, static_cast<size_t>(T) * max_groups * 4);
+    }
+  }
+  if (out->requests) ALLOC_TRY(req_d, dev, cells * sizeof(saber_request));
   const bool trace = out->decisions != nullptr;
   if (trace) {
     if (out->decision_cap < 1 || !out->n_decisions)
@@ -1295,10 +1376,7 @@ extern "C" saber_status saber_cuda_run_batch(const saber_run_batch_desc* desc,
     ALLOC_TRY(len_d, dev, len.size() * 8);
     ALLOC_TRY(draws_d, dev, static_cast<size_t>(std::max<int64_t>(1, total_draws)) * 4);
   }
-  bool lane_ok = true;
-  for (size_t i = 0; i < cells; ++i)
-    if (!(mo[i] <= kLaneMaxOutput)) lane_ok = false;
-  if (saber_status s = scratch.alloc(dev, nmax, lane_ok)) return s;
+  if (saber_status s = scratch.alloc(dev, nmax)) return s;
   // One tick table, for the most common tick of the batch.
   TickTableBuf ticktab;
   {
@@ -1337,6 +1415,7 @@ extern "C" saber_status saber_cuda_run_batch(const saber_run_batch_desc* desc,
   CUDA_TRY(cudaMemcpy(wl.task.p, task.data(), cells, cudaMemcpyHostToDevice));
   CUDA_TRY(cudaMemcpy(tables.p, tab.data(), tab.size() * 8, cudaMemcpyHostToDevice));
   CUDA_TRY(cudaMemcpy(descs_d.p, descs.data(), descs.size() * sizeof(TrajDesc), cudaMemcpyHostToDevice));
+  if (group_d.p) CUDA_TRY(cudaMemcpy(group_d.p, group.data(), cells * 4, cudaMemcpyHostToDevice));
   if (!seeds.empty()) {
     CUDA_TRY(cudaMemcpy(seeds_d.p, seeds.data(), seeds.size() * 8, cudaMemcpyHostToDevice));
     CUDA_TRY(cudaMemcpy(off_d.p, off.data(), off.size() * 8, cudaMemcpyHostToDevice));
@@ -1346,6 +1425,7 @@ extern "C" saber_status saber_cuda_run_batch(const saber_run_batch_desc* desc,
   Timer tm;
   if (saber_status s = tm.init()) return s;
   cudaStream_t st = nullptr;
+  SyncOnExit sync_guard(&st);
   int launches = 0;
   CUDA_TRY(cudaEventRecord(tm.a, st));
   CUDA_TRY(cudaMemsetAsync(rows_d.p, 0, rows_d.bytes, st));
@@ -1358,6 +1438,8 @@ extern "C" saber_status saber_cuda_run_batch(const saber_run_batch_desc* desc,
     ++launches;
     CUDA_TRY(cudaMemsetAsync(demo_d.p, 0, cells, st));
   }
+  if (gen_d.p) CUDA_TRY(cudaMemsetAsync(gen_d.p, 0, cells * 8, st));
+  if (req_d.p) CUDA_TRY(cudaMemsetAsync(req_d.p, 0, cells * sizeof(saber_request), st));
   WorkloadParams wp{};
   wp.items = wl.items.as<WorkloadItem>();
   wp.n_items = T;
@@ -1406,6 +1488,7 @@ extern "C" saber_status saber_cuda_run_batch(const saber_run_batch_desc* desc,
   sp.out.completion = comp_d.as<double>();
   sp.out.admit = records ? admit_d.as<double>() : nullptr;
   sp.out.demoted = records ? demo_d.as<uint8_t>() : nullptr;
+  sp.out.generated = gen_d.p ? gen_d.as<double>() : nullptr;
   sp.out.trace = trace ? trace_d.as<saber_decision>() : nullptr;
   sp.out.trace_count = trace ? tcount_d.as<int64_t>() : nullptr;
   sp.out.trace_cap = trace ? out->decision_cap : 0;
@@ -1427,6 +1510,32 @@ extern "C" saber_status saber_cuda_run_batch(const saber_run_batch_desc* desc,
   rm.n_traj = T;
   LAUNCH_TRY(launch_row_metrics(rm, st));
   ++launches;
+  if (want_states || req_d.p) {
+    RecordsParams rp{};
+    rp.traj = sp.traj;
+    rp.n_traj = T;
+    rp.wl = sp.wl;
+    rp.group = group_d.p ? group_d.as<int32_t>() : nullptr;
+    rp.completion = comp_d.as<double>();
+    rp.admit = admit_d.as<double>();
+    rp.demoted = demo_d.as<uint8_t>();
+    rp.generated = gen_d.as<double>();
+    rp.requests = req_d.p ? req_d.as<saber_request>() : nullptr;
+    rp.states = state_d.p ? state_d.as<saber_request_state>() : nullptr;
+    rp.cdf_latency = cdfl_d.p ? cdfl_d.as<double>() : nullptr;
+    rp.cdf_fraction = cdff_d.p ? cdff_d.as<double>() : nullptr;
+    rp.group_issued = gi_d.p ? gi_d.as<int32_t>() : nullptr;
+    rp.group_met = gm_d.p ? gm_d.as<int32_t>() : nullptr;
+    rp.max_groups = max_groups;
+    if (rp.requests) {
+      LAUNCH_TRY(launch_pack_requests(rp, st));
+      ++launches;
+    }
+    if (rp.states) {
+      LAUNCH_TRY(launch_records(rp, st));
+      ++launches;
+    }
+  }
   CUDA_TRY(cudaEventRecord(tm.b, st));
   CUDA_TRY(cudaEventSynchronize(tm.b));
   float ms = 0.f;
@@ -1436,13 +1545,12 @@ extern "C" saber_status saber_cuda_run_batch(const saber_run_batch_desc* desc,
 
   CUDA_TRY(cudaMemcpy(out->rows, rows_d.p, static_cast<size_t>(T) * sizeof(saber_traj_row),
                       cudaMemcpyDeviceToHost));
+  // [T][nmax] device rows -> the caller's [T][max_n] rows
   auto copy_rows = [&](void* dst, const DevBuf& src, size_t elem) -> saber_status {
     if (!dst) return SABER_OK;
-    std::vector<uint8_t> h(cells * elem);
-    CUDA_TRY(cudaMemcpy(h.data(), src.p, cells * elem, cudaMemcpyDeviceToHost));
-    for (int k = 0; k < T; ++k)
-      std::memcpy(static_cast<uint8_t*>(dst) + static_cast<size_t>(k) * out->max_n * elem,
-                  h.data() + static_cast<size_t>(k) * nmax * elem, static_cast<size_t>(nmax) * elem);
+    CUDA_TRY(cudaMemcpy2D(dst, static_cast<size_t>(out->max_n) * elem, src.p,
+                          static_cast<size_t>(nmax) * elem, static_cast<size_t>(nmax) * elem,
+                          static_cast<size_t>(T), cudaMemcpyDeviceToHost));
     return SABER_OK;
   };
   if (saber_status s = copy_rows(out->completion_times, comp_d, 8)) return s;
@@ -1451,11 +1559,26 @@ extern "C" saber_status saber_cuda_run_batch(const saber_run_batch_desc* desc,
     if (saber_status s = copy_rows(out->admit_times, admit_d, 8)) return s;
     if (saber_status s = copy_rows(out->demoted, demo_d, 1)) return s;
   }
+  if (saber_status s = copy_rows(out->requests, req_d, sizeof(saber_request))) return s;
+  if (saber_status s = copy_rows(out->states, state_d, sizeof(saber_request_state))) return s;
+  if (saber_status s = copy_rows(out->cdf_latency, cdfl_d, 8)) return s;
+  if (saber_status s = copy_rows(out->cdf_fraction, cdff_d, 8)) return s;
+  if (max_groups > 0) {
+    CUDA_TRY(cudaMemcpy(out->group_issued, gi_d.p, static_cast<size_t>(T) * max_groups * 4,
+                        cudaMemcpyDeviceToHost));
+    CUDA_TRY(cudaMemcpy(out->group_met, gm_d.p, static_cast<size_t>(T) * max_groups * 4,
+                        cudaMemcpyDeviceToHost));
+  }
   if (trace) {
     CUDA_TRY(cudaMemcpy(out->n_decisions, tcount_d.p, static_cast<size_t>(T) * 8, cudaMemcpyDeviceToHost));
-    CUDA_TRY(cudaMemcpy(out->decisions, trace_d.p,
-                        static_cast<size_t>(T) * out->decision_cap * sizeof(saber_decision),
-                        cudaMemcpyDeviceToHost));
+    // only the records each trajectory wrote
+    for (int k = 0; k < T; ++k) {
+      const int64_t nk = std::min(out->n_decisions[k], out->decision_cap);
+      if (nk > 0)
+        CUDA_TRY(cudaMemcpy(out->decisions + static_cast<size_t>(k) * out->decision_cap,
+                            trace_d.as<saber_decision>() + static_cast<size_t>(k) * out->decision_cap,
+                            static_cast<size_t>(nk) * sizeof(saber_decision), cudaMemcpyDeviceToHost));
+    }
   }
   out->device_ms = ms;
   out->kernel_launches = launches;
@@ -1463,6 +1586,104 @@ extern "C" saber_status saber_cuda_run_batch(const saber_run_batch_desc* desc,
   if (err == kErrRngExhausted)
     return fail(SABER_EINTERNAL, "scheduler RNG stream exhausted (draw bound violated)");
   if (err != 0) return fail(SABER_EINTERNAL, "trajectory kernel error " + std::to_string(err));
+  return SABER_OK;
+}
+
+// generate() (workload.cpp:52-79) for many specs: the host draws (mt19937_64,
+// glibc log: SURVEY F1/F5) and the device expansion the trajectory engine uses
+// (workloads_kernel), packed as saber_request rows.
+extern "C" saber_status saber_cuda_generate(const saber_workload_spec* specs, int32_t n_specs,
+                                            int32_t device, saber_request* out, int32_t max_n) {
+  if (!specs || !out || n_specs < 1) return fail(SABER_EINVAL, "generate: no specs");
+  int nmax = 1;
+  for (int k = 0; k < n_specs; ++k) {  // validate(WorkloadSpec) (workload.cpp:41-48)
+    const saber_workload_spec& w = specs[k];
+    if (!(w.rps > 0.0)) return fail(SABER_EINVAL, "rps must be > 0");
+    if (w.num_requests < 1) return fail(SABER_EINVAL, "num_requests must be >= 1");
+    if (w.length_jitter < 0.0 || w.length_jitter >= 1.0)
+      return fail(SABER_EINVAL, "length_jitter must be in [0, 1)");
+    if (saber_status e = validate_mix(w.mix)) return e;
+    nmax = std::max(nmax, w.num_requests);
+  }
+  if (max_n < nmax) return fail(SABER_EINVAL, "generate: max_n smaller than num_requests");
+  if (saber_status s = use_device(device)) return s;
+  const int dev = device;
+  const int T = n_specs;
+  const size_t cells = static_cast<size_t>(T) * nmax;
+  std::vector<WorkloadItem> items(static_cast<size_t>(T));
+  std::vector<double> base(cells * 4, 0.0), th(static_cast<size_t>(T) * 4);
+  std::vector<int8_t> tt(static_cast<size_t>(T) * 4), tlast(static_cast<size_t>(T));
+  std::vector<TrajDesc> descs(static_cast<size_t>(T));
+  for (int k = 0; k < T; ++k) {
+    const saber_workload_spec& w = specs[k];
+    double nls = 0.0;
+    seed_draws(w.seed, w.num_requests, &base[static_cast<size_t>(k) * nmax * 4], &nls);
+    mix_thresholds(w.mix, &th[static_cast<size_t>(k) * 4], &tt[static_cast<size_t>(k) * 4],
+                   &tlast[static_cast<size_t>(k)]);
+    WorkloadItem& it = items[static_cast<size_t>(k)];
+    it.kind = 0;
+    it.n = w.num_requests;
+    it.seed_idx = k;
+    it.mix = k;
+    it.rps = w.rps;
+    it.jitter = w.length_jitter;
+    it.ceiling = std::nan("");
+    TrajDesc& d = descs[static_cast<size_t>(k)];
+    d = TrajDesc{};
+    d.workload = k;
+    d.n = w.num_requests;
+    d.row = k;
+  }
+  Workloads wl;
+  DevBuf descs_d, req_d;
+  if (saber_status s = wl.alloc(dev, T, nmax)) return s;
+  ALLOC_TRY(wl.items, dev, items.size() * sizeof(WorkloadItem));
+  ALLOC_TRY(wl.seed_base, dev, base.size() * 8);
+  ALLOC_TRY(wl.th, dev, th.size() * 8);
+  ALLOC_TRY(wl.tt, dev, tt.size());
+  ALLOC_TRY(wl.tl, dev, tlast.size());
+  ALLOC_TRY(descs_d, dev, descs.size() * sizeof(TrajDesc));
+  ALLOC_TRY(req_d, dev, cells * sizeof(saber_request));
+  cudaStream_t st = nullptr;
+  SyncOnExit sync_guard(&st);
+  CUDA_TRY(cudaMemcpyAsync(wl.items.p, items.data(), items.size() * sizeof(WorkloadItem),
+                           cudaMemcpyHostToDevice, st));
+  CUDA_TRY(cudaMemcpyAsync(wl.seed_base.p, base.data(), base.size() * 8, cudaMemcpyHostToDevice, st));
+  CUDA_TRY(cudaMemcpyAsync(wl.th.p, th.data(), th.size() * 8, cudaMemcpyHostToDevice, st));
+  CUDA_TRY(cudaMemcpyAsync(wl.tt.p, tt.data(), tt.size(), cudaMemcpyHostToDevice, st));
+  CUDA_TRY(cudaMemcpyAsync(wl.tl.p, tlast.data(), tlast.size(), cudaMemcpyHostToDevice, st));
+  CUDA_TRY(cudaMemcpyAsync(descs_d.p, descs.data(), descs.size() * sizeof(TrajDesc),
+                           cudaMemcpyHostToDevice, st));
+  WorkloadParams wp{};
+  wp.items = wl.items.as<WorkloadItem>();
+  wp.n_items = T;
+  wp.seed_base = wl.seed_base.as<double>();
+  wp.seed_stride = nmax;
+  wp.mix_thresh = wl.th.as<double>();
+  wp.mix_task = wl.tt.as<int8_t>();
+  wp.mix_last = wl.tl.as<int8_t>();
+  wp.arrival = wl.arr.as<double>();
+  wp.deadline = wl.dl.as<double>();
+  wp.sla = wl.sla.as<double>();
+  wp.max_out = wl.mo.as<double>();
+  wp.input = wl.in.as<double>();
+  wp.demote_after = wl.dem.as<double>();
+  wp.horizon = wl.hor.as<double>();
+  wp.task = wl.task.as<int8_t>();
+  wp.nmax = nmax;
+  CUDA_TRY(cudaMemsetAsync(req_d.p, 0, cells * sizeof(saber_request), st));
+  LAUNCH_TRY(launch_workloads(wp, st));
+  RecordsParams rp{};
+  rp.traj = descs_d.as<TrajDesc>();
+  rp.n_traj = T;
+  rp.wl = wl.view(nmax);
+  rp.requests = req_d.as<saber_request>();
+  LAUNCH_TRY(launch_pack_requests(rp, st));
+  CUDA_TRY(cudaMemcpy2DAsync(out, static_cast<size_t>(max_n) * sizeof(saber_request), req_d.p,
+                             static_cast<size_t>(nmax) * sizeof(saber_request),
+                             static_cast<size_t>(nmax) * sizeof(saber_request), static_cast<size_t>(T),
+                             cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
   return SABER_OK;
 }
 
@@ -1511,6 +1732,7 @@ extern "C" saber_status saber_cuda_fit_batch(const saber_fit_desc* desc, saber_f
   Timer tm;
   if (saber_status s = tm.init()) return s;
   cudaStream_t st = nullptr;
+  SyncOnExit sync_guard(&st);
   CUDA_TRY(cudaEventRecord(tm.a, st));
   if (M > 0) {
     CUDA_TRY(cudaMemcpyAsync(loads.p, desc->loads, static_cast<size_t>(M) * 4, cudaMemcpyHostToDevice, st));
@@ -1642,7 +1864,7 @@ extern "C" saber_status saber_cuda_mc_trace(const saber_mc_desc* desc, int64_t k
     r.sla_seconds = kSlaH[task];
     r.deadline = arrival + kSlaH[task];
     r.task = task;
-    r.pad_ = 0;
+    r.group = kNameRankH[r.task >= 0 && r.task < 4 ? r.task : 0];
   }
   *spec = saber_traj_spec{};
   spec->mix = mix;
@@ -1806,7 +2028,7 @@ extern "C" saber_status saber_cuda_mc_sweep(const saber_mc_desc* desc, saber_mc_
   if (out->rows) host_rows.resize(static_cast<size_t>(chunk));
   // split launches (SABER-only + static-only kernels) need both classes
   const bool split_ok = d.with_saber && d.n_caps > 0 && scratch.launch.group == 32 &&
-                        !scratch.launch.lane && std::getenv("SABER_NO_SPLIT") == nullptr;
+                        std::getenv("SABER_NO_SPLIT") == nullptr;
   std::vector<int32_t> ord_h;
   DevBuf order_d;
   cudaStream_t side = nullptr;
@@ -1821,6 +2043,7 @@ extern "C" saber_status saber_cuda_mc_sweep(const saber_mc_desc* desc, saber_mc_
       if (*b) cudaEventDestroy(*b);
     }
   } sguard{&side, &fork_ev, &join_ev};
+  SyncOnExit sync_guard(&st, &side);  // after every DevBuf and the side stream
   if (split_ok) {
     ord_h.resize(static_cast<size_t>(chunk));
     ALLOC_TRY(order_d, dev, static_cast<size_t>(chunk) * 4);
@@ -2038,6 +2261,7 @@ extern "C" saber_status saber_cuda_profile_batch(const saber_profile_desc* desc,
   Timer tm;
   if (saber_status e = tm.init()) return e;
   cudaStream_t st = nullptr;
+  SyncOnExit sync_guard(&st);
   CUDA_TRY(cudaEventRecord(tm.a, st));
   CUDA_TRY(cudaMemcpyAsync(tables.p, tab.data(), tab.size() * 8, cudaMemcpyHostToDevice, st));
   CUDA_TRY(cudaMemcpyAsync(pr.p, prate.data(), prate.size() * 8, cudaMemcpyHostToDevice, st));

@@ -77,6 +77,7 @@ struct SimOutputs {
   double* completion;         // [rows][nmax]   pre-filled NaN by the caller
   double* admit;              // [rows][nmax] or null
   uint8_t* demoted;           // [rows][nmax] or null
+  double* generated;          // [rows][nmax] or null: fluid progress of slots still running at the end
   saber_decision* trace;      // [trace_rows][trace_cap] or null
   int64_t* trace_count;       // [rows] or null
   int64_t trace_cap;
@@ -127,11 +128,10 @@ enum : int32_t {
 struct SimLaunch {
   int nwords;     // 64-bit mask words (n <= 64 * nwords)
   int group;      // lanes per trajectory
-  int lane;       // 1 = lane-per-trajectory lockstep kernel (sim_lane.cu)
   int block;      // threads per block
   int grid;       // persistent blocks
   int grid_sel[3];  // persistent blocks per mode-specialised variant (G = 32)
-  int slot_rows;  // group kernel: ceil(nmax / group); lane kernel: nmax
+  int slot_rows;  // ceil(nmax / group)
   size_t smem;    // dynamic shared memory per block
 };
 constexpr int kSimBlock = 128;
@@ -141,11 +141,6 @@ int launch_sim(const SimParams& p, const SimLaunch& l, void* stream);
 // streak bounds without table searches on the trajectory's critical path).
 int launch_tick_index(const WorkloadTables& wl, int64_t cells, const TickTable& tt, int32_t* ka,
                       int32_t* kd, void* stream);
-// Lane-per-trajectory lockstep kernel: n <= 128, max_output_tokens < 2^23.
-constexpr int kLaneMaxRequests = 128;
-constexpr double kLaneMaxOutput = 8388607.0;
-int plan_sim_lane(int nmax, SimLaunch* out);
-int launch_sim_lane(const SimParams& p, const SimLaunch& l, void* stream);
 
 struct RngGenParams {
   const uint64_t* seeds;  // [n_streams] already xor-salted
@@ -213,6 +208,30 @@ struct RowMetricsParams {
   int32_t narrow;  // 1 = a few single-warp blocks (beside the trajectory kernels)
 };
 int launch_row_metrics(const RowMetricsParams& p, void* stream);
+
+// run() epilogue (records.cu): the workload as saber_request, the final
+// request states / records and the per-group latency CDFs.  All outputs are
+// [rows][nmax] (group counts [rows][max_groups]); `group` is [W][nmax] for
+// replayed workloads (-1 = generated: the task's name rank), or null.
+struct RecordsParams {
+  const TrajDesc* traj;
+  int32_t n_traj;
+  WorkloadTables wl;
+  const int32_t* group;
+  const double* completion;
+  const double* admit;
+  const uint8_t* demoted;
+  const double* generated;
+  saber_request* requests;
+  saber_request_state* states;
+  double* cdf_latency;
+  double* cdf_fraction;
+  int32_t* group_issued;
+  int32_t* group_met;
+  int32_t max_groups;
+};
+int launch_pack_requests(const RecordsParams& p, void* stream);
+int launch_records(const RecordsParams& p, void* stream);
 
 // Sweep summary (simloop.cpp:206-275).
 struct SummaryParams {

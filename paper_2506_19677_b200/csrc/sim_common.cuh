@@ -1,5 +1,5 @@
-// sim_common.cuh — device helpers shared by the trajectory kernels
-// (sim_kernel.cu: G-lane groups; sim_lane.cu: lane-per-trajectory lockstep).
+// sim_common.cuh — device helpers of the trajectory kernels (sim_kernel.cu,
+// mc.cu).
 #pragma once
 
 #include <cuda_runtime.h>

@@ -881,6 +881,15 @@ __device__ __forceinline__ void simulate_one(const SimParams& P, int ti, const S
   }
 
   if (failed && leader) atomicCAS(P.out.error, kErrNone, kErrRngExhausted);
+  if (kRecords && P.out.generated) {
+    // fluid progress of the requests still running (Request::generated_tokens;
+    // a slot in prefill has generated nothing yet)
+    double* __restrict__ GEN = P.out.generated + d.row * nmax;
+    for (int k = sub, s = S.idx(sub); k < A; k += G, s += kWarp) {
+      const double g = S.g[s];
+      GEN[static_cast<int>(S.m[s] & kIdMask)] = g < 0.0 ? 0.0 : g;
+    }
+  }
   if (leader) {
     saber_traj_row* R = P.out.rows + d.row;
     R->n = n;
@@ -1179,14 +1188,12 @@ int plan_sim(int nmax, int group, SimLaunch* out) {
   // (single-warp blocks on a side stream) finds room (bench.py pipelining).
   if (l.grid_sel[kSelSaber] > 16 * kSimBlock / kWarp) l.grid_sel[kSelSaber] -= 8;
   l.grid = l.grid_sel[0];
-  l.lane = 0;
   l.block = kSimBlock;
   *out = l;
   return 0;
 }
 
 int launch_sim(const SimParams& p, const SimLaunch& l, void* stream) {
-  if (l.lane) return launch_sim_lane(p, l, stream);
   const bool trace = p.out.trace != nullptr;
   const bool records = p.out.admit != nullptr || p.out.demoted != nullptr;
   const int sel = p.mode_sel;

@@ -44,7 +44,8 @@ def test_library_is_sm100a():
 STRUCTS = ["saber_model", "saber_mix", "saber_traj_row", "saber_decision", "saber_sweep_desc",
            "saber_mix_summary", "saber_sweep_out", "saber_sweep_buffers", "saber_request",
            "saber_traj_spec", "saber_run_batch_desc", "saber_run_batch_out", "saber_fit_desc",
-           "saber_fit_out"]
+           "saber_fit_out", "saber_request_state", "saber_workload_spec", "saber_mc_desc",
+           "saber_mc_out", "saber_profile_spec", "saber_profile_desc", "saber_profile_out"]
 
 
 def test_struct_layouts_match_header():
@@ -57,6 +58,10 @@ def test_struct_layouts_match_header():
         prog += f'printf("desc.{name} %zu\\n", offsetof(saber_sweep_desc, {name}));\n'
     for name, _ in N.saber_traj_spec._fields_:
         prog += f'printf("spec.{name} %zu\\n", offsetof(saber_traj_spec, {name}));\n'
+    for name, _ in N.saber_run_batch_out._fields_:
+        prog += f'printf("rbo.{name} %zu\\n", offsetof(saber_run_batch_out, {name}));\n'
+    for name, _ in N.saber_request_state._fields_:
+        prog += f'printf("rst.{name} %zu\\n", offsetof(saber_request_state, {name}));\n'
     prog += "return 0;}\n"
     with tempfile.TemporaryDirectory() as d:
         c = os.path.join(d, "l.c")
@@ -68,13 +73,14 @@ def test_struct_layouts_match_header():
     for s in STRUCTS:
         assert int(got[s]) == C.sizeof(getattr(N, s)), s
     for prefix, cls in (("row", N.saber_traj_row), ("desc", N.saber_sweep_desc),
-                        ("spec", N.saber_traj_spec)):
+                        ("spec", N.saber_traj_spec), ("rbo", N.saber_run_batch_out),
+                        ("rst", N.saber_request_state)):
         for name, _ in cls._fields_:
             assert int(got[f"{prefix}.{name}"]) == getattr(cls, name).offset, (prefix, name)
 
 
 def test_abi_version():
-    assert N.lib().saber_cuda_abi_version() == 1
+    assert N.lib().saber_cuda_abi_version() == N.ABI_VERSION == 2
 
 
 def test_validation_mirrors_reference_errors():
