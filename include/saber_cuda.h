@@ -22,6 +22,8 @@
  *   saber_cuda_predict_table  <- double predict(const SpeedModel&, int)       estimator.hpp:39
  *   saber_cuda_generate       <- std::vector<Request> generate(const WorkloadSpec&)
  *                                 workload.hpp:31, workload.cpp:52-79 (batched)
+ *   saber_cuda_trace_from_csv / _to_csv <- trace_from_csv / trace_to_csv
+ *                                 workload.hpp:38-39, workload.cpp:87-138
  *
  * Conventions: plain C, POD structs, caller-owned memory, no exceptions.  Every
  * function returns a saber_status; on failure saber_cuda_last_error() holds a
@@ -343,6 +345,20 @@ saber_status saber_cuda_generate(const saber_workload_spec* specs, int32_t n_spe
                                  saber_request* out, int32_t max_n);
 
 /* --------------------------------------------------------------------------
+ * Trace CSV round trip (host-side, no device) <-
+ *   std::vector<Request> trace_from_csv(const std::string&)  workload.hpp:39, workload.cpp:97-138
+ *   std::string trace_to_csv(const std::vector<Request>&)    workload.hpp:38, workload.cpp:87-95
+ * from_csv parses `len` bytes of `text`; *n_out = rows; SABER_ECAPACITY when
+ * out is NULL or cap < rows (call again with a larger buffer).  to_csv writes
+ * a NUL-terminated text; *len_out = its length without the NUL;
+ * SABER_ECAPACITY when cap <= *len_out.
+ * -------------------------------------------------------------------------- */
+saber_status saber_cuda_trace_from_csv(const char* text, size_t len, saber_request* out,
+                                       int32_t cap, int32_t* n_out);
+saber_status saber_cuda_trace_to_csv(const saber_request* requests, int32_t n, char* buf,
+                                     size_t cap, size_t* len_out);
+
+/* --------------------------------------------------------------------------
  * Monte-Carlo sweep with bursty arrivals (BASELINE config 5; no reference
  * counterpart: the reference generator is Poisson only, workload.cpp:60).
  * Trajectory k (0 <= k < n_traj) simulates cell k % n_cells of the grid
@@ -438,6 +454,9 @@ typedef struct {
 
 /* Number of samples profile() yields for one spec (host-side, no device). */
 int64_t saber_cuda_profile_samples(const saber_profile_spec* spec);
+/* planned_distinct_loads(num_requests, l_max) (calibration.hpp, calibration.cpp:45-56):
+ * distinct burst sizes a profiling budget reaches (host-side, no device). */
+int32_t saber_cuda_profile_planned_loads(int32_t num_requests, int32_t l_max);
 saber_status saber_cuda_profile_batch(const saber_profile_desc* desc, saber_profile_out* out);
 
 /* --------------------------------------------------------------------------
@@ -458,12 +477,22 @@ typedef struct {
   /* per family f (0..2) and curve c: index [f * n_curves + c] */
   double* params;          /* [3 * n_curves][3]: fitted params or FitError best params */
   double* r2;              /* fit_r2, or FitError best_sse when status != 0 */
-  int32_t* status;         /* 0 ok, 1 FitError (estimator.hpp:46-58), -1 not fitted */
-  int32_t* best_family;    /* [n_curves] calibrate(): -1 when no family fit */
+  int32_t* status;         /* 0 ok, -1 not fitted, > 0 FitError (estimator.hpp:46-58)
+                              with the reason SABER_FITERR_* */
+  int32_t* best_family;    /* [n_curves] calibrate(): the selected family; -1 when no
+                              family fit; -(2 + d) when only d < 3 distinct loads */
   int32_t* iterations;     /* [3 * n_curves] total LM iterations over the 5 starts (or NULL) */
   double device_ms;
   int32_t kernel_launches;
 } saber_fit_out;
+
+/* FitError reasons (estimator.cpp:208-346), i.e. FitError::what():
+ *   TOO_FEW            "too few samples or distinct loads to fit <family>"
+ *   NO_CONVERGENCE     "optimizer did not converge for <family>"
+ *   INCREASING_LINEAR  "fitted linear model is increasing in load"
+ *   NOT_MONOTONE       "fitted model is not non-increasing in load" */
+enum { SABER_FITERR_TOO_FEW = 1, SABER_FITERR_NO_CONVERGENCE = 2,
+       SABER_FITERR_INCREASING_LINEAR = 3, SABER_FITERR_NOT_MONOTONE = 4 };
 
 saber_status saber_cuda_fit_batch(const saber_fit_desc* desc, saber_fit_out* out);
 

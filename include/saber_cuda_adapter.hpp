@@ -43,6 +43,18 @@ namespace detail {
 inline const char* kTask[4] = {"code_qna", "code_generation", "code_summary", "code_translation"};
 inline const char* kFamily[3] = {"usl", "logistic", "linear"};  // ModelFamily names
 
+// FitError::what() of the engine's reason code (saber_cuda.h SABER_FITERR_*).
+inline std::string fit_error_message(int kind, int family) {
+  switch (kind) {
+    case SABER_FITERR_TOO_FEW:
+      return std::string("too few samples or distinct loads to fit ") + kFamily[family];
+    case SABER_FITERR_NO_CONVERGENCE:
+      return std::string("optimizer did not converge for ") + kFamily[family];
+    case SABER_FITERR_INCREASING_LINEAR: return "fitted linear model is increasing in load";
+    default: return "fitted model is not non-increasing in load";
+  }
+}
+
 inline int task_index(const std::string& name) {
   for (int t = 0; t < 4; ++t)
     if (name == kTask[t]) return t;
@@ -396,8 +408,7 @@ inline SpeedModel fit(const std::vector<LoadSpeedSample>& samples, ModelFamily f
   o.status = status;
   detail::check(saber_cuda_fit_batch(&d, &o));
   const std::array<double, 3> p = {params[3 * f], params[3 * f + 1], params[3 * f + 2]};
-  if (status[f] != 0)
-    throw FitError(std::string("fit failed for ") + detail::kFamily[f], family, p, r2[f]);
+  if (status[f] != 0) throw FitError(detail::fit_error_message(status[f], f), family, p, r2[f]);
   SpeedModel m;
   m.family = family;
   m.params = p;
@@ -423,7 +434,9 @@ inline CalibrationReport calibrate(const std::vector<LoadSpeedSample>& samples, 
   o.status = status;
   o.best_family = &best;
   detail::check(saber_cuda_fit_batch(&d, &o));
-  if (best == -2) throw CalibrationError("calibrate: insufficient distinct loads");
+  if (best <= -2)
+    throw CalibrationError("calibrate: insufficient distinct loads (" + std::to_string(-2 - best) +
+                           " < 3)");
   if (best == -1) throw CalibrationError("calibrate: no model family produced a fit");
   CalibrationReport rep;
   for (int f = 0; f < 3; ++f) {
@@ -435,7 +448,7 @@ inline CalibrationReport calibrate(const std::vector<LoadSpeedSample>& samples, 
       e.model.params = {params[3 * f], params[3 * f + 1], params[3 * f + 2]};
       e.model.fit_r2 = r2[f];
     } else {
-      e.error = std::string("fit failed for ") + detail::kFamily[f];
+      e.error = detail::fit_error_message(status[f], f);
     }
     rep.fits.push_back(e);
   }

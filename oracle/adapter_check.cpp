@@ -172,13 +172,30 @@ int main() {
     const auto fa = saber::fit(sa, saber::ModelFamily::Usl);
     const auto fb = saber::cuda::fit(sb, saber::ModelFamily::Usl);
     expect(saber::to_json(fa) == saber::to_json(fb), "fit usl");
-    bool threw = false;
-    try {
-      saber::cuda::fit({{1, 10.0}, {2, 12.0}}, saber::ModelFamily::Linear);
-    } catch (const saber::FitError& e) {
-      threw = e.family == saber::ModelFamily::Linear;
-    }
-    expect(threw, "FitError for an increasing linear fit");
+    // FitError / CalibrationError: same type, family, message and payload
+    auto fit_error = [](auto&& call) -> std::string {
+      try {
+        call();
+      } catch (const saber::FitError& e) {
+        return std::string("FitError ") + saber::to_string(e.family) + " " + e.what() + " " +
+               std::to_string(e.best_sse);
+      } catch (const saber::CalibrationError& e) {
+        return std::string("CalibrationError ") + e.what();
+      }
+      return "no error";
+    };
+    const std::vector<saber::LoadSpeedSample> rising = {{1, 10.0}, {2, 12.0}};
+    const std::vector<saber::LoadSpeedSample> two = {{1, 10.0}, {2, 9.0}, {2, 8.5}};
+    expect(fit_error([&] { saber::fit(rising, saber::ModelFamily::Linear); }) ==
+               fit_error([&] { saber::cuda::fit(rising, saber::ModelFamily::Linear); }),
+           "FitError increasing linear");
+    expect(fit_error([&] { saber::fit(two, saber::ModelFamily::Usl); }) ==
+               fit_error([&] { saber::cuda::fit(two, saber::ModelFamily::Usl); }),
+           "FitError too few loads");
+    expect(fit_error([&] { saber::calibrate(two); }) ==
+               fit_error([&] { saber::cuda::calibrate(two); }),
+           "CalibrationError insufficient loads");
+    std::printf("%s\n", fit_error([&] { saber::cuda::calibrate(two); }).c_str());
   } catch (const std::exception& e) {
     std::printf("EXCEPTION %s\n", e.what());
     return 2;

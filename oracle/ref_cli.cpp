@@ -1,18 +1,13 @@
-// saber_sim_cuda — the reference CLI surface (proj/tools/saber_sim.cpp:347-439)
-// on the B200 engine: same subcommands (calibrate / run / sweep), flags,
-// output files, SABER_SIM_SEED default and exit codes (0 ok, 2 usage, 3
-// runtime).  Inputs and outputs go through the reference's own JSON / CSV
-// code (saber_core), the computation through saber::cuda (the drop-in
-// adapter over the C ABI, include/saber_cuda_adapter.hpp), so every output
-// file is byte-identical to the CPU tool's.  CLI11 is not on this image; the
-// argument parser below accepts the CLI11 forms the reference uses
-// (`--flag value`, `--flag=value`, and the one boolean `--with-saber`).
+// ref_cli.cpp — TEST INFRASTRUCTURE ONLY.
 //
-// `--backend ref` (not in the reference) runs the reference's own CPU
-// functions instead, so tests can diff the two tools' outputs file by file.
-//
-// Built by oracle/Makefile (it links the compiled reference library for the
-// I/O): oracle/_ref/saber_sim_cuda.
+// The reference's CLI surface (proj/tools/saber_sim.cpp:347-439) rebuilt on the
+// UNMODIFIED reference library (oracle/_ref/libsaber_ref.so): the reference
+// tool needs CLI11, which is not on this image, so this file supplies an
+// argument parser for the CLI11 forms the reference uses (`--flag value`,
+// `--flag=value`, the boolean `--with-saber`) around the reference's own
+// calibrate / run / sweep calls and writers.  tests/test_cli.py diffs the
+// product CLI (paper_2506_19677_b200/bin/saber_sim_b200) against it file by
+// file.  Built by oracle/Makefile into oracle/_ref/saber_sim_ref.
 #include <cerrno>
 #include <cstdint>
 #include <cstdlib>
@@ -28,7 +23,10 @@
 
 #include "json.hpp"  // nlohmann 3.11.3, the reference's JSON library
 #include "saber/text_io.hpp"
-#include "saber_cuda_adapter.hpp"
+#include "saber/calibration.hpp"
+#include "saber/metrics.hpp"
+#include "saber/scheduler.hpp"
+#include "saber/simloop.hpp"
 
 namespace fs = std::filesystem;
 
@@ -41,7 +39,6 @@ struct UsageError : std::runtime_error {
   using std::runtime_error::runtime_error;
 };
 
-bool g_cpu = false;  // --backend ref
 
 std::string slurp(const fs::path& p) {
   std::ifstream in(p, std::ios::binary);
@@ -188,7 +185,7 @@ Args parse_args(int argc, char** argv, int first, const std::vector<std::string>
       a.with_saber = true;
       continue;
     }
-    bool ok = tok == "--backend";
+    bool ok = false;
     for (const auto& k : known) ok = ok || tok == k;
     if (!ok) throw UsageError("unknown option " + tok);
     if (!inline_val) {
@@ -196,11 +193,6 @@ Args parse_args(int argc, char** argv, int first, const std::vector<std::string>
       val = argv[++i];
     }
     a.opt[tok] = val;
-  }
-  if (a.has("--backend")) {
-    const std::string& b = a.get("--backend");
-    if (b != "cuda" && b != "ref") throw UsageError("--backend: expected cuda or ref");
-    g_cpu = b == "ref";
   }
   return a;
 }
@@ -236,8 +228,8 @@ int cmd_calibrate(const Args& a) {
   spec.seed = seed;
   spec.length_jitter = a.has("--jitter") ? unit_range(a, "--jitter") : 0.2;
   const saber::EngineConfig engine;
-  const auto s = g_cpu ? saber::profile(engine, spec, l_max) : saber::cuda::profile(engine, spec, l_max);
-  const auto report = g_cpu ? saber::calibrate(s) : saber::cuda::calibrate(s);
+  const auto s = saber::profile(engine, spec, l_max);
+  const auto report = saber::calibrate(s);
   const fs::path out(a.get("--out"));
   put_file(out / "samples.csv", saber::samples_to_csv(s));
   put_file(out / "models.json", saber::to_json(report));
@@ -277,7 +269,7 @@ int cmd_run(const Args& a) {
     throw UsageError("saber scheduler requires --model");
   if (cfg.scheduler.mode == saber::SchedulerMode::Static && cfg.scheduler.static_batch_size < 1)
     throw UsageError("static scheduler requires --cap");
-  const saber::RunOutput r = g_cpu ? saber::run(cfg) : saber::cuda::run(cfg);
+  const saber::RunOutput r = saber::run(cfg);
   const fs::path out(a.get("--out"));
   put_file(out / "records.csv", saber::records_to_csv(r.records));
   put_file(out / "decisions.csv", saber::decisions_to_csv(r.decisions));
@@ -323,7 +315,7 @@ int cmd_sweep(const Args& a) {
   }
   grid.with_saber = a.with_saber;
   if (grid.with_saber && !base.model) throw UsageError("--with-saber requires --model");
-  const saber::SweepResult res = g_cpu ? saber::sweep(grid, base, jobs) : saber::cuda::sweep(grid, base, jobs);
+  const saber::SweepResult res = saber::sweep(grid, base, jobs);
   const fs::path out(a.get("--out"));
   put_file(out / "results.csv", saber::results_to_csv(res.rows));
   put_file(out / "summary.json", saber::summary_to_json(res));
@@ -332,15 +324,14 @@ int cmd_sweep(const Args& a) {
 }
 
 const char* kUsage =
-    "usage: saber_sim_cuda {calibrate|run|sweep} --out DIR [options]\n"
+    "usage: saber_sim_ref {calibrate|run|sweep} --out DIR [options]\n"
     "  calibrate: --lmax N --samples N --seed S --mix ID|FILE --jitter X\n"
     "  run:       --config FILE --mix ID|FILE --rps X --requests N --scheduler saber|static\n"
     "             --cap N --model FILE --window N --tick X --jitter X --prefill-rate X\n"
     "             --horizon X --seed S\n"
     "  sweep:     --config FILE --mixes LIST --rps LIST --caps LIST --with-saber --model FILE\n"
     "             --repeats N --requests N --window N --tick X --jitter X --prefill-rate X\n"
-    "             --jobs N --seed S\n"
-    "  (all)      --backend cuda|ref   (ref: the reference CPU functions, for diffing)\n";
+    "             --jobs N --seed S\n";
 
 }  // namespace
 

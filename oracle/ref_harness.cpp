@@ -316,4 +316,38 @@ int ref_sweep(const orc_sim_config* base, const int32_t* mix_ids,
   });
 }
 
+// trace_from_csv / trace_to_csv (workload.cpp:87-138) for the trace parity
+// tests; requests in orc_request form.
+int ref_trace_from_csv(const char* text, orc_request* out, int32_t cap, int32_t* n) {
+  return guarded([&] {
+    const auto reqs = saber::trace_from_csv(text);
+    *n = static_cast<int32_t>(reqs.size());
+    for (std::size_t i = 0; i < reqs.size() && static_cast<int32_t>(i) < cap; ++i) {
+      out[i].arrival_time = reqs[i].arrival_time;
+      out[i].sla_seconds = reqs[i].sla_seconds;
+      out[i].deadline = reqs[i].deadline;
+      out[i].input_tokens = reqs[i].input_tokens;
+      out[i].max_output_tokens = reqs[i].max_output_tokens;
+      out[i].task = task_index(reqs[i].task);
+    }
+  });
+}
+
+int ref_trace_to_csv(const orc_request* rq, int32_t n, char* buf, size_t cap, size_t* len) {
+  return guarded([&] {
+    std::vector<saber::Request> reqs(static_cast<std::size_t>(n));
+    for (int32_t i = 0; i < n; ++i) {
+      saber::Request& r = reqs[static_cast<std::size_t>(i)];
+      r.id = static_cast<uint64_t>(i);
+      r.task = kTaskName[rq[i].task];
+      r.arrival_time = rq[i].arrival_time;
+      r.input_tokens = rq[i].input_tokens;
+      r.max_output_tokens = rq[i].max_output_tokens;
+    }
+    const std::string s = saber::trace_to_csv(reqs);
+    *len = s.size();
+    if (cap > s.size()) std::memcpy(buf, s.c_str(), s.size() + 1);
+  });
+}
+
 }  // extern "C"

@@ -224,6 +224,11 @@ SYMBOLS = [
     ("saber_cuda_generate", C.c_int, [_P(saber_workload_spec), C.c_int32, C.c_int32,
                                       _P(saber_request), C.c_int32]),
     ("saber_cuda_release_cache", C.c_int, [C.c_int32]),
+    ("saber_cuda_profile_planned_loads", C.c_int32, [C.c_int32, C.c_int32]),
+    ("saber_cuda_trace_from_csv", C.c_int, [C.c_char_p, C.c_size_t, _P(saber_request), C.c_int32,
+                                            _P(C.c_int32)]),
+    ("saber_cuda_trace_to_csv", C.c_int, [_P(saber_request), C.c_int32, C.c_char_p, C.c_size_t,
+                                          _P(C.c_size_t)]),
     ("saber_cuda_last_error", C.c_char_p, []),
     ("saber_cuda_abi_version", C.c_int32, []),
     ("saber_cuda_device_count", C.c_int32, []),

@@ -8,6 +8,7 @@ caller of the reference finds the same surface:
     run(config)                     -> RunOutput        simloop.hpp:49
     run_with_requests(config, reqs) -> RunOutput        simloop.hpp:53-54
     generate(spec)                  -> List[Request]    workload.hpp:31
+    trace_from_csv / trace_to_csv                       workload.hpp:38-39
     fit(samples, family)            -> SpeedModel       estimator.hpp:61
     calibrate(samples)              -> CalibrationReport calibration.hpp:54
     predict(model, load), max_speed(model)              estimator.hpp:39-42
@@ -541,6 +542,39 @@ def generate(spec: WorkloadSpec, device: int = 0) -> List[Request]:
             for i, q in enumerate(out)]
 
 
+def trace_from_csv(text: str) -> List[Request]:
+    """workload.cpp:97-138 (saber_cuda_trace_from_csv): the replay workload of a
+    trace CSV; raises InvalidArgument with the reference's messages."""
+    raw = text.encode()
+    n = C.c_int32(0)
+    st = N.lib().saber_cuda_trace_from_csv(raw, len(raw), None, 0, C.byref(n))
+    if st != N.SABER_ECAPACITY:
+        _check(st)
+    buf = (N.saber_request * max(1, n.value))()
+    _check(N.lib().saber_cuda_trace_from_csv(raw, len(raw), buf, n.value, C.byref(n)))
+    return [Request(i, TASK_NAMES[q.task], q.arrival_time, q.input_tokens, q.max_output_tokens,
+                    q.sla_seconds, q.deadline) for i, q in enumerate(buf[: n.value])]
+
+
+def trace_to_csv(requests: Sequence[Request]) -> str:
+    """workload.cpp:87-95 (saber_cuda_trace_to_csv)."""
+    arr = (N.saber_request * max(1, len(requests)))()
+    for i, r in enumerate(requests):
+        if r.task not in TASK_INDEX:
+            raise InvalidArgument(f"trace csv: unknown task {r.task}")
+        arr[i].arrival_time = r.arrival_time
+        arr[i].input_tokens = r.input_tokens
+        arr[i].max_output_tokens = r.max_output_tokens
+        arr[i].task = TASK_INDEX[r.task]
+    need = C.c_size_t(0)
+    st = N.lib().saber_cuda_trace_to_csv(arr, len(requests), None, 0, C.byref(need))
+    if st != N.SABER_ECAPACITY:
+        _check(st)
+    buf = C.create_string_buffer(need.value + 1)
+    _check(N.lib().saber_cuda_trace_to_csv(arr, len(requests), buf, need.value + 1, C.byref(need)))
+    return buf.value.decode()
+
+
 # ---------------------------------------------------------------- sweep path
 class SweepPlan:
     """Staged sweep (saber_cuda_sweep_plan_*): create once, run many times."""
@@ -749,8 +783,8 @@ class CalibrationReport:
 class FitBatchResult:
     params: np.ndarray       # [3 families][n_curves][3]
     r2: np.ndarray           # [3][n_curves] fit_r2, or FitError best_sse
-    status: np.ndarray       # [3][n_curves] 0 ok, 1 FitError, -1 not fitted
-    best_family: Optional[np.ndarray]  # [n_curves] (calibrate): -2 too few loads, -1 none
+    status: np.ndarray       # [3][n_curves] 0 ok, -1 not fitted, > 0 FitError reason (1..4)
+    best_family: Optional[np.ndarray]  # [n_curves] (calibrate): -(2+d) only d < 3 loads, -1 none
     iterations: np.ndarray   # [3][n_curves] LM iterations over the 5 starts
     device_ms: float
     kernel_launches: int
@@ -795,13 +829,25 @@ def _samples_arrays(samples):
     return loads, speeds
 
 
+def fit_error_message(kind: int, family: int) -> str:
+    """FitError::what() for the engine's reason code (saber_cuda.h SABER_FITERR_*)."""
+    if kind == 1:
+        return f"too few samples or distinct loads to fit {FAMILIES[family]}"
+    if kind == 2:
+        return f"optimizer did not converge for {FAMILIES[family]}"
+    if kind == 3:
+        return "fitted linear model is increasing in load"
+    return "fitted model is not non-increasing in load"
+
+
 def fit(samples, family: int, device: int = 0) -> SpeedModel:
     """estimator.cpp:241-346 on the GPU; raises FitError like the reference."""
     loads, speeds = _samples_arrays(samples)
     res = fit_batch(loads, speeds, [0, len(loads)], family_mask=1 << family, device=device)
     p = res.params[family, 0]
     if res.status[family, 0] != 0:
-        raise FitError(f"fit failed for {FAMILIES[family]}", family, p, res.r2[family, 0])
+        raise FitError(fit_error_message(int(res.status[family, 0]), family), family, p,
+                       res.r2[family, 0])
     return SpeedModel(family, tuple(float(x) for x in p), float(res.r2[family, 0]))
 
 
@@ -810,8 +856,8 @@ def calibrate(samples, device: int = 0) -> CalibrationReport:
     loads, speeds = _samples_arrays(samples)
     res = fit_batch(loads, speeds, [0, len(loads)], calibrate=True, device=device)
     b = int(res.best_family[0])
-    if b == -2:
-        raise CalibrationError("calibrate: insufficient distinct loads")
+    if b <= -2:
+        raise CalibrationError(f"calibrate: insufficient distinct loads ({-2 - b} < 3)")
     if b == -1:
         raise CalibrationError("calibrate: no model family produced a fit")
     fits = []
@@ -819,7 +865,7 @@ def calibrate(samples, device: int = 0) -> CalibrationReport:
         ok = res.status[f, 0] == 0
         fits.append(FamilyFit(f, bool(ok), SpeedModel(f, tuple(float(x) for x in res.params[f, 0]),
                                                       float(res.r2[f, 0])) if ok else None,
-                              "" if ok else f"fit failed for {FAMILIES[f]}"))
+                              "" if ok else fit_error_message(int(res.status[f, 0]), f)))
     return CalibrationReport(fits[b].model, fits)
 
 

@@ -38,6 +38,12 @@ saber_status fail(saber_status s, const std::string& msg) {
   return s;
 }
 
+}  // namespace
+
+saber_status saberb200::set_error(saber_status s, const std::string& msg) { return fail(s, msg); }
+
+namespace {
+
 #define CUDA_TRY(expr)                                                                  \
   do {                                                                                  \
     cudaError_t e_ = (expr);                                                            \
@@ -506,6 +512,18 @@ saber_status validate_sweep(const saber_sweep_desc& d) {
       return fail(SABER_EINVAL, "unknown mix preset: w" + std::to_string(d.mixes[i]));
   for (int i = 0; i < d.n_rps; ++i)
     if (!(d.rps[i] > 0.0)) return fail(SABER_EINVAL, "rps must be > 0");
+  // The reference pools grid entries by value (simloop.cpp:206-275: rows are
+  // matched on mix name, rps value and cap value); the engine's summary works
+  // per grid index, so repeated entries are rejected instead of pooled.
+  for (int i = 0; i < d.n_mixes; ++i)
+    for (int j = 0; j < i; ++j)
+      if (d.mixes[i] == d.mixes[j]) return fail(SABER_EINVAL, "sweep: duplicate mix in the grid");
+  for (int i = 0; i < d.n_rps; ++i)
+    for (int j = 0; j < i; ++j)
+      if (d.rps[i] == d.rps[j]) return fail(SABER_EINVAL, "sweep: duplicate rps in the grid");
+  for (int i = 0; i < d.n_caps; ++i)
+    for (int j = 0; j < i; ++j)
+      if (d.caps[i] == d.caps[j]) return fail(SABER_EINVAL, "sweep: duplicate cap in the grid");
   if (d.num_requests < 1) return fail(SABER_EINVAL, "num_requests must be >= 1");
   if (d.num_requests > kMaxRequests)
     return fail(SABER_EINVAL, "num_requests > " + std::to_string(kMaxRequests) +
@@ -2214,6 +2232,18 @@ extern "C" int64_t saber_cuda_profile_samples(const saber_profile_spec* spec) {
   BurstPlan plan;
   if (plan_bursts(*spec, &plan) != SABER_OK) return -1;
   return plan.issued;
+}
+
+// calibration.cpp:45-56: bursts cycle through sizes 1..l_max until the
+// budget is issued; the distinct loads are the distinct sizes reached.
+extern "C" int32_t saber_cuda_profile_planned_loads(int32_t num_requests, int32_t l_max) {
+  if (l_max < 1 || num_requests < 1) return 0;
+  int64_t issued = 0, bursts = 0;
+  for (int32_t size = 0; issued < num_requests && bursts < l_max; ++bursts) {
+    size = size % l_max + 1;
+    issued += size;
+  }
+  return static_cast<int32_t>(bursts);
 }
 
 extern "C" saber_status saber_cuda_profile_batch(const saber_profile_desc* desc,

@@ -4,10 +4,14 @@
 
 #include <cstddef>
 #include <cstdint>
+#include <string>
 
 #include "../../include/saber_cuda.h"
 
 namespace saberb200 {
+
+// Sets the message saber_cuda_last_error() returns (host.cpp); returns `s`.
+saber_status set_error(saber_status s, const std::string& msg);
 
 // Largest request count the register-bitmask trajectory kernel supports
 // (8 x 64-bit words of per-request tier masks).  Larger n is rejected with

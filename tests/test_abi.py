@@ -92,6 +92,11 @@ def test_validation_mirrors_reference_errors():
         S.sweep(S.SweepGrid(["w1"], [1.0], [], True), base)
     with pytest.raises(S.InvalidArgument, match="unknown mix preset"):
         S.sweep(S.SweepGrid(["w9"], [1.0], [10], False), base)
+    for grid in (S.SweepGrid(["w1", "w1"], [1.0], [10], False),
+                 S.SweepGrid(["w1"], [2.0, 2.0], [10], False),
+                 S.SweepGrid(["w1"], [1.0], [10, 20, 10], False)):
+        with pytest.raises(S.InvalidArgument, match="duplicate"):
+            S.sweep(grid, base)
     bad = S.SimConfig()
     bad.scheduler.tick = 0.0
     bad.model = S.SpeedModel(0, (100, 0.05, 0.001))
