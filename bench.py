@@ -166,31 +166,63 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
+# ------------------------------------------------------------ host / config --
+def host_info():
+    """CPU model, SMT state and logical core count of the box."""
+    model = None
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    smt = None
+    try:
+        smt = open("/sys/devices/system/cpu/smt/active").read().strip() == "1"
+    except OSError:
+        pass
+    return {"cpu_model": model, "smt": smt, "logical_cores": os.cpu_count()}
+
+
+def bench_config(world):
+    """The workload both arms report (key-identical, so the driver can match
+    them): config 2 over 64 seeds per GPU."""
+    return {"workload": WORKLOAD, "trajectories_per_step": len(MIXES) * len(RPS) * (len(CAPS) + 1) *
+            SEEDS_PER_GPU * world, "seeds": SEEDS_PER_GPU * world, "n_gpus": world}
+
+
 # -------------------------------------------------------------- reference --
 def reference_sample(seeds, jobs=0):
     """Time oracle/_ref (the unmodified reference compiled from its sources)
     running saber::sweep on `seeds` seeds of the same grid, all host cores."""
     import oracle as O  # noqa: E402  (CPU-baseline / reference arm only)
     ref = O.Oracle("reference")
-    base = O.make_config(mix="w3", n=N_REQ, seed=BASE_SEED,
-                         model=(O.USL, CAL_USL), gt=O.DEFAULT_GT)
-    base.has_model = 1
+    base = reference_base(O, seeds)
     t0 = time.perf_counter()
     r = ref.sweep(base, MIXES, RPS, CAPS, True, seeds, jobs=jobs)
     dt = time.perf_counter() - t0
     return r, dt
 
 
+def reference_base(O, seeds):
+    base = O.make_config(mix="w3", n=N_REQ, seed=BASE_SEED, model=(O.USL, CAL_USL), gt=O.DEFAULT_GT)
+    base.has_model = 1
+    return base
+
+
 def reference_arm(args):
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import oracle as O  # noqa: E402
     rank = env_int("RANK", 0)
+    world = env_int("WORLD_SIZE", args.gpus)
     if rank != 0:
         return 0
     cores = os.cpu_count() or 1
     rows_per_seed = len(MIXES) * len(RPS) * (len(CAPS) + 1)
-    # size the per-step sample: ~3 s of all-core CPU work per step
-    _, t1 = reference_sample(1)
-    seeds = int(max(1, min(SEEDS_PER_GPU, round(3.0 / max(t1, 1e-3)))))
+    # each step: the first 64 seeds of the workload (rank 0's shard at N = 1;
+    # a bounded sample of it at N > 1), saber::sweep on every host thread
+    seeds = SEEDS_PER_GPU
     for _ in range(args.warmup):
         reference_sample(seeds)
     times = []
@@ -199,14 +231,22 @@ def reference_arm(args):
         times.append(dt)
     rows = rows_per_seed * seeds
     value = rows * args.steps / sum(times)
+    # decisions of the same trajectories (untimed): the reference's run() over
+    # the sample's cells (saber::sweep returns no decision data)
+    dec, _ = O.sweep_decisions(reference_base(O, seeds), MIXES, RPS, CAPS, True, seeds)
+    decisions = float(dec.sum())
     sample = (f"{seeds} seed(s) x {rows_per_seed} cells = {rows} trajectories per step "
               f"(saber::sweep jobs=0 -> {cores} threads)")
     line = {"metric": METRIC, "value": value, "unit": "traj/s", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * sum(times) / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic (reference generate(): mt19937_64 Poisson arrivals)",
-            "config": {"workload": WORKLOAD, "trajectories_per_step": rows, "l2": "n/a (CPU)"},
+            "data": "synthetic (generate(): mt19937_64 Poisson arrivals, task/length draws; "
+                    f"seeds {BASE_SEED}..{BASE_SEED + seeds - 1})",
+            "config": bench_config(world),
             "impl": "reference",
+            "decisions_per_s": decisions * args.steps / sum(times),
+            "decisions_per_step": decisions,
+            "host": host_info(),
             "cpu_baseline": {"value": value, "unit": "traj/s", "cores": cores, "kind": "reference",
                              "sample": sample},
             "e2e": {"value": value, "unit": "traj/s", "h2d_bytes_per_step": 0,
@@ -419,18 +459,19 @@ def engine_arm(args):
     if rank == 0:
         cpu = None
         if world == 1 and not args.no_cpu_baseline:
-            cpu = cpu_baseline(rows, grid, base)
+            cpu = cpu_baseline(rows, summ, best, base)
         line = {
             "metric": METRIC, "value": value, "unit": "traj/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (generate(): mt19937_64 Poisson arrivals, task/length draws; "
                     f"seeds {BASE_SEED}..{BASE_SEED + base.repeats - 1})",
-            "config": {"workload": WORKLOAD, "trajectories_per_step": total_rows,
-                       "seeds": base.repeats, "l2": "flushed between steps (256 MB write)",
-                       "parallelism": f"rows strided over {world} GPU(s)",
-                       "pipelining": "none" if args.no_pipeline else
-                       "2 plans: summary of sweep k overlaps the simulation of sweep k+1"},
+            "config": bench_config(world),
+            "execution": {"l2": "flushed between steps (256 MB write)",
+                          "parallelism": f"rows strided over {world} GPU(s)",
+                          "pipelining": "none" if args.no_pipeline else
+                          "2 plans: summary of sweep k overlaps the simulation of sweep k+1"},
+            "host": host_info(),
             "decisions_per_s": decisions * args.steps / (total_ms / 1e3),
             "decisions_per_step": decisions,
             "e2e": {"value": e2e_value, "unit": "traj/s", "h2d_bytes_per_step": h2d,
@@ -509,9 +550,18 @@ class _CudaView:
                                          "data": (int(ptr), False), "version": 3, "strides": None}
 
 
-def cpu_baseline(gpu_rows, grid, base):
-    """The reference on the host cores, on a bounded sample of the same
-    workload; also checks the sample's goodputs equal the GPU's rows."""
+def _same(a, b):
+    """Bitwise-equal float arrays (NaN == NaN)."""
+    a, b = np.asarray(a, dtype=np.float64), np.asarray(b, dtype=np.float64)
+    return bool(a.shape == b.shape and np.array_equal(a.view(np.uint64), b.view(np.uint64)))
+
+
+def cpu_baseline(gpu_rows, summ, best, base):
+    """The reference on the host cores: saber::sweep over the same 64 seeds
+    (the whole N = 1 workload), timed; then every row's goodput / ratio mean /
+    std / cv, the per-mix summary and the best caps compared bit for bit with
+    the GPU's, and the decision counts and digests of 8 seeds' rows (the
+    reference's run() over those cells, untimed)."""
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     try:
         import oracle as O  # noqa: F401
@@ -520,23 +570,28 @@ def cpu_baseline(gpu_rows, grid, base):
     except ImportError:
         return None
     cores = os.cpu_count() or 1
-    _, t1 = reference_sample(1)
-    seeds = int(max(1, min(SEEDS_PER_GPU, round(15.0 / max(t1, 1e-3)))))
+    seeds = base.repeats
     r, dt = reference_sample(seeds)
-    rows_per_seed = len(MIXES) * len(RPS) * (len(CAPS) + 1)
-    n = rows_per_seed * seeds
-    # GPU rows for the same (mix, rps, variant, seed) keys
-    R = base.repeats
-    per_cell = len(CAPS) + 1
-    idx = []
-    for c in range(len(MIXES) * len(RPS) * per_cell):
-        for s in range(seeds):
-            idx.append(c * R + s)
-    same = bool(np.array_equal(gpu_rows["goodput"][np.array(idx)], r["goodput"]))
+    n = len(MIXES) * len(RPS) * (len(CAPS) + 1) * seeds
+    checks = {k: _same(gpu_rows[k], r[k]) for k in ("goodput", "ratio_mean", "ratio_std", "cv")}
+    gsum = np.array([[s.saber_mean_goodput, s.best_static_mean_goodput, s.delta, s.saber_pooled_cv,
+                      s.best_static_pooled_cv, s.saber_rps_mean_cv, s.best_static_rps_mean_cv]
+                     for s in summ])
+    checks["summary"] = _same(gsum, r["summary"])
+    checks["best_cap"] = bool(np.array_equal(np.asarray(best), r["best_cap"]))
+    hs = 8
+    dec, hsh = O.sweep_decisions(reference_base(O, hs), MIXES, RPS, CAPS, True, hs)
+    idx = np.array([c * seeds + k for c in range(len(MIXES) * len(RPS) * (len(CAPS) + 1))
+                    for k in range(hs)])
+    checks["decisions"] = bool(np.array_equal(gpu_rows["decisions"][idx], dec))
+    checks["decision_hash"] = bool(np.array_equal(gpu_rows["decision_hash"][idx].astype(np.uint64), hsh))
     return {"value": n / dt, "unit": "traj/s", "cores": cores, "kind": "reference",
             "sample": f"saber::sweep over seeds {BASE_SEED}..{BASE_SEED + seeds - 1} of the same grid "
-                      f"({n} trajectories, {dt:.1f} s, jobs=0)",
-            "same_goodput_rows": n, "same_goodput": same}
+                      f"({n} trajectories, {dt:.2f} s, jobs=0)",
+            "same_goodput_rows": n, "same_goodput": checks["goodput"],
+            "parity": checks, "parity_ok": all(checks.values()),
+            "parity_scope": f"rows/summary/best caps: all {n}; decision counts+digests: "
+                            f"{len(idx)} rows (seeds {BASE_SEED}..{BASE_SEED + hs - 1})"}
 
 
 def main():

@@ -319,6 +319,26 @@ class Oracle:
                 "best_cap": np.array(best[:]).reshape(len(mixes), len(rps))}
 
 
+def sweep_decisions(base: OrcSimConfig, mixes, rps, caps, with_saber, repeats, jobs=0):
+    """Per-row decision counts and digests of a sweep, from the compiled
+    reference's run() over the sweep's cells (ref_sweep_decisions)."""
+    lib = C.CDLL(REFERENCE_SO)
+    f = lib.ref_sweep_decisions
+    mix_ids = (C.c_int32 * len(mixes))(*[int(m[1:]) for m in mixes])
+    rps_a = (C.c_double * len(rps))(*rps)
+    caps_a = (C.c_int32 * max(1, len(caps)))(*caps)
+    n_rows = len(mixes) * len(rps) * (len(caps) * repeats + (repeats if with_saber else 0))
+    dec = np.zeros(n_rows, dtype=np.int64)
+    hs = np.zeros(n_rows, dtype=np.uint64)
+    rc = f(C.byref(base), mix_ids, len(mixes), rps_a, len(rps), caps_a, len(caps),
+           1 if with_saber else 0, repeats, jobs, dec.ctypes.data_as(C.c_void_p),
+           hs.ctypes.data_as(C.c_void_p))
+    if rc != 0:
+        lib.ref_last_error.restype = C.c_char_p
+        raise OracleError(lib.ref_last_error().decode())
+    return dec, hs
+
+
 def reference_available() -> bool:
     return os.path.exists(REFERENCE_SO)
 

@@ -8,6 +8,10 @@
 // the plain-C signatures of oracle/oracle.h (prefix ref_), so tests and the
 // bench's reference arm can drive the real reference on the same inputs as
 // the CUDA engine.
+#include <atomic>
+#include <mutex>
+#include <thread>
+#include <algorithm>
 #include <cmath>
 #include <cstring>
 #include <exception>
@@ -140,6 +144,16 @@ void fill_out(const saber::RunOutput& o, orc_traj_out* out, orc_record* recs,
   out->rng_draws = -1;
   out->last_arrival = o.requests.empty() ? 0.0 : o.requests.back().arrival_time;
   out->horizon = NAN;
+}
+
+orc_mix to_orc_mix(const saber::WorkloadMix& m) {
+  orc_mix x{};
+  for (const auto& [name, frac] : m.proportions) {
+    const int t = task_index(name);
+    x.frac[t] = frac;
+    x.present[t] = 1;
+  }
+  return x;
 }
 
 template <class F>
@@ -313,6 +327,57 @@ int ref_sweep(const orc_sim_config* base, const int32_t* mix_ids,
           best_cap[i * n_rps + k] = it == s.best_cap_by_rps.end() ? 0 : it->second;
         }
     }
+  });
+}
+
+// The decision logs of a sweep's cells, in the sweep's row order (the cell
+// configs simloop.cpp:137-163 builds), each cell through saber::run on a
+// pool of `jobs` threads: per row the decision count and the digest of
+// oracle.h.  saber::sweep itself returns no decision data.
+int ref_sweep_decisions(const orc_sim_config* base, const int32_t* mix_ids, int32_t n_mixes,
+                        const double* rps, int32_t n_rps, const int32_t* caps, int32_t n_caps,
+                        int32_t with_saber, int32_t repeats, int32_t jobs, int64_t* decisions,
+                        uint64_t* hashes) {
+  return guarded([&] {
+    std::vector<orc_sim_config> cells;
+    for (int32_t m = 0; m < n_mixes; ++m)
+      for (int32_t r = 0; r < n_rps; ++r) {
+        orc_sim_config c = *base;
+        c.mix = to_orc_mix(saber::preset_mix("w" + std::to_string(mix_ids[m])));
+        c.rps = rps[r];
+        for (int32_t k = 0; k <= n_caps; ++k) {
+          if (k == n_caps && !with_saber) break;
+          for (int32_t i = 0; i < repeats; ++i) {
+            orc_sim_config x = c;
+            x.workload_seed = x.seed = base->seed + static_cast<uint64_t>(i);
+            x.mode = k < n_caps ? ORC_STATIC : ORC_SABER;
+            x.cap = k < n_caps ? caps[k] : 0;
+            x.has_model = k < n_caps ? 0 : base->has_model;
+            cells.push_back(x);
+          }
+        }
+      }
+    std::atomic<std::size_t> next{0};
+    std::string err;
+    std::mutex mu;
+    auto worker = [&] {
+      for (std::size_t i = next++; i < cells.size(); i = next++) {
+        try {
+          orc_traj_out o{};
+          fill_out(saber::run(to_config(cells[i])), &o, nullptr, nullptr, 0, nullptr);
+          decisions[i] = o.decisions;
+          hashes[i] = o.decision_hash;
+        } catch (const std::exception& e) {
+          std::lock_guard<std::mutex> lk(mu);
+          err = e.what();
+        }
+      }
+    };
+    const int n = jobs > 0 ? jobs : static_cast<int>(std::max(1u, std::thread::hardware_concurrency()));
+    std::vector<std::thread> pool;
+    for (int t = 0; t < n; ++t) pool.emplace_back(worker);
+    for (auto& t : pool) t.join();
+    if (!err.empty()) throw std::runtime_error(err);
   });
 }
 
