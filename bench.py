@@ -504,7 +504,8 @@ def engine_arm(args):
 
 
 def _one_shot(S, grid, base, device):
-    """One saber_cuda_sweep call: host buffers in and out."""
+    """One saber_cuda_sweep call: host buffers in and out (what the drop-in
+    saber::cuda::sweep issues, include/saber_cuda_adapter.hpp)."""
     import ctypes as C
     N = S._native
     p = S.SweepPlan.__new__(S.SweepPlan)
@@ -530,11 +531,13 @@ def _one_shot(S, grid, base, device):
     d.device = device
     d.shard_index, d.shard_count = 0, 1
     n_rows = int(N.lib().saber_cuda_sweep_rows(C.byref(d)))
-    rows = np.empty(n_rows, dtype=S.ROW_DTYPE)
+    # the SweepResult payload of the reference's sweep(): per row the four
+    # statistics (saber_row_stats) plus the per-mix summary and best caps
+    stats = (N.saber_row_stats * n_rows)()
     summ = (N.saber_mix_summary * len(grid.mixes))()
     best = np.empty((len(grid.mixes), len(grid.rps_list)), dtype=np.int32)
     o = N.saber_sweep_out()
-    o.rows = rows.ctypes.data_as(C.POINTER(N.saber_traj_row))
+    o.row_stats = stats
     o.summary = summ
     o.best_cap_by_rps = best.ctypes.data_as(C.POINTER(C.c_int32))
     S.api._check(N.lib().saber_cuda_sweep(C.byref(d), C.byref(o)))

@@ -171,6 +171,15 @@ typedef struct {
   double best_static_rps_mean_cv;
 } saber_mix_summary;
 
+/* The reference's SweepRow payload (simloop.hpp:63-73): the four statistics
+ * of a row; its keys (mix, rps, scheduler, cap, seed) follow from the grid order. */
+typedef struct {
+  double goodput;
+  double ratio_mean;  /* NaN when nothing completed */
+  double ratio_std;
+  double cv;
+} saber_row_stats;
+
 typedef struct {
   saber_traj_row* rows;            /* [n_rows] or NULL */
   double* completion_times;        /* [n_rows][num_requests] or NULL (NaN = never) */
@@ -182,6 +191,9 @@ typedef struct {
   int32_t kernel_launches;
   int64_t h2d_bytes;               /* host->device bytes of the inputs (plan create) */
   int64_t d2h_bytes;               /* device->host bytes of the results (fetch) */
+  /* ABI 2: [n_rows] or NULL — just the SweepRow statistics (32 B per row
+   * instead of the 280 B saber_traj_row), packed on the device */
+  saber_row_stats* row_stats;
 } saber_sweep_out;
 
 /* Number of rows a sweep produces (= SweepResult::rows.size()). */

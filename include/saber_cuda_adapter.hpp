@@ -340,11 +340,11 @@ inline SweepResult sweep(const SweepGrid& grid, const SimConfig& base, int jobs 
   d.shard_index = 0;
   d.shard_count = 1;
   const int64_t n_rows = saber_cuda_sweep_rows(&d);
-  std::vector<saber_traj_row> rows(static_cast<size_t>(n_rows > 0 ? n_rows : 0));
+  std::vector<saber_row_stats> rows(static_cast<size_t>(n_rows > 0 ? n_rows : 0));
   std::vector<saber_mix_summary> summ(mixes.size());
   std::vector<int32_t> best(mixes.size() * rps.size());
   saber_sweep_out o{};
-  o.rows = rows.data();
+  o.row_stats = rows.data();
   o.summary = summ.data();
   o.best_cap_by_rps = best.data();
   detail::check(saber_cuda_sweep(&d, &o));

@@ -70,12 +70,18 @@ class saber_mix_summary(C.Structure):
                 ("best_static_rps_mean_cv", C.c_double)]
 
 
+class saber_row_stats(C.Structure):
+    _fields_ = [("goodput", C.c_double), ("ratio_mean", C.c_double), ("ratio_std", C.c_double),
+                ("cv", C.c_double)]
+
+
 class saber_sweep_out(C.Structure):
     _fields_ = [
         ("rows", C.POINTER(saber_traj_row)), ("completion_times", C.POINTER(C.c_double)),
         ("summary", C.POINTER(saber_mix_summary)), ("best_cap_by_rps", C.POINTER(C.c_int32)),
         ("n_rows", C.c_int64), ("device_ms", C.c_double), ("kernel_launches", C.c_int32),
         ("h2d_bytes", C.c_int64), ("d2h_bytes", C.c_int64),
+        ("row_stats", C.POINTER(saber_row_stats)),
     ]
 
 

@@ -470,7 +470,7 @@ struct saber_sweep_plan {
 
   Workloads wl;
   DevBuf tables, seeds, s_off, s_len, draws, descs, rows, comp, cursor, err, caps_d;
-  DevBuf summary, best_cap, cell_scratch, ratios, order;
+  DevBuf summary, best_cap, cell_scratch, ratios, order, stats;
   Scratch scratch;
   TickTableBuf ticktab;
   int32_t n_saber_first = 0;  // SABER rows lead the order: split launch
@@ -1072,12 +1072,20 @@ saber_status saber_cuda_sweep_plan_fetch(saber_sweep_plan* P, saber_sweep_out* o
   out->h2d_bytes = P->h2d_bytes;
   out->d2h_bytes = 0;
   if (out->rows) out->d2h_bytes += static_cast<int64_t>(P->n_rows) * sizeof(saber_traj_row);
+  if (out->row_stats) out->d2h_bytes += static_cast<int64_t>(P->n_rows) * sizeof(saber_row_stats);
   if (out->completion_times) out->d2h_bytes += static_cast<int64_t>(P->n_rows) * P->n * 8;
   if (out->summary) out->d2h_bytes += P->desc.n_mixes * static_cast<int64_t>(sizeof(saber_mix_summary));
   if (out->best_cap_by_rps) out->d2h_bytes += static_cast<int64_t>(P->desc.n_mixes) * P->desc.n_rps * 4;
   if (out->rows)
     CUDA_TRY(cudaMemcpy(out->rows, P->rows.p, static_cast<size_t>(P->n_rows) * sizeof(saber_traj_row),
                         cudaMemcpyDeviceToHost));
+  if (out->row_stats) {
+    const size_t bytes = static_cast<size_t>(P->n_rows) * sizeof(saber_row_stats);
+    if (!P->stats.p) ALLOC_TRY(P->stats, P->device, bytes);
+    LAUNCH_TRY(launch_pack_row_stats(P->rows.as<saber_traj_row>(), P->n_rows,
+                                     P->stats.as<saber_row_stats>(), nullptr));
+    CUDA_TRY(cudaMemcpy(out->row_stats, P->stats.p, bytes, cudaMemcpyDeviceToHost));
+  }
   if (out->completion_times)
     CUDA_TRY(cudaMemcpy(out->completion_times, P->comp.p, static_cast<size_t>(P->n_rows) * P->n * 8,
                         cudaMemcpyDeviceToHost));

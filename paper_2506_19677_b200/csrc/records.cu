@@ -138,7 +138,25 @@ __global__ void __launch_bounds__(128) records_kernel(const RecordsParams p) {
   }
 }
 
+__global__ void __launch_bounds__(256) pack_row_stats_kernel(const saber_traj_row* rows, int64_t n,
+                                                            saber_row_stats* out) {
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const saber_traj_row& r = rows[i];
+    out[i] = saber_row_stats{r.goodput, r.ratio_mean, r.ratio_std, r.cv};
+  }
+}
+
 }  // namespace
+
+int launch_pack_row_stats(const saber_traj_row* rows, int64_t n_rows, saber_row_stats* out,
+                          void* stream) {
+  if (n_rows == 0) return 0;
+  const int64_t want = (n_rows + 255) / 256;
+  const int grid = static_cast<int>(want < 1184 ? want : 1184);
+  pack_row_stats_kernel<<<grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(rows, n_rows, out);
+  return cudaGetLastError() == cudaSuccess ? 0 : 1;
+}
 
 int launch_pack_requests(const RecordsParams& p, void* stream) {
   const int64_t cells = static_cast<int64_t>(p.n_traj) * p.wl.nmax;

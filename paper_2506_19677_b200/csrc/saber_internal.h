@@ -251,6 +251,9 @@ struct SummaryParams {
   int32_t narrow;               // 1 = few small blocks (runs beside the trajectory kernels)
 };
 int launch_summary(const SummaryParams& p, void* stream);
+// The four SweepRow statistics of every row, packed (sweep fetch).
+int launch_pack_row_stats(const saber_traj_row* rows, int64_t n_rows, saber_row_stats* out,
+                          void* stream);
 
 // Bursty Monte-Carlo sweep (mc.cu, BASELINE config 5).
 }  // namespace saberb200

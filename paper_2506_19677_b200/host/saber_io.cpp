@@ -110,7 +110,7 @@ std::string results_csv(const SweepFiles& s) {  // simloop.cpp:279-294
   std::string out = "mix,rps,scheduler,static_cap,repeat_seed,goodput,ratio_mean,ratio_std,cv\n";
   size_t k = 0;
   auto row = [&](const std::string& mix, double rps, int cap, int rep) {
-    const saber_traj_row& x = s.rows[k++];
+    const saber_row_stats& x = s.rows[k++];
     CsvLine(&out) << mix << fmt17(rps) << (cap > 0 ? "static" : "saber")
                   << (cap > 0 ? std::to_string(cap) : std::string())
                   << std::to_string(s.seed + static_cast<uint64_t>(rep)) << fmt17(x.goodput)

@@ -62,7 +62,7 @@ struct SweepFiles {
   bool with_saber = false;
   int32_t repeats = 1;
   uint64_t seed = 0;
-  std::vector<saber_traj_row> rows;         // grid order, repeats innermost
+  std::vector<saber_row_stats> rows;        // grid order, repeats innermost
   std::vector<saber_mix_summary> summary;   // per mix
   std::vector<int32_t> best_cap;            // [mix][rps]
 };

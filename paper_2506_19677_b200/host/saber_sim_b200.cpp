@@ -514,7 +514,7 @@ int sweep(const Args& a, uint64_t default_seed) {
   s.summary.resize(s.mixes.size());
   s.best_cap.resize(s.mixes.size() * s.rps.size());
   saber_sweep_out o{};
-  o.rows = s.rows.data();
+  o.row_stats = s.rows.data();
   o.summary = s.summary.data();
   o.best_cap_by_rps = s.best_cap.data();
   engine(saber_cuda_sweep(&d, &o));
