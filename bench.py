@@ -298,18 +298,28 @@ def engine_arm(args):
     if os.environ.get("SABER_BENCH_DEVICE") is not None:
         local = env_int("SABER_BENCH_DEVICE", 0)
     backend = os.environ.get("SABER_BENCH_BACKEND", "nccl")
+    # N > 1: the engine's own NCCL communicator does the final statistics
+    # reduce (saber_cuda_sweep_plan_gather); torch.distributed is plumbing
+    # only (barriers, the NCCL id broadcast, the max-over-ranks time).  The
+    # gloo hook (two ranks on one GPU, tests only) gathers with torch instead,
+    # since NCCL allows one rank per GPU.  SABER_BENCH_NCCL=1 forces the
+    # engine-NCCL path at N = 1 (tests).
+    multi = world > 1 or os.environ.get("SABER_BENCH_NCCL") == "1"
+    engine_nccl = multi and backend == "nccl"
     dist = None
-    if world > 1:
+    if multi:
         import torch.distributed as dist  # noqa: F811
         torch.cuda.set_device(local)
-        if backend == "nccl":
-            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-        else:
-            dist.init_process_group(backend)
+        dist.init_process_group("gloo")
     else:
         torch.cuda.set_device(local)
     device = torch.cuda.current_device()
     stream = torch.cuda.current_stream()
+    comm = None
+    if engine_nccl:
+        uid = [S.NcclComm.unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        comm = S.NcclComm(uid[0], world, rank, device)
 
     grid = S.SweepGrid(MIXES, RPS, CAPS, True)
     base = S.SimConfig()
@@ -326,8 +336,8 @@ def engine_arm(args):
     views = []
     for pl in plans:
         bufs = pl.buffers()
-        if world > 1:
-            # zero-copy int64 views of the plan's row/completion buffers for NCCL
+        if multi and not engine_nccl:
+            # zero-copy int64 views of the plan's row/completion buffers (gloo hook)
             views.append((torch.as_tensor(_CudaView(bufs.rows, bufs.rows_bytes), device=f"cuda:{device}"),
                           torch.as_tensor(_CudaView(bufs.completion_times, bufs.completion_bytes),
                                           device=f"cuda:{device}")))
@@ -335,23 +345,29 @@ def engine_arm(args):
             views.append(None)
     side = torch.cuda.Stream(device=device, priority=-1)  # high priority: summary blocks go first
     summary_done = [None] * n_plans
+    root = rank == 0
 
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.int32, device=device)
 
-    def gather(i):
-        if world > 1:
-            # NCCL final statistics reduce: shards are disjoint (other ranks'
-            # rows are 0), so an integer sum of the raw bits is an exact gather
-            dist.all_reduce(views[i][0])
-            dist.all_reduce(views[i][1])
+    def gather(i, strm):
+        """The final statistics reduce: shards are disjoint (other ranks' rows
+        are 0), so an integer sum of the raw bits onto rank 0 is an exact gather."""
+        if engine_nccl:
+            plans[i].gather(comm, 0, strm.cuda_stream)
+        elif multi:
+            for v in views[i]:
+                dist.all_reduce(v)
 
     def step(k, sync):
         i = k % n_plans
         pl = plans[i]
         if sync:
             pl.run(stream.cuda_stream)
-            gather(i)
-            pl.summarize(stream.cuda_stream)
+            gather(i, stream)
+            if root:
+                pl.summarize(stream.cuda_stream)
+            else:
+                stream.synchronize()
             return
         if summary_done[i] is not None:
             stream.wait_event(summary_done[i])  # plan i's buffers are free again
@@ -361,8 +377,9 @@ def engine_arm(args):
         sim_done.record(stream)
         side.wait_event(sim_done)
         with torch.cuda.stream(side):
-            gather(i)
-            pl.summarize_launch(side.cuda_stream)
+            gather(i, side)
+            if root:
+                pl.summarize_launch(side.cuda_stream)
         e = torch.cuda.Event()
         e.record(side)
         summary_done[i] = e
@@ -395,14 +412,14 @@ def engine_arm(args):
     clk = clocks.stop()
     total_ms = t_start.elapsed_time(t_end)
     if dist:
-        t = torch.tensor([total_ms], dtype=torch.float64, device=device)
+        t = torch.tensor([total_ms], dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         total_ms = float(t.item())
     plan = plans[(args.steps - 1) % n_plans]
     launches_per_step = plan.stats()[2]
     sim_ms = [pl.stats()[1] for pl in plans]
 
-    rows, _, summ, best = plan.fetch(completion=False, summary=True)
+    rows, _, summ, best = plan.fetch(completion=False, summary=root)
     total_rows = plan.n_rows
     value = total_rows * args.steps / (total_ms / 1e3)
     decisions = float(rows["decisions"].sum())
@@ -414,7 +431,7 @@ def engine_arm(args):
     # kernels, D2H of rows + summary) per step.
     e2e_times = []
     h2d = d2h = 0
-    if world == 1:
+    if not multi:
         for k in range(args.warmup + args.steps):
             torch.cuda.synchronize()
             t0 = time.perf_counter()
@@ -434,20 +451,22 @@ def engine_arm(args):
             t0 = time.perf_counter()
             pl = S.SweepPlan(grid, base, device=device, shard_index=rank, shard_count=world)
             pl.run(stream.cuda_stream)
-            b = pl.buffers()
-            rt = torch.as_tensor(_CudaView(b.rows, b.rows_bytes), device=f"cuda:{device}")
-            ct = torch.as_tensor(_CudaView(b.completion_times, b.completion_bytes), device=f"cuda:{device}")
-            dist.all_reduce(rt)
-            dist.all_reduce(ct)
-            pl.summarize(stream.cuda_stream)
-            pl.fetch(completion=False, summary=True)
+            if engine_nccl:
+                pl.gather(comm, 0, stream.cuda_stream)
+            else:
+                b = pl.buffers()
+                for ptr, nb in ((b.rows, b.rows_bytes), (b.completion_times, b.completion_bytes)):
+                    dist.all_reduce(torch.as_tensor(_CudaView(ptr, nb), device=f"cuda:{device}"))
+            if root:
+                pl.summarize(stream.cuda_stream)
+                pl.fetch_stats()
             torch.cuda.synchronize()
             dt = time.perf_counter() - t0
             if k >= args.warmup:
                 e2e_times.append(dt)
             h2d, d2h = pl.last_h2d_bytes, pl.last_d2h_bytes
             pl.close()
-        t = torch.tensor([sum(e2e_times)], dtype=torch.float64, device=device)
+        t = torch.tensor([sum(e2e_times)], dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_value = total_rows * len(e2e_times) / float(t.item())
 
@@ -496,6 +515,8 @@ def engine_arm(args):
             line["cpu_baseline"] = cpu
     for pl in plans:
         pl.close()
+    if comm is not None:
+        comm.close()
     if line is not None:
         print(json.dumps(line), flush=True)
     if dist:

@@ -244,6 +244,33 @@ saber_status saber_cuda_sweep_plan_stats(saber_sweep_plan* plan, double* device_
 void saber_cuda_sweep_plan_destroy(saber_sweep_plan* plan);
 
 /* --------------------------------------------------------------------------
+ * Multi-GPU.  A sweep shards its rows over GPUs (desc
+ * shard_index / shard_count: rows r with r % count == index) with no exchange
+ * during simulation; the final statistics reduce is one NCCL uint64 SUM of the
+ * shards' row and completion buffers onto the root (disjoint shards, so an
+ * exact gather), after which the root summarizes and fetches.
+ *   one process per GPU: saber_cuda_nccl_unique_id on one rank (the caller
+ *     broadcasts the 128 bytes), saber_cuda_nccl_init on every rank, and
+ *     saber_cuda_sweep_plan_gather after each plan launch/run;
+ *   one process, several GPUs: saber_cuda_sweep_multi (a host thread, stream
+ *     and plan per device, ncclCommInitAll).
+ * NCCL (libnccl.so.2) is loaded on first use.
+ * -------------------------------------------------------------------------- */
+typedef struct saber_nccl saber_nccl;
+saber_status saber_cuda_nccl_unique_id(uint8_t* id /* [128] */);
+saber_status saber_cuda_nccl_init(const uint8_t* id /* [128] */, int32_t n_ranks, int32_t rank,
+                                  int32_t device, saber_nccl** comm);
+void saber_cuda_nccl_destroy(saber_nccl* comm);
+/* Enqueues the reduce of this rank's plan buffers onto `root` on `stream`
+ * (after the plan's launch on that stream); every rank calls it. */
+saber_status saber_cuda_sweep_plan_gather(saber_sweep_plan* plan, saber_nccl* comm, int32_t root,
+                                          void* cuda_stream);
+/* The whole sweep (desc->shard_count == 1) over n_devices distinct GPUs; the
+ * outputs are those of saber_cuda_sweep. */
+saber_status saber_cuda_sweep_multi(const saber_sweep_desc* desc, const int32_t* devices,
+                                    int32_t n_devices, saber_sweep_out* out);
+
+/* --------------------------------------------------------------------------
  * Trajectory batch (run / run_with_requests).  Each trajectory is either
  * generated (generate(): WorkloadSpec + its seed) or replayed from explicit
  * requests (ids 0..n-1 in arrival order).

@@ -230,6 +230,12 @@ SYMBOLS = [
     ("saber_cuda_generate", C.c_int, [_P(saber_workload_spec), C.c_int32, C.c_int32,
                                       _P(saber_request), C.c_int32]),
     ("saber_cuda_release_cache", C.c_int, [C.c_int32]),
+    ("saber_cuda_nccl_unique_id", C.c_int, [C.c_char_p]),
+    ("saber_cuda_nccl_init", C.c_int, [C.c_char_p, C.c_int32, C.c_int32, C.c_int32, _P(C.c_void_p)]),
+    ("saber_cuda_nccl_destroy", None, [C.c_void_p]),
+    ("saber_cuda_sweep_plan_gather", C.c_int, [C.c_void_p, C.c_void_p, C.c_int32, C.c_void_p]),
+    ("saber_cuda_sweep_multi", C.c_int, [_P(saber_sweep_desc), _P(C.c_int32), C.c_int32,
+                                         _P(saber_sweep_out)]),
     ("saber_cuda_profile_planned_loads", C.c_int32, [C.c_int32, C.c_int32]),
     ("saber_cuda_trace_from_csv", C.c_int, [C.c_char_p, C.c_size_t, _P(saber_request), C.c_int32,
                                             _P(C.c_int32)]),

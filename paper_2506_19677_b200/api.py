@@ -310,6 +310,8 @@ def _row_dtype():
 
 
 ROW_DTYPE = _row_dtype()
+ROW_STATS_DTYPE = np.dtype([("goodput", np.float64), ("ratio_mean", np.float64),
+                            ("ratio_std", np.float64), ("cv", np.float64)])
 assert ROW_DTYPE.itemsize == C.sizeof(N.saber_traj_row)
 
 COUNTER_NAMES = ["ticks", "passes", "decode_updates", "prefill_updates", "refresh_entries",
@@ -576,6 +578,62 @@ def trace_to_csv(requests: Sequence[Request]) -> str:
 
 
 # ---------------------------------------------------------------- sweep path
+def _sweep_desc(grid: SweepGrid, base: SimConfig, device: int, shard_index: int, shard_count: int,
+                keep: list) -> N.saber_sweep_desc:
+    d = N.saber_sweep_desc()
+    mix_ids = []
+    for m in grid.mixes:
+        if m not in ("w1", "w2", "w3"):
+            raise InvalidArgument(f"unknown mix preset: {m}")
+        mix_ids.append(int(m[1:]))
+    mixes = (C.c_int32 * max(1, len(mix_ids)))(*mix_ids)
+    rps = (C.c_double * max(1, len(grid.rps_list)))(*[float(r) for r in grid.rps_list])
+    caps = (C.c_int32 * max(1, len(grid.caps)))(*[int(c) for c in grid.caps])
+    keep += [mixes, rps, caps]
+    d.mixes, d.n_mixes = mixes, len(mix_ids)
+    d.rps, d.n_rps = rps, len(grid.rps_list)
+    d.caps, d.n_caps = caps, len(grid.caps)
+    d.with_saber = 1 if grid.with_saber else 0
+    d.num_requests = base.workload.num_requests
+    d.length_jitter = base.workload.length_jitter
+    d.window_size = base.scheduler.window_size
+    d.tick = base.scheduler.tick
+    d.has_model = 1 if base.model is not None else 0
+    if base.model is not None:
+        d.model = _model(base.model)
+    d.ground_truth = _model(base.engine.ground_truth)
+    d.prefill_rate = base.engine.prefill_rate
+    d.has_horizon = 1 if base.horizon is not None else 0
+    d.horizon = float(base.horizon) if base.horizon is not None else 0.0
+    d.repeats = base.repeats
+    d.seed = int(base.seed) & 0xFFFFFFFFFFFFFFFF
+    d.device = device
+    d.shard_index = shard_index
+    d.shard_count = shard_count
+    return d
+
+
+class NcclComm:
+    """One rank of the engine's NCCL communicator (saber_cuda_nccl_*): the
+    final statistics reduce of a sharded sweep (SweepPlan.gather)."""
+
+    @staticmethod
+    def unique_id() -> bytes:
+        buf = C.create_string_buffer(128)
+        _check(N.lib().saber_cuda_nccl_unique_id(buf))
+        return buf.raw
+
+    def __init__(self, uid: bytes, n_ranks: int, rank: int, device: int):
+        h = C.c_void_p()
+        _check(N.lib().saber_cuda_nccl_init(uid, n_ranks, rank, device, C.byref(h)))
+        self.handle, self.n_ranks, self.rank = h, n_ranks, rank
+
+    def close(self):
+        if self.handle:
+            N.lib().saber_cuda_nccl_destroy(self.handle)
+            self.handle = None
+
+
 class SweepPlan:
     """Staged sweep (saber_cuda_sweep_plan_*): create once, run many times."""
 
@@ -584,36 +642,7 @@ class SweepPlan:
         self.grid = grid
         self.base = base
         self._keep = []
-        d = N.saber_sweep_desc()
-        mix_ids = []
-        for m in grid.mixes:
-            if m not in ("w1", "w2", "w3"):
-                raise InvalidArgument(f"unknown mix preset: {m}")
-            mix_ids.append(int(m[1:]))
-        mixes = (C.c_int32 * max(1, len(mix_ids)))(*mix_ids)
-        rps = (C.c_double * max(1, len(grid.rps_list)))(*[float(r) for r in grid.rps_list])
-        caps = (C.c_int32 * max(1, len(grid.caps)))(*[int(c) for c in grid.caps])
-        self._keep += [mixes, rps, caps]
-        d.mixes, d.n_mixes = mixes, len(mix_ids)
-        d.rps, d.n_rps = rps, len(grid.rps_list)
-        d.caps, d.n_caps = caps, len(grid.caps)
-        d.with_saber = 1 if grid.with_saber else 0
-        d.num_requests = base.workload.num_requests
-        d.length_jitter = base.workload.length_jitter
-        d.window_size = base.scheduler.window_size
-        d.tick = base.scheduler.tick
-        d.has_model = 1 if base.model is not None else 0
-        if base.model is not None:
-            d.model = _model(base.model)
-        d.ground_truth = _model(base.engine.ground_truth)
-        d.prefill_rate = base.engine.prefill_rate
-        d.has_horizon = 1 if base.horizon is not None else 0
-        d.horizon = float(base.horizon) if base.horizon is not None else 0.0
-        d.repeats = base.repeats
-        d.seed = int(base.seed) & 0xFFFFFFFFFFFFFFFF
-        d.device = device
-        d.shard_index = shard_index
-        d.shard_count = shard_count
+        d = _sweep_desc(grid, base, device, shard_index, shard_count, self._keep)
         self.desc = d
         self.n_rows = int(N.lib().saber_cuda_sweep_rows(C.byref(d)))
         h = C.c_void_p()
@@ -641,6 +670,10 @@ class SweepPlan:
     def summarize_launch(self, stream: int = 0):
         """Enqueue summarize() without waiting (pair with wait())."""
         _check(N.lib().saber_cuda_sweep_plan_summarize_launch(self.handle, C.c_void_p(stream)))
+
+    def gather(self, comm: "NcclComm", root: int = 0, stream: int = 0):
+        """Enqueue the NCCL reduce of this shard's rows onto `root` (every rank)."""
+        _check(N.lib().saber_cuda_sweep_plan_gather(self.handle, comm.handle, root, C.c_void_p(stream)))
 
     def wait(self):
         """Synchronise the enqueued work, check the kernels' error flag."""
@@ -673,6 +706,20 @@ class SweepPlan:
         _check(N.lib().saber_cuda_sweep_plan_fetch(self.handle, C.byref(o)))
         self.last_h2d_bytes, self.last_d2h_bytes = int(o.h2d_bytes), int(o.d2h_bytes)
         return rows, comp, summ, best
+
+    def fetch_stats(self):
+        """The SweepResult payload: per-row statistics (saber_row_stats) plus
+        the summary and best caps (what the drop-in sweep() returns)."""
+        stats = np.zeros(self.n_rows, dtype=ROW_STATS_DTYPE)
+        summ = (N.saber_mix_summary * self.desc.n_mixes)()
+        best = np.zeros((self.desc.n_mixes, self.desc.n_rps), dtype=np.int32)
+        o = N.saber_sweep_out()
+        o.row_stats = stats.ctypes.data_as(C.POINTER(N.saber_row_stats))
+        o.summary = summ
+        o.best_cap_by_rps = best.ctypes.data_as(C.POINTER(C.c_int32))
+        _check(N.lib().saber_cuda_sweep_plan_fetch(self.handle, C.byref(o)))
+        self.last_h2d_bytes, self.last_d2h_bytes = int(o.h2d_bytes), int(o.d2h_bytes)
+        return stats, summ, best
 
     def close(self):
         if self.handle:
@@ -717,7 +764,31 @@ def sweep(grid: SweepGrid, base: SimConfig, jobs: int = 0, device: int = 0,
         dev_ms = plan.stats()[0]
     finally:
         plan.close()
-    # column-wise (numpy -> Python floats in bulk), then one object per row
+    res = _sweep_result(grid, base, rows, summ, best, dev_ms)
+    if completion:
+        res.completion_times = comp
+    return res
+
+
+def sweep_multi(grid: SweepGrid, base: SimConfig, devices: Sequence[int]) -> SweepResult:
+    """sweep() over several GPUs of this process (saber_cuda_sweep_multi): one
+    shard per device, NCCL reduce onto the first, summary there."""
+    keep: list = []
+    d = _sweep_desc(grid, base, int(devices[0]), 0, 1, keep)
+    n_rows = int(N.lib().saber_cuda_sweep_rows(C.byref(d)))
+    rows = np.zeros(n_rows, dtype=ROW_DTYPE)
+    summ = (N.saber_mix_summary * max(1, len(grid.mixes)))()
+    best = np.zeros((len(grid.mixes), len(grid.rps_list)), dtype=np.int32)
+    o = N.saber_sweep_out()
+    o.rows = rows.ctypes.data_as(C.POINTER(N.saber_traj_row))
+    o.summary = summ
+    o.best_cap_by_rps = best.ctypes.data_as(C.POINTER(C.c_int32))
+    devs = (C.c_int32 * len(devices))(*[int(x) for x in devices])
+    _check(N.lib().saber_cuda_sweep_multi(C.byref(d), devs, len(devices), C.byref(o)))
+    return _sweep_result(grid, base, rows, summ, best, o.device_ms)
+
+
+def _sweep_result(grid, base, rows, summ, best, dev_ms):
     cols = [rows[f].tolist() for f in ("goodput", "ratio_mean", "ratio_std", "cv")]
     out_rows = [SweepRow(m, r, mode, cap, seed, g, rm, rs, cv)
                 for (m, r, mode, cap, seed), g, rm, rs, cv in zip(sweep_row_keys(grid, base), *cols)]
@@ -728,10 +799,7 @@ def sweep(grid: SweepGrid, base: SimConfig, jobs: int = 0, device: int = 0,
         summary[m] = MixSummary(s.saber_mean_goodput, s.best_static_mean_goodput, s.delta,
                                 s.saber_pooled_cv, s.best_static_pooled_cv, s.saber_rps_mean_cv,
                                 s.best_static_rps_mean_cv, caps)
-    res = SweepResult(out_rows, summary, rows, dev_ms)
-    if completion:
-        res.completion_times = comp
-    return res
+    return SweepResult(out_rows, summary, rows, dev_ms)
 
 
 # ---------------------------------------------------------------- estimator
