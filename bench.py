@@ -427,48 +427,91 @@ def engine_arm(args):
     fp64_ops = algorithmic_fp64_ops(rows[np.arange(len(rows)) % world == rank])
     sim_avg_ms = float(np.mean(sim_ms))
 
-    # e2e: the one-shot C-ABI call with host buffers (host prologue, H2D, all
-    # kernels, D2H of rows + summary) per step.
-    e2e_times = []
-    h2d = d2h = 0
-    if not multi:
-        for k in range(args.warmup + args.steps):
-            torch.cuda.synchronize()
-            t0 = time.perf_counter()
-            out = _one_shot(S, grid, base, device)
-            torch.cuda.synchronize()
-            if k >= args.warmup:
-                e2e_times.append(time.perf_counter() - t0)
-            h2d, d2h = out
-        e2e_value = total_rows * len(e2e_times) / sum(e2e_times)
-    else:
-        # N > 1 through the staged public API: per step and
-        # rank, plan create (host prologue + H2D), run, NCCL gather, summary,
-        # D2H of every row and the summary; wall clock, max over ranks.
-        for k in range(args.warmup + args.steps):
-            torch.cuda.synchronize()
-            dist.barrier()
-            t0 = time.perf_counter()
-            pl = S.SweepPlan(grid, base, device=device, shard_index=rank, shard_count=world)
-            pl.run(stream.cuda_stream)
-            if engine_nccl:
-                pl.gather(comm, 0, stream.cuda_stream)
-            else:
-                b = pl.buffers()
+    # e2e through the public API with host buffers, every step: the host
+    # prologue + H2D of the step's inputs (plan reseed: per-seed generate()
+    # draws into pinned staging, async upload), all device work, and the D2H
+    # of the SweepResult payload (row statistics, summary, best caps) into
+    # pinned host memory; pipelined over two plans like `value` (the D2H of
+    # step k overlaps step k+1).  Wall clock, max over ranks.  The one-shot
+    # saber_cuda_sweep (host in, host out, nothing overlapped) is reported
+    # beside it.
+    e2e_plans = [S.SweepPlan(grid, base, device=device, shard_index=rank, shard_count=world)
+                 for _ in range(2)]
+    pinned = []
+    for _ in e2e_plans:
+        st = torch.empty(total_rows * 4, dtype=torch.float64, pin_memory=True)
+        bc = torch.empty(len(MIXES) * len(RPS), dtype=torch.int32, pin_memory=True)
+        pinned.append((st, bc, st.numpy().view(S.ROW_STATS_DTYPE),
+                       (S._native.saber_mix_summary * len(MIXES))(),
+                       bc.numpy().reshape(len(MIXES), len(RPS))))
+    done = [None, None]
+
+    def e2e_step(k):
+        i = k % 2
+        pl = e2e_plans[i]
+        if done[i] is not None:
+            done[i].synchronize()  # plan i's previous results are on the host
+        pl.reseed(BASE_SEED, stream.cuda_stream)
+        pl.launch(stream.cuda_stream)
+        ev = torch.cuda.Event()
+        ev.record(stream)
+        side.wait_event(ev)
+        gather_e2e(pl, side)
+        if root:
+            pl.summarize_launch(side.cuda_stream)
+            _, _, stats_np, summ_c, best_np = pinned[i]
+            pl.fetch_stats_async(stats_np, summ_c, best_np, side.cuda_stream)
+        e = torch.cuda.Event()
+        e.record(side)
+        done[i] = e
+
+    def gather_e2e(pl, strm):
+        if engine_nccl:
+            pl.gather(comm, 0, strm.cuda_stream)
+        elif multi:
+            b = pl.buffers()
+            with torch.cuda.stream(strm):
                 for ptr, nb in ((b.rows, b.rows_bytes), (b.completion_times, b.completion_bytes)):
                     dist.all_reduce(torch.as_tensor(_CudaView(ptr, nb), device=f"cuda:{device}"))
-            if root:
-                pl.summarize(stream.cuda_stream)
-                pl.fetch_stats()
-            torch.cuda.synchronize()
-            dt = time.perf_counter() - t0
-            if k >= args.warmup:
-                e2e_times.append(dt)
-            h2d, d2h = pl.last_h2d_bytes, pl.last_d2h_bytes
-            pl.close()
-        t = torch.tensor([sum(e2e_times)], dtype=torch.float64)
+
+    for k in range(args.warmup):
+        e2e_step(k)
+    torch.cuda.synchronize()
+    for pl in e2e_plans:
+        pl.wait()
+    if dist:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for k in range(args.steps):
+        e2e_step(args.warmup + k)
+    torch.cuda.synchronize()
+    e2e_wall = time.perf_counter() - t0
+    for pl in e2e_plans:
+        pl.wait()
+    h2d, d2h = e2e_plans[0].last_h2d_bytes, e2e_plans[0].last_d2h_bytes
+    if dist:
+        t = torch.tensor([e2e_wall], dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_value = total_rows * len(e2e_times) / float(t.item())
+        e2e_wall = float(t.item())
+    e2e_value = total_rows * args.steps / e2e_wall
+    e2e_same = None
+    if root:
+        last = pinned[(args.warmup + args.steps - 1) % 2][2]
+        e2e_same = all(np.array_equal(last[f].view(np.uint64), rows[f].astype(np.float64).view(np.uint64))
+                       for f in ("goodput", "ratio_mean", "ratio_std", "cv"))
+    for pl in e2e_plans:
+        pl.close()
+    one_shot = None
+    if not multi:
+        ts = []
+        for k in range(args.warmup + args.steps):
+            torch.cuda.synchronize()
+            t1 = time.perf_counter()
+            _one_shot(S, grid, base, device)
+            torch.cuda.synchronize()
+            if k >= args.warmup:
+                ts.append(time.perf_counter() - t1)
+        one_shot = total_rows * len(ts) / sum(ts)
 
     peak = S.fp64_peak_tflops(device)
     achieved = fp64_ops / (sim_avg_ms / 1e3) / 1e12
@@ -494,7 +537,12 @@ def engine_arm(args):
             "decisions_per_s": decisions * args.steps / (total_ms / 1e3),
             "decisions_per_step": decisions,
             "e2e": {"value": e2e_value, "unit": "traj/s", "h2d_bytes_per_step": h2d,
-                    "d2h_bytes_per_step": d2h},
+                    "d2h_bytes_per_step": d2h,
+                    "path": "SweepPlan reseed (host prologue + async H2D) -> launch -> summarize -> "
+                            "async D2H of row stats + summary into pinned memory, 2 plans in flight",
+                    "results_equal_value_run": e2e_same,
+                    "one_shot": {"value": one_shot, "unit": "traj/s",
+                                 "path": "saber_cuda_sweep: host buffers in and out, nothing overlapped"}},
             "gpu_launches": launches_per_step * args.steps,
             "roofline": {"bound": "fp64", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                          "frac": achieved / peak if peak else None, "traffic": traffic,

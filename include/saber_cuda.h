@@ -237,6 +237,17 @@ saber_status saber_cuda_sweep_plan_launch_sim(saber_sweep_plan* plan, void* cuda
 saber_status saber_cuda_sweep_plan_metrics_launch(saber_sweep_plan* plan, void* cuda_stream);
 saber_status saber_cuda_sweep_plan_buffers(saber_sweep_plan* plan, saber_sweep_buffers* out);
 saber_status saber_cuda_sweep_plan_fetch(saber_sweep_plan* plan, saber_sweep_out* out);
+/* Pipelined use (several sweeps in flight):
+ *   reseed     : the host prologue for base seed `seed` (per-seed generate()
+ *                draws, glibc log) into the plan's pinned staging, uploaded
+ *                asynchronously on `stream`; the next launch simulates it
+ *   fetch_async: the out struct's requested results copied on `stream`
+ *                (caller buffers should be pinned; read them after the stream
+ *                synchronises).  Enqueue after summarize_launch on the same
+ *                stream (or order the streams) when the summary is wanted. */
+saber_status saber_cuda_sweep_plan_reseed(saber_sweep_plan* plan, uint64_t seed, void* cuda_stream);
+saber_status saber_cuda_sweep_plan_fetch_async(saber_sweep_plan* plan, saber_sweep_out* out,
+                                               void* cuda_stream);
 /* CUDA-event time and launches of the last plan_run (+ summarize). */
 saber_status saber_cuda_sweep_plan_stats(saber_sweep_plan* plan, double* device_ms,
                                          double* sim_kernel_ms, int32_t* launches);

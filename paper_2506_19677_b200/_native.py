@@ -218,6 +218,8 @@ SYMBOLS = [
     ("saber_cuda_sweep_plan_stats", C.c_int, [C.c_void_p, _P(C.c_double), _P(C.c_double),
                                               _P(C.c_int32)]),
     ("saber_cuda_sweep_plan_destroy", None, [C.c_void_p]),
+    ("saber_cuda_sweep_plan_reseed", C.c_int, [C.c_void_p, C.c_uint64, C.c_void_p]),
+    ("saber_cuda_sweep_plan_fetch_async", C.c_int, [C.c_void_p, _P(saber_sweep_out), C.c_void_p]),
     ("saber_cuda_run_batch", C.c_int, [_P(saber_run_batch_desc), _P(saber_run_batch_out)]),
     ("saber_cuda_fit_batch", C.c_int, [_P(saber_fit_desc), _P(saber_fit_out)]),
     ("saber_cuda_profile_samples", C.c_int64, [_P(saber_profile_spec)]),

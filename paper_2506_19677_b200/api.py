@@ -642,6 +642,7 @@ class SweepPlan:
         self.grid = grid
         self.base = base
         self._keep = []
+        self.last_h2d_bytes = self.last_d2h_bytes = 0
         d = _sweep_desc(grid, base, device, shard_index, shard_count, self._keep)
         self.desc = d
         self.n_rows = int(N.lib().saber_cuda_sweep_rows(C.byref(d)))
@@ -706,6 +707,21 @@ class SweepPlan:
         _check(N.lib().saber_cuda_sweep_plan_fetch(self.handle, C.byref(o)))
         self.last_h2d_bytes, self.last_d2h_bytes = int(o.h2d_bytes), int(o.d2h_bytes)
         return rows, comp, summ, best
+
+    def reseed(self, seed: int, stream: int = 0):
+        """Host prologue for base seed `seed` + async upload on `stream`."""
+        _check(N.lib().saber_cuda_sweep_plan_reseed(self.handle, int(seed) & 0xFFFFFFFFFFFFFFFF,
+                                                    C.c_void_p(stream)))
+
+    def fetch_stats_async(self, stats: np.ndarray, summ, best: np.ndarray, stream: int = 0):
+        """Enqueue the SweepResult payload's copies into caller buffers (pinned
+        for a truly asynchronous copy); read them after `stream` synchronises."""
+        o = N.saber_sweep_out()
+        o.row_stats = stats.ctypes.data_as(C.POINTER(N.saber_row_stats))
+        o.summary = summ
+        o.best_cap_by_rps = best.ctypes.data_as(C.POINTER(C.c_int32))
+        _check(N.lib().saber_cuda_sweep_plan_fetch_async(self.handle, C.byref(o), C.c_void_p(stream)))
+        self.last_h2d_bytes, self.last_d2h_bytes = int(o.h2d_bytes), int(o.d2h_bytes)
 
     def fetch_stats(self):
         """The SweepResult payload: per-row statistics (saber_row_stats) plus

@@ -479,7 +479,18 @@ struct saber_sweep_plan {
   // Recorded on the caller's stream at every exit of an enqueueing call
   // (success or error), so destroy can wait for all of the plan's work.
   cudaEvent_t tail_run = nullptr, tail_summ = nullptr;
+  // reseed: pinned staging of the per-seed inputs, reusable once `staged` fired
+  double* h_base = nullptr;
+  uint64_t* h_seeds = nullptr;
+  cudaEvent_t staged = nullptr;
+  double rmin = 0.0;
   ~saber_sweep_plan() {
+    if (staged) {
+      cudaEventSynchronize(staged);
+      cudaEventDestroy(staged);
+    }
+    if (h_base) cudaFreeHost(h_base);
+    if (h_seeds) cudaFreeHost(h_seeds);
     if (side) cudaStreamDestroy(side);
     if (fork) cudaEventDestroy(fork);
     if (join) cudaEventDestroy(join);
@@ -663,9 +674,10 @@ saber_status saber_cuda_sweep_plan_create(const saber_sweep_desc* desc, saber_sw
 
   // Scheduler RNG streams, one per seed, sized by the horizon bound.
   std::vector<uint64_t> seeds;
+  P->rmin = P->rps[0];
+  for (double r : P->rps) P->rmin = std::min(P->rmin, r);
   if (desc->with_saber) {
-    double rmin = P->rps[0];
-    for (double r : P->rps) rmin = std::min(rmin, r);
+    const double rmin = P->rmin;
     for (int i = 0; i < R; ++i) {
       const double last = neglog_sum[static_cast<size_t>(i)] / rmin * (1.0 + 1e-9) + n * 1e-6;
       const double hb = desc->has_horizon ? desc->horizon : last + 10.0 * 12.0 + 1.0;
@@ -704,6 +716,7 @@ saber_status saber_cuda_sweep_plan_create(const saber_sweep_desc* desc, saber_sw
   ALLOC_TRY(P->best_cap, dev, static_cast<size_t>(n_mixes) * n_rps * 4);
   ALLOC_TRY(P->cell_scratch, dev, static_cast<size_t>(n_mixes) * n_rps * 6 * 8);
   ALLOC_TRY(P->ratios, dev, static_cast<size_t>(P->n_rows) * n * 8);
+  ALLOC_TRY(P->stats, dev, static_cast<size_t>(std::max<int64_t>(1, P->n_rows)) * sizeof(saber_row_stats));
   if (desc->with_saber) {
     ALLOC_TRY(P->seeds, dev, seeds.size() * 8);
     ALLOC_TRY(P->s_off, dev, P->stream_full.size() * 8);
@@ -1081,7 +1094,6 @@ saber_status saber_cuda_sweep_plan_fetch(saber_sweep_plan* P, saber_sweep_out* o
                         cudaMemcpyDeviceToHost));
   if (out->row_stats) {
     const size_t bytes = static_cast<size_t>(P->n_rows) * sizeof(saber_row_stats);
-    if (!P->stats.p) ALLOC_TRY(P->stats, P->device, bytes);
     LAUNCH_TRY(launch_pack_row_stats(P->rows.as<saber_traj_row>(), P->n_rows,
                                      P->stats.as<saber_row_stats>(), nullptr));
     CUDA_TRY(cudaMemcpy(out->row_stats, P->stats.p, bytes, cudaMemcpyDeviceToHost));
@@ -1111,6 +1123,89 @@ saber_status saber_cuda_sweep_plan_stats(saber_sweep_plan* P, double* device_ms,
   if (device_ms) *device_ms = P->last_ms;
   if (sim_ms) *sim_ms = P->sim_ms;
   if (launches) *launches = P->launches;
+  return SABER_OK;
+}
+
+saber_status saber_cuda_sweep_plan_reseed(saber_sweep_plan* P, uint64_t seed, void* stream) {
+  if (!P) return fail(SABER_EINVAL, "null plan");
+  CUDA_TRY(cudaSetDevice(P->device));
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const int n = P->n, R = P->R;
+  const size_t base_bytes = static_cast<size_t>(R) * n * 4 * 8;
+  if (!P->h_base) {
+    CUDA_TRY(cudaMallocHost(&P->h_base, base_bytes));
+    CUDA_TRY(cudaMallocHost(&P->h_seeds, static_cast<size_t>(R) * 8));
+    CUDA_TRY(cudaEventCreateWithFlags(&P->staged, cudaEventDisableTiming));
+  } else {
+    CUDA_TRY(cudaEventSynchronize(P->staged));  // the previous upload read the staging
+  }
+  // host prologue: per-seed generate() draws, glibc log
+  std::vector<double> neglog(static_cast<size_t>(R));
+  for (int i = 0; i < R; ++i)
+    seed_draws(seed + static_cast<uint64_t>(i), n, P->h_base + static_cast<size_t>(i) * n * 4,
+               &neglog[static_cast<size_t>(i)]);
+  P->desc.seed = seed;
+  int64_t bytes = static_cast<int64_t>(base_bytes);
+  CUDA_TRY(cudaMemcpyAsync(P->wl.seed_base.p, P->h_base, base_bytes, cudaMemcpyHostToDevice, s));
+  if (P->desc.with_saber) {
+    bool lengths_changed = false;
+    for (int i = 0; i < R; ++i) {
+      P->h_seeds[i] = (seed + static_cast<uint64_t>(i)) ^ kSchedulerSeedSalt;
+      const double last = neglog[static_cast<size_t>(i)] / P->rmin * (1.0 + 1e-9) + n * 1e-6;
+      const double hb = P->desc.has_horizon ? P->desc.horizon : last + 10.0 * 12.0 + 1.0;
+      const int64_t full = draw_bound(hb, P->desc.tick, P->desc.window_size, n);
+      lengths_changed |= std::min(full, P->stream_cap) != P->stream_len[static_cast<size_t>(i)];
+      P->stream_full[static_cast<size_t>(i)] = full;
+    }
+    if (lengths_changed) {  // stream layout changes: re-derive it (synchronous, rare)
+      CUDA_TRY(cudaStreamSynchronize(s));
+      if (saber_status e = set_stream_lengths(P, P->device)) return e;
+    }
+    CUDA_TRY(cudaMemcpyAsync(P->seeds.p, P->h_seeds, static_cast<size_t>(R) * 8,
+                             cudaMemcpyHostToDevice, s));
+    bytes += static_cast<int64_t>(R) * 8;
+  }
+  CUDA_TRY(cudaEventRecord(P->staged, s));
+  P->h2d_bytes = bytes;
+  return SABER_OK;
+}
+
+saber_status saber_cuda_sweep_plan_fetch_async(saber_sweep_plan* P, saber_sweep_out* out,
+                                               void* stream) {
+  if (!P || !out) return fail(SABER_EINVAL, "null argument");
+  CUDA_TRY(cudaSetDevice(P->device));
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if ((out->summary || out->best_cap_by_rps) && !P->summary_pending && !P->summarized)
+    return fail(SABER_EINVAL, "summary requested before summarize");
+  out->n_rows = P->n_rows;
+  out->h2d_bytes = P->h2d_bytes;
+  out->d2h_bytes = 0;
+  const size_t nr = static_cast<size_t>(P->n_rows);
+  if (out->rows) {
+    CUDA_TRY(cudaMemcpyAsync(out->rows, P->rows.p, nr * sizeof(saber_traj_row), cudaMemcpyDeviceToHost, s));
+    out->d2h_bytes += static_cast<int64_t>(nr * sizeof(saber_traj_row));
+  }
+  if (out->row_stats) {
+    LAUNCH_TRY(launch_pack_row_stats(P->rows.as<saber_traj_row>(), P->n_rows,
+                                     P->stats.as<saber_row_stats>(), s));
+    CUDA_TRY(cudaMemcpyAsync(out->row_stats, P->stats.p, nr * sizeof(saber_row_stats),
+                             cudaMemcpyDeviceToHost, s));
+    out->d2h_bytes += static_cast<int64_t>(nr * sizeof(saber_row_stats));
+  }
+  if (out->completion_times) {
+    CUDA_TRY(cudaMemcpyAsync(out->completion_times, P->comp.p, nr * P->n * 8, cudaMemcpyDeviceToHost, s));
+    out->d2h_bytes += static_cast<int64_t>(nr * P->n * 8);
+  }
+  if (out->summary) {
+    const size_t b = static_cast<size_t>(P->desc.n_mixes) * sizeof(saber_mix_summary);
+    CUDA_TRY(cudaMemcpyAsync(out->summary, P->summary.p, b, cudaMemcpyDeviceToHost, s));
+    out->d2h_bytes += static_cast<int64_t>(b);
+  }
+  if (out->best_cap_by_rps) {
+    const size_t b = static_cast<size_t>(P->desc.n_mixes) * P->desc.n_rps * 4;
+    CUDA_TRY(cudaMemcpyAsync(out->best_cap_by_rps, P->best_cap.p, b, cudaMemcpyDeviceToHost, s));
+    out->d2h_bytes += static_cast<int64_t>(b);
+  }
   return SABER_OK;
 }
 
