@@ -441,9 +441,12 @@ def engine_arm(args):
     for _ in e2e_plans:
         st = torch.empty(total_rows * 4, dtype=torch.float64, pin_memory=True)
         bc = torch.empty(len(MIXES) * len(RPS), dtype=torch.int32, pin_memory=True)
+        sm = torch.empty(len(MIXES) * 7, dtype=torch.float64, pin_memory=True)
+        # (every result buffer pinned: a pageable destination would make the
+        # async copy synchronous and serialise the host with the GPU)
         pinned.append((st, bc, st.numpy().view(S.ROW_STATS_DTYPE),
-                       (S._native.saber_mix_summary * len(MIXES))(),
-                       bc.numpy().reshape(len(MIXES), len(RPS))))
+                       (S._native.saber_mix_summary * len(MIXES)).from_address(sm.data_ptr()),
+                       bc.numpy().reshape(len(MIXES), len(RPS)), sm))
     done = [None, None]
 
     def e2e_step(k):
@@ -459,7 +462,7 @@ def engine_arm(args):
         gather_e2e(pl, side)
         if root:
             pl.summarize_launch(side.cuda_stream)
-            _, _, stats_np, summ_c, best_np = pinned[i]
+            _, _, stats_np, summ_c, best_np, _ = pinned[i]
             pl.fetch_stats_async(stats_np, summ_c, best_np, side.cuda_stream)
         e = torch.cuda.Event()
         e.record(side)
