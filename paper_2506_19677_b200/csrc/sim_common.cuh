@@ -70,6 +70,40 @@ __device__ __forceinline__ unsigned group_sum(unsigned v, unsigned gmask) {
   return __reduce_add_sync(gmask, v);
 }
 
+// Whole-warp reductions (G == 32 paths).  dkey maps a non-NaN double to a
+// 64-bit key whose unsigned order is the double order (-0 < +0 is harmless:
+// the keys are only compared, and keyd inverts dkey exactly).
+__device__ __forceinline__ uint64_t dkey(double v) {
+  const uint64_t b = dbits(v);
+  return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+}
+__device__ __forceinline__ double keyd(uint64_t k) {
+  return bitsd((k >> 63) ? (k & 0x7FFFFFFFFFFFFFFFull) : ~k);
+}
+__device__ __forceinline__ uint64_t warp_min_u64(uint64_t v) {
+  const unsigned hi = static_cast<unsigned>(v >> 32);
+  const unsigned mhi = __reduce_min_sync(0xFFFFFFFFu, hi);
+  const unsigned mlo =
+      __reduce_min_sync(0xFFFFFFFFu, hi == mhi ? static_cast<unsigned>(v) : 0xFFFFFFFFu);
+  return (static_cast<uint64_t>(mhi) << 32) | mlo;
+}
+__device__ __forceinline__ uint64_t warp_max_u64(uint64_t v) {
+  const unsigned hi = static_cast<unsigned>(v >> 32);
+  const unsigned mhi = __reduce_max_sync(0xFFFFFFFFu, hi);
+  const unsigned mlo = __reduce_max_sync(0xFFFFFFFFu, hi == mhi ? static_cast<unsigned>(v) : 0u);
+  return (static_cast<uint64_t>(mhi) << 32) | mlo;
+}
+__device__ __forceinline__ uint64_t warp_sum_u64(uint64_t v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xFFFFFFFFu, v, o);
+  return v;
+}
+__device__ __forceinline__ unsigned lanemask_lt() {
+  unsigned m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+
 // Position of the k-th set bit of x (0-based, k < popc(x)): branch-free
 // binary search on popcounts (no data-dependent loop, so lanes asking for
 // different k stay converged).
@@ -150,30 +184,37 @@ struct DecisionLog {
   int32_t k0, k1, k2, k3, k4;
 };
 
+// One full decision record (trace mode) at log index idx.
+__device__ __forceinline__ void write_decision(saber_decision* tr, int64_t idx, int64_t cap,
+                                               int32_t* err, double t, int id, int kind, int load,
+                                               uint64_t pb, uint64_t rb) {
+  if (idx < cap) {
+    saber_decision& d = tr[idx];
+    d.time = t;
+    d.request_id = static_cast<uint64_t>(id);
+    d.kind = kind;
+    d.load_before = load;
+    d.has_pred = pb != kAbsent;
+    d.has_req = rb != kAbsent;
+    d.pred_speed = pb != kAbsent ? bitsd(pb) : nan("");
+    d.req_speed = rb != kAbsent ? bitsd(rb) : nan("");
+  } else {
+    atomicCAS(err, kErrNone, kErrTraceOverflow);
+  }
+}
+
+__device__ __forceinline__ uint64_t decision_word(int id, int kind, int load) {
+  return static_cast<uint64_t>(static_cast<uint32_t>(id)) | (static_cast<uint64_t>(kind) << 32) |
+         (static_cast<uint64_t>(static_cast<uint32_t>(load)) << 40);
+}
+
 template <bool kTrace>
 __device__ __forceinline__ void push_decision(DecisionLog& L, double t, int id,
                                               int kind, int load, uint64_t pb,
                                               uint64_t rb, saber_decision* tr,
                                               int64_t cap, int32_t* err, bool writer) {
-  const uint64_t w = static_cast<uint64_t>(static_cast<uint32_t>(id)) |
-                     (static_cast<uint64_t>(kind) << 32) |
-                     (static_cast<uint64_t>(static_cast<uint32_t>(load)) << 40);
-  L.h += decision_term(static_cast<uint64_t>(L.n), dbits(t), w, pb, rb);
-  if (kTrace && tr != nullptr && writer) {
-    if (L.n < cap) {
-      saber_decision& d = tr[L.n];
-      d.time = t;
-      d.request_id = static_cast<uint64_t>(id);
-      d.kind = kind;
-      d.load_before = load;
-      d.has_pred = pb != kAbsent;
-      d.has_req = rb != kAbsent;
-      d.pred_speed = pb != kAbsent ? bitsd(pb) : nan("");
-      d.req_speed = rb != kAbsent ? bitsd(rb) : nan("");
-    } else {
-      atomicCAS(err, kErrNone, kErrTraceOverflow);
-    }
-  }
+  L.h += decision_term(static_cast<uint64_t>(L.n), dbits(t), decision_word(id, kind, load), pb, rb);
+  if (kTrace && tr != nullptr && writer) write_decision(tr, L.n, cap, err, t, id, kind, load, pb, rb);
   ++L.n;
   L.k0 += kind == 0;
   L.k1 += kind == 1;

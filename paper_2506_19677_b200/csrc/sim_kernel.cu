@@ -1,33 +1,7 @@
-// sim_kernel.cu — the trajectory engine (K1) and its per-row metrics epilogue
-// (K2) for sm_100a.
-//
-// A GROUP of G lanes owns one trajectory.  A persistent grid
-// pulls trajectory indices from an atomic work queue; every lane of the group
-// carries an identical copy of the trajectory's scalar state (clock, tiers as
-// register bitmasks, ledger, RNG cursor, decision hash) and runs the
-// reference's tick loop (simloop.cpp:78-101):
-//   arrivals -> refresh_tiers -> admission_step | static_step  (scheduler.cpp)
-//   -> Engine::advance_to (engine.cpp:51-127) -> completions.
-// The engine's per-slot work — the only part that scales with the batch — is
-// split across the group: slot k is updated by lane k % G, with the slot
-// state (fluid progress / prefill debt, max_out | id) held in shared memory in
-// a lane-interleaved layout (conflict-free 64-bit accesses), and the
-// next-event minima combined with REDUX.MIN over the group.
-//
-// Bit-exactness with the reference: compiled with --fmad=false
-// (the reference has no FMA); every floating-point expression keeps
-// the reference's operand order; predict() comes from host-built tables
-// (SURVEY F6); the scheduler RNG from precomputed mt19937_64 streams
-// (SURVEY F2).  Three exact rewrites remove work without changing any result:
-//   * min_i fl(rem_i / speed) == fl(min_i rem_i / speed), because correctly
-//     rounded division by a positive constant is monotone;
-//   * that one divide is skipped when min_rem >= speed*dt*(1+1e-12), which
-//     proves fl(min_rem / speed) >= dt, i.e. the boundary cannot bind;
-//   * a high-tier request cannot demote before demote_after[i], a safe lower
-//     bound (prologue.cu), so refresh only scans when one might.
-// Slot order inside the engine never affects a result (min is order-free,
-// completions of one pass share the clock), so completed slots are removed by
-// swap-with-last instead of the reference's order-preserving erase.
+// sim_kernel.cu — host side of the trajectory engine (launch planning,
+// kernel selection over the instantiation units) plus the per-row metrics
+// epilogue (K2) and the tick-index kernel.  The engine itself (K1) is in
+// sim_kernel.cuh.
 #include <cuda_runtime.h>
 
 #include <cmath>
@@ -36,72 +10,17 @@
 
 #include "saber_internal.h"
 #include "sim_common.cuh"
+#include "sim_kernel.cuh"
 
 namespace saberb200 {
+
+// Defined by sim_inst_nw{1,2,4,8}.cu: the mask-width-NW instantiations.
+void* pick_sim_nw1(int g, bool trace, bool records, int sel);
+void* pick_sim_nw2(int g, bool trace, bool records, int sel);
+void* pick_sim_nw4(int g, bool trace, bool records, int sel);
+void* pick_sim_nw8(int g, bool trace, bool records, int sel);
+
 namespace {
-
-using namespace simdev;
-
-#ifndef SABER_SIM_MIN_BLOCKS
-#define SABER_SIM_MIN_BLOCKS 4
-#endif
-#ifndef SABER_STATIC_MIN_BLOCKS
-#define SABER_STATIC_MIN_BLOCKS 5
-#endif
-#ifndef SABER_SABER_MIN_BLOCKS
-#define SABER_SABER_MIN_BLOCKS 4
-#endif
-
-#ifdef SABER_STREAK_STATS
-#define SEC_BEGIN() const long long sec_t0_ = clock64()
-#define SEC_END(k) st_cyc[k] += clock64() - sec_t0_
-#else
-#define SEC_BEGIN()
-#define SEC_END(k)
-#endif
-
-// Scheduler-mode specialisation of the trajectory kernel:
-// kSel 0 = any trajectory, 1 = static only, 2 = SABER only.  The specialised
-// variants drop the other mode's code (smaller footprint in the instruction
-// cache, fewer live registers) and serve the sweep's two row classes.
-enum : int { kSelAny = 0, kSelStatic = 1, kSelSaber = 2 };
-
-
-// Shared-memory slot arrays of one group: slot k lives at row k / G, column
-// grp * G + k % G of the warp's [rows][32] tile (so lane k % G of the group
-// always touches its own column: 32 lanes hit 32 consecutive 8-byte words).
-template <int G>
-struct Slots {
-  double* g;     // fluid progress (>= 0) or -prefill_left (< 0); kDoneMark when done
-  uint64_t* m;   // bits(max_output_tokens) | request id (low 16 bits are free)
-  uint32_t* dbuf;  // this group's staging buffer for scheduler draws, G * (kMaxWindow - 1)
-  int col0;      // grp * G
-  static_assert((G & (G - 1)) == 0, "G must be a power of two");
-  __device__ __forceinline__ int idx(int k) const {
-    return ((k / G) << 5) + col0 + (k & (G - 1));
-  }
-};
-
-// An integer q <= a / b (a >= 0 finite, b > 0), capped at 2^30, without a
-// DDIV: b is rounded up and a down to float, the approximate reciprocal
-// (MUFU, |rel err| < 2^-22) and the product are scaled down by 4e-5, so the
-// result is a strict lower bound of the true quotient.
-__device__ __forceinline__ int floor_div_lb(double a, double b) {
-  float r;
-  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(__double2float_ru(b)));
-  const float q = __double2float_rd(a) * (r * 0.99996f);
-  return static_cast<int>(fminf(q, 1073741824.0f));
-}
-
-// min{k : T[k] >= x} over the tick table (len if none; x may be +-inf;
-// NaN maps to len).
-__device__ __forceinline__ int tick_index(const TickTable& tt, double x) {
-  if (isnan(x)) return tt.len;
-  int k = static_cast<int>(fmin(fmax(x * tt.inv_tick, 0.0), static_cast<double>(tt.len)));
-  while (k > 0 && tt.T[k - 1] >= x) --k;
-  while (k < tt.len && tt.T[k] < x) ++k;
-  return k;
-}
 
 __global__ void tick_index_kernel(const WorkloadTables wl, int64_t cells, const TickTable tt,
                                   int32_t* ka, int32_t* kd) {
@@ -109,859 +28,6 @@ __global__ void tick_index_kernel(const WorkloadTables wl, int64_t cells, const 
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     ka[i] = tick_index(tt, wl.arrival[i]);
     kd[i] = tick_index(tt, wl.demote_after[i]);
-  }
-}
-
-// Quiet streak: K consecutive ticks k0 .. k0+K-1, each one
-// full quiet pass of dt = DT[k], applied slot by slot from registers.
-// Per pass the reference computes generated += speed*dt (decode) or
-// prefill_left -= dt (prefill, stored as g = -prefill_left); here every slot
-// adds fl(mult * dt) with mult = speed (decode) or 1.0 (prefill: fl(1*dt) = dt),
-// which is that same value.  The caller has proved that no pass of the streak
-// ends a prefill, binds the decode boundary or completes a slot.  Returns the
-// exact prefill minimum after the streak (the per-pass chain min_pf -= dt).
-// kDec: no slot is in prefill (npre == 0, uniform), so every slot adds the
-// same fl(speed * dt) and the product is formed once per tick, not per slot.
-template <int G, int kC, bool kDec>
-__device__ __forceinline__ double streak_chunks(const Slots<G>& S, int sub, int A, double speed,
-                                               const double* __restrict__ DT, int K, double pf) {
-  // Chunk 0 runs on every lane of the group (it also carries the replicated
-  // min_pf chain); later chunks only while the lane still owns slots.
-  for (int base = sub, first = 1; first || base < A; base += kC * G, first = 0) {
-    double g[kC], mult[kC];
-#pragma unroll
-    for (int i = 0; i < kC; ++i) {
-      const int k = base + i * G;
-      g[i] = k < A ? S.g[S.idx(k)] : 0.0;
-      mult[i] = g[i] < 0.0 ? 1.0 : speed;
-    }
-    int j = 0;
-#pragma unroll 1
-    for (; j + 4 <= K; j += 4) {
-      const double d0 = DT[j], d1 = DT[j + 1], d2 = DT[j + 2], d3 = DT[j + 3];
-      if (kDec) {
-        const double s0 = speed * d0, s1 = speed * d1, s2 = speed * d2, s3 = speed * d3;
-#pragma unroll
-        for (int i = 0; i < kC; ++i) g[i] = (((g[i] + s0) + s1) + s2) + s3;
-      } else {
-#pragma unroll
-        for (int i = 0; i < kC; ++i) {
-          g[i] = g[i] + mult[i] * d0;
-          g[i] = g[i] + mult[i] * d1;
-          g[i] = g[i] + mult[i] * d2;
-          g[i] = g[i] + mult[i] * d3;
-        }
-        if (first) pf = (((pf - d0) - d1) - d2) - d3;
-      }
-    }
-#pragma unroll 1
-    for (; j < K; ++j) {
-      const double d0 = DT[j];
-#pragma unroll
-      for (int i = 0; i < kC; ++i) g[i] = g[i] + mult[i] * d0;  // mult == speed when kDec
-      if (!kDec && first) pf = pf - d0;
-    }
-#pragma unroll
-    for (int i = 0; i < kC; ++i) {
-      const int k = base + i * G;
-      if (k < A) S.g[S.idx(k)] = g[i];
-    }
-  }
-  return pf;
-}
-
-template <int G>
-__device__ __forceinline__ double streak_slots(const Slots<G>& S, int sub, int A, int npre,
-                                               double speed, const double* __restrict__ DT, int K,
-                                               double pf) {
-  if (A <= G) return streak_chunks<G, 1, false>(S, sub, A, speed, DT, K, pf);
-  if (npre == 0) {  // min_pf is +inf and stays so
-    if (A <= 2 * G) return streak_chunks<G, 2, true>(S, sub, A, speed, DT, K, pf);
-    return streak_chunks<G, 4, true>(S, sub, A, speed, DT, K, pf);
-  }
-  if (A <= 2 * G) return streak_chunks<G, 2, false>(S, sub, A, speed, DT, K, pf);
-  return streak_chunks<G, 4, false>(S, sub, A, speed, DT, K, pf);
-}
-
-// Gate streak decisions: ticks k0+1 .. k0+K-1 of a streak
-// whose tick k0 gate admitted nobody.  Each such tick runs the reference's
-// admission_step (scheduler.cpp:57-95) on an unchanged window: w-1 draws for
-// the Fisher-Yates, then every candidate is rejected — RejectOwn when
-// pred < need(t), else RejectActive (need grows with t, so a candidate that
-// could pass its own test at k0 was already blocked by the ledger).  Lane
-// `sub` takes ticks k0+1+sub, k0+1+sub+G, ...; the digest terms (oracle.h)
-// carry their log index n0 + (j-1) w + c, so they are summed in any order.
-template <int G, bool kTrace, int NW>
-__device__ __forceinline__ void gate_streak_decisions(
-    const SimParams& P, const Slots<G>& S, int sub, unsigned gmask, const Mask<NW>& high,
-    const double* __restrict__ MO, const double* __restrict__ DL,
-    const uint32_t* __restrict__ draws, int64_t draw_pos, int k0, int K, int w, int load,
-    double pred, DecisionLog& L, saber_decision* tr, const uint32_t* __restrict__ INV) {
-  // the window (first w queued ids) on lanes 0..w-1
-  int wid = 0;
-  double wm = 0.0, wdl = 0.0;
-  if (sub < w) {
-    wid = high.select(sub);
-    wm = MO[wid];
-    wdl = DL[wid];
-  }
-  const uint64_t pb = dbits(pred);
-  const uint64_t wl = static_cast<uint64_t>(static_cast<uint32_t>(load)) << 40;
-  const int64_t n0 = L.n;
-  uint64_t hs = 0;
-  unsigned own = 0, act = 0;
-  for (int jb = 1; jb < K; jb += G) {
-    const int j = jb + sub;
-    const bool live = j < K;
-    const double tj = live ? P.ticks.T[k0 + j] : 0.0;
-    const uint64_t tb = dbits(tj);
-    // This round's draws (ticks jb .. jb+G-1, w-1 each, consecutive in the
-    // stream) are staged through shared memory with coalesced loads, then
-    // every lane runs its tick's Fisher-Yates from there (a rolled loop keeps
-    // the kernel's instruction footprint small).
-    const int nd = min(G, K - jb) * (w - 1);
-    const uint32_t* __restrict__ src = draws + draw_pos + static_cast<int64_t>(jb - 1) * (w - 1);
-    for (int q = sub; q < nd; q += G) S.dbuf[q] = src[q];
-    __syncwarp(gmask);
-    const uint32_t* my = S.dbuf + sub * (w - 1);
-    uint64_t ord = 0xFEDCBA9876543210ull;
-#pragma unroll 1
-    for (int q = 0; q < w - 1; ++q) {
-      const uint32_t x = live ? my[q] : 0u;
-      const uint32_t i = static_cast<uint32_t>(w - 1 - q);
-      const uint32_t jj = x - __umulhi(x, INV[i + 1]) * (i + 1);
-      const uint64_t a = (ord >> (4 * i)) & 15ull;
-      const uint64_t bb = (ord >> (4 * jj)) & 15ull;
-      const uint64_t x2 = a ^ bb;
-      ord ^= (x2 << (4 * i)) | (x2 << (4 * jj));
-    }
-    __syncwarp(gmask);  // the buffer is refilled next round
-    for (int c = 0; c < w; ++c) {
-      const int p = static_cast<int>((ord >> (4 * c)) & 15ull);
-      const int id = __shfl_sync(gmask, wid, S.col0 + p);
-      const double m = __shfl_sync(gmask, wm, S.col0 + p);
-      const double dl = __shfl_sync(gmask, wdl, S.col0 + p);
-      if (!live) continue;
-      const double need = queued_need(m, dl, tj);
-      const int kind = pred < need ? SABER_REJECT_OWN : SABER_REJECT_ACTIVE;
-      own += kind == SABER_REJECT_OWN;
-      act += kind == SABER_REJECT_ACTIVE;
-      const int64_t idx = n0 + static_cast<int64_t>(j - 1) * w + c;
-      const uint64_t w64 = static_cast<uint64_t>(static_cast<uint32_t>(id)) |
-                           (static_cast<uint64_t>(kind) << 32) | wl;
-      hs += decision_term(static_cast<uint64_t>(idx), tb, w64, pb, dbits(need));
-      if (kTrace && tr != nullptr) {
-        if (idx < P.out.trace_cap) {
-          saber_decision& dd = tr[idx];
-          dd.time = tj;
-          dd.request_id = static_cast<uint64_t>(id);
-          dd.kind = kind;
-          dd.load_before = load;
-          dd.has_pred = 1;
-          dd.has_req = 1;
-          dd.pred_speed = pred;
-          dd.req_speed = need;
-        } else {
-          atomicCAS(P.out.error, kErrNone, kErrTraceOverflow);
-        }
-      }
-    }
-  }
-  // group sums (64-bit digest: butterfly over the group's lanes)
-#pragma unroll
-  for (int o = 1; o < G; o <<= 1) hs += __shfl_xor_sync(gmask, hs, o);
-  own = group_sum<G>(own, gmask);
-  act = group_sum<G>(act, gmask);
-  const int64_t nd = static_cast<int64_t>(K - 1) * w;
-  L.h += hs;
-  L.n += static_cast<int32_t>(nd);
-  L.k2 += static_cast<int32_t>(own);
-  L.k3 += static_cast<int32_t>(act);
-}
-
-// Simulates trajectory `ti` on this group.
-template <int NW, int G, bool kTrace, bool kRecords, int kSel>
-__device__ __forceinline__ void simulate_one(const SimParams& P, int ti, const Slots<G>& S,
-                                             int sub, unsigned gmask,
-                                             double* __restrict__ LNEED,
-                                             uint16_t* __restrict__ LOW,
-                                             const uint32_t* __restrict__ INV) {
-  const TrajDesc d = P.traj[P.order ? P.order[ti] : ti];
-  const int n = d.n;
-  const int nmax = P.wl.nmax;
-  const int64_t wo = static_cast<int64_t>(d.workload) * nmax;
-  const double* __restrict__ ARR = P.wl.arrival + wo;
-  const double* __restrict__ DL = P.wl.deadline + wo;
-  const double* __restrict__ MO = P.wl.max_out + wo;
-  const double* __restrict__ IN = P.wl.input + wo;
-  const double* __restrict__ DEM = P.wl.demote_after + wo;
-  const double* __restrict__ GT = P.tables + d.gt_tab;
-  const bool saber = kSel == kSelSaber ? true
-                     : kSel == kSelStatic ? false
-                                          : d.mode == SABER_MODE_SABER;
-  if (kSel != kSelAny && saber != (d.mode == SABER_MODE_SABER)) {
-    if (sub == 0) atomicCAS(P.out.error, kErrNone, kErrBadDesc);  // loud: wrong kernel
-    return;
-  }
-  const double* __restrict__ MT = P.tables + (saber ? d.model_tab : d.gt_tab);
-  const double horizon = isnan(d.horizon) ? P.wl.horizon[d.workload] : d.horizon;
-  const double tick = d.tick;
-  const double pr = d.prefill_rate;
-  const double ceiling = saber ? MT[1] : 0.0;  // max_speed = predict(model, 1)
-  const uint32_t* __restrict__ draws =
-      saber ? P.rng.draws + P.rng.off[d.stream] : nullptr;
-  const int64_t draw_len = saber ? P.rng.len[d.stream] : 0;
-  double* __restrict__ COMP = P.out.completion + d.row * nmax;
-  double* __restrict__ ADM = kRecords && P.out.admit ? P.out.admit + d.row * nmax : nullptr;
-  uint8_t* __restrict__ DEMO =
-      kRecords && P.out.demoted ? P.out.demoted + d.row * nmax : nullptr;
-  const bool leader = sub == 0;
-  saber_decision* tr = kTrace && P.out.trace ? P.out.trace + d.row * P.out.trace_cap : nullptr;
-
-  Mask<NW> high, ledger;
-  high.clear();
-  ledger.clear();
-  int ledger_size = 0;
-  double ledger_max = -kInf;
-  double min_td = kInf;  // lower bound on the earliest possible demotion
-  int low_head = 0, low_tail = 0;
-
-  int A = 0;         // |active|
-  int npre = 0;      // active slots still in prefill
-  double clock = 0.0;
-  double min_pf = kInf;   // exact min prefill_left over prefill slots
-  double rem_lb = kInf;   // lower bound on min (max_out - generated) over decode slots
-  bool rem_exact = true;  // rem_lb is the exact minimum
-  double m_hi = 0.0;      // >= max_output_tokens of every active slot
-  // speed_A caches predict(gt, A); it changes only with A.
-  double speed_A = 0.0;
-  bool sblock = false;  // quiet-streak bounds exhausted until the next event (§3.5)
-  auto retune = [&]() { speed_A = GT[A]; };
-
-  int next = 0;
-  double na_t = n > 0 ? ARR[0] : kInf;
-  int completed = 0;
-  int64_t draw_pos = 0;
-  bool failed = false;
-
-  DecisionLog L{kHashSeed, 0, 0, 0, 0, 0, 0};
-  int32_t ticks = 0, passes = 0, decode_updates = 0, prefill_updates = 0;
-  int32_t refresh_entries = 0, cands = 0, ledger_scanned = 0, rng_draws = 0;
-
-  // Engine::admit (engine.cpp:26-49): append slot A.  Every lane of the group
-  // writes the same values, so the owning lane reads back its own write.
-  auto admit = [&](int id, double now) {
-    const double pl = pr > 0.0 ? IN[id] / pr : 0.0;
-    const double m = MO[id];
-    const int s = S.idx(A);
-    if (pl == 0.0) {
-      S.g[s] = 0.0;  // decode starts at admission
-      rem_lb = dmin(rem_lb, m - 0.0);
-    } else {
-      S.g[s] = -pl;
-      min_pf = dmin(min_pf, pl);
-      ++npre;
-    }
-    m_hi = (m_hi < m) ? m : m_hi;
-    S.m[s] = dbits(m) | static_cast<uint64_t>(id);
-    ++A;
-    sblock = false;
-    retune();
-    if (kRecords && ADM && leader) ADM[id] = now;
-  };
-
-  // Tick table: kh = first tick index at/after the horizon,
-  // ka = first tick index at/after the next arrival (lazily, -1 = stale).
-  const int32_t* __restrict__ KA = P.wl.arr_tick ? P.wl.arr_tick + wo : nullptr;
-  const int32_t* __restrict__ KD = P.wl.dem_tick ? P.wl.dem_tick + wo : nullptr;
-  bool use_tab = !P.no_streak && P.ticks.len > 0 && tick == P.ticks.tick && KA != nullptr;
-  const int kh = use_tab ? tick_index(P.ticks, horizon) : 0;
-  // tick index of the next arrival, and of min_td (tick_index is monotone, so
-  // it follows min_td's own updates: min at arrival, recomputed at a scan)
-  int ka = use_tab ? (n > 0 ? KA[0] : P.ticks.len) : 0;
-  int min_kd = 0x7FFFFFFF;
-#ifdef SABER_STREAK_STATS
-  int st_ticks = 0, st_count = 0, st_quiet = 0, st_exact = 0;
-  const long long st_t0 = clock64();
-  long long st_cyc[5] = {0, 0, 0, 0, 0};
-  int st_scans = 0;
-#endif
-
-  double t = 0.0;
-  for (;;) {
-    // Arrivals due at t (simloop.cpp:79-85).
-    while (na_t <= t) {
-      high.set(next);
-      if (saber) min_td = dmin(min_td, DEM[next]);
-      if (saber && use_tab) min_kd = min(min_kd, KD[next]);
-      ++next;
-      na_t = next < n ? ARR[next] : kInf;
-      if (use_tab) ka = next < n ? KA[next] : P.ticks.len;
-    }
-    ++ticks;
-    const int load = A;
-    // Gate outcome of this tick, for a gate streak.
-    bool gate_idle = false;
-    int gate_w = 0;
-    double gate_pred = 0.0;
-#ifdef SABER_STREAK_STATS
-    const long long sched_t0 = clock64();
-#endif
-    if (saber) {
-      const int hc = high.count();
-      refresh_entries += hc;
-      // refresh_tiers (scheduler.cpp:38-55): scan in queue (= id) order only
-      // when some entry may have crossed its demotion bound.
-      if (hc > 0 && t >= min_td) {
-#ifdef SABER_STREAK_STATS
-        const long long scan_t0 = clock64();
-        st_scans += 1;
-#endif
-        double nm = kInf;
-        int nkd = 0x7FFFFFFF;
-        for (int i = 0; i < NW; ++i) {
-          uint64_t b = high.word(i);
-          while (b) {
-            const int bit = __ffsll(static_cast<long long>(b)) - 1;
-            b &= b - 1;
-            const int id = i * 64 + bit;
-            const double T = DEM[id];
-            bool demote = false;
-            if (t >= T) {
-              const double need = queued_need(MO[id], DL[id], t);
-              if (need > ceiling) {
-                demote = true;
-                high.andnot(i, 1ull << bit);
-                LOW[low_tail] = static_cast<uint16_t>(id);
-                ++low_tail;
-                push_decision<kTrace>(L, t, id, SABER_DEMOTE, load, dbits(ceiling), dbits(need),
-                                      tr, P.out.trace_cap, P.out.error, leader);
-                if (kRecords && DEMO && leader) DEMO[id] = 1;
-              }
-            }
-            if (!demote) {
-              nm = dmin(nm, T);
-              if (use_tab) nkd = min(nkd, KD[id]);
-            }
-          }
-        }
-        min_td = nm;
-        min_kd = nkd;
-#ifdef SABER_STREAK_STATS
-        st_cyc[4] += clock64() - scan_t0;
-#endif
-      }
-      if (high.any()) {
-        // admission_step, high tier (scheduler.cpp:58-95).
-        const int hcount = high.count();
-        const int w = d.window < hcount ? d.window : hcount;
-        if (draw_pos + (w - 1) > draw_len) {
-          failed = true;
-          break;
-        }
-        // Fisher-Yates over the window: j = rng() % (i+1) for i = w-1..1.
-        // Draws are stored mod lcm(1..16); x % d is exact via the reciprocal
-        // table (x < 2^20).  All w-1 draws are independent
-        // loads, issued before anything consumes them.
-        const double pred = MT[load + 1];
-        const bool violates = pred < ledger_max;  // ActiveLedger::violates
-        unsigned okmask = 0;
-        // The gate (scheduler.cpp:71-94), evaluated for the whole window at
-        // once.  Candidate c is admitted iff it is the first with pred >= need
-        // and no ledger violation; decisions are then emitted in shuffled order.
-        constexpr int kQ = G >= kMaxWindow ? 1 : (kMaxWindow + G - 1) / G;
-        int cid[kQ];
-        double cneed[kQ];
-        if constexpr (G >= kMaxWindow) {
-          // Lane q holds draw q, which serves swap i = w-1-q.  Lane c owns
-          // shuffled position c: the element FY leaves at c is
-          // tau_{w-1}(...tau_1(c)) with tau_i = (i j_i), walked over
-          // i = 1..w-1 with compares and selects, all lanes at once.
-          int jl = 0;
-          if (sub < w - 1) {
-            const uint32_t x = draws[draw_pos + sub];
-            const uint32_t d1 = static_cast<uint32_t>(w - sub);  // i + 1
-            jl = static_cast<int>(x - __umulhi(x, INV[d1]) * d1);
-          }
-          int pos = sub;
-#pragma unroll 1
-          for (int q = w - 2; q >= 0; --q) {
-            const int i = w - 1 - q;
-            const int j = __shfl_sync(gmask, jl, S.col0 + q);
-            pos = pos == i ? j : (pos == j ? i : pos);
-          }
-          cid[0] = 0;
-          cneed[0] = 0.0;
-          if (sub < w) {
-            cid[0] = high.select(pos);
-            cneed[0] = queued_need(MO[cid[0]], DL[cid[0]], t);
-            if (!(pred < cneed[0]) && !violates) okmask = 1u << sub;
-          }
-        } else {
-          uint32_t xq[kMaxWindow - 1];
-#pragma unroll
-          for (int q = 0; q < kMaxWindow - 1; ++q) xq[q] = q < w - 1 ? draws[draw_pos + q] : 0u;
-          uint64_t ord = 0xFEDCBA9876543210ull;  // window positions as nibbles
-#pragma unroll
-          for (int q = 0; q < kMaxWindow - 1; ++q) {
-            if (q < w - 1) {
-              const int i = w - 1 - q;
-              const uint32_t d1 = static_cast<uint32_t>(i + 1);
-              const uint32_t j = xq[q] - __umulhi(xq[q], INV[d1]) * d1;
-              const uint64_t a = (ord >> (4 * i)) & 15ull;
-              const uint64_t bb = (ord >> (4 * j)) & 15ull;
-              const uint64_t x2 = a ^ bb;
-              ord ^= (x2 << (4 * i)) | (x2 << (4 * j));
-            }
-          }
-#pragma unroll
-          for (int q = 0; q < kQ; ++q) {
-            const int c = sub + G * q;
-            cid[q] = 0;
-            cneed[q] = 0.0;
-            if (c < w) {
-              cid[q] = high.select(static_cast<int>((ord >> (4 * c)) & 15ull));
-              cneed[q] = queued_need(MO[cid[q]], DL[cid[q]], t);
-              if (!(pred < cneed[q]) && !violates) okmask |= 1u << c;
-            }
-          }
-        }
-        draw_pos += w - 1;
-        rng_draws += w - 1;
-        ledger_scanned += ledger_size;
-        if (G > 1) okmask = __reduce_or_sync(gmask, okmask);
-        const int first = okmask ? __ffs(okmask) - 1 : w;  // admitted position, or none
-        gate_idle = first == w;
-        gate_w = w;
-        gate_pred = pred;
-        const int last = first < w ? first : w - 1;
-        for (int c = 0; c <= last; ++c) {
-          int id;
-          double need;
-          if (G == 1) {
-            id = cid[c];
-            need = cneed[c];
-          } else {
-            const int q = c / G;
-            int myid = cid[0];
-            double myneed = cneed[0];
-#pragma unroll
-            for (int qq = 1; qq < kQ; ++qq)
-              if (qq == q) {
-                myid = cid[qq];
-                myneed = cneed[qq];
-              }
-            id = __shfl_sync(gmask, myid, S.col0 + (c % G));
-            need = __shfl_sync(gmask, myneed, S.col0 + (c % G));
-          }
-          ++cands;
-          if (c < first) {
-            push_decision<kTrace>(L, t, id, pred < need ? SABER_REJECT_OWN : SABER_REJECT_ACTIVE,
-                                  load, dbits(pred), dbits(need), tr, P.out.trace_cap, P.out.error,
-                                  leader);
-          } else {
-            admit(id, t);
-            ledger.set(id);
-            ++ledger_size;
-            LNEED[id] = need;
-            ledger_max = (ledger_max < need) ? need : ledger_max;
-            high.reset(id);
-            push_decision<kTrace>(L, t, id, SABER_ADMIT_HIGH, load, dbits(pred), dbits(need), tr,
-                                  P.out.trace_cap, P.out.error, leader);
-          }
-        }
-      } else if (low_head < low_tail) {
-        // admission_step, low tier (scheduler.cpp:97-108).
-        const int id = LOW[low_head];
-        ++low_head;
-        const double need = queued_need(MO[id], DL[id], t);
-        admit(id, t);
-        push_decision<kTrace>(L, t, id, SABER_ADMIT_LOW, load, kAbsent, dbits(need), tr,
-                              P.out.trace_cap, P.out.error, leader);
-      }
-    } else {
-      // StaticScheduler::static_step (scheduler.cpp:129-144).
-      while (A < d.cap && high.any()) {
-        const int id = high.lowest();
-        high.reset(id);
-        const int before = A;
-        admit(id, t);
-        push_decision<kTrace>(L, t, id, SABER_ADMIT_HIGH, before, kAbsent, kAbsent, tr,
-                              P.out.trace_cap, P.out.error, leader);
-      }
-    }
-
-#ifdef SABER_STREAK_STATS
-    st_cyc[2] += clock64() - sched_t0;
-#endif
-    if (t >= horizon) break;
-
-    // Quiet streak: from this tick on, consecutive ticks
-    // whose scheduler step is provably a no-op (no arrival, nothing
-    // admissible) and whose single engine pass is provably quiet run as one
-    // register-resident sweep over the slots.  K is bounded by the next
-    // arrival's tick, the horizon, and the prefill / decode minima:
-    //   * min_pf_j > dt_j (1 + 1e-12) for every pass j (no prefill ends);
-    //   * min_rem_j >= sdt_j (1 + 1e-9) + 1e-15 (m_hi + sdt_j + 1), the
-    //     quiet-pass test below (decode boundary cannot bind, no completion);
-    // both minima shrink by at most dt_max / speed*dt_max (+ rounding) per pass.
-    // A SABER tick whose gate admitted nobody starts a gate streak: with the
-    // high tier, load and ledger unchanged, every later tick of the streak
-    // rejects the same window again (need = m / (dl - t) only grows), so its
-    // decisions are generated lane-parallel (gate_streak below).
-    const bool gate_streak = saber && high.any();
-    if (use_tab && !sblock && A > 0 &&
-        (saber ? (gate_streak ? (G >= kMaxWindow && gate_idle) : low_head == low_tail)
-               : !(A < d.cap && high.any()))) {
-      const int k0 = ticks - 1;
-      const double dtm = P.ticks.dt_max;
-      // Kb passes keep both minima provably quiet: for pass j <= Kb - 1 the
-      // remaining margin is still >= one full per-pass decrement.
-      int Kb = 1 << 30;
-      if (npre > 0) Kb = floor_div_lb(min_pf * (1.0 - 2e-7), dtm * (1.0 + 1e-6));
-      double delta = 0.0;
-      if (A > npre) {
-        const double sm = speed_A * dtm * (1.0 + 1e-15);
-        delta = sm * (1.0 + 1e-6) + 2e-15 * (m_hi + sm + 1.0);
-        Kb = min(Kb, floor_div_lb(rem_lb, delta));
-      }
-      // The bounds only shrink until the next admission / exact pass.
-      if (Kb < 2) sblock = true;
-      int K = 0;
-      if (Kb >= 2) {
-        K = min(Kb, min(ka - k0, kh - 1 - k0));
-        if (gate_streak) {
-          // no refresh scan (t < min_td) and enough scheduler draws
-          K = min(K, min_kd - k0);
-          if (gate_w > 1)
-            K = static_cast<int>(min(static_cast<int64_t>(K),
-                                     1 + (draw_len - draw_pos) / (gate_w - 1)));
-        }
-      }
-      if (K >= 2) {
-#ifdef SABER_DEBUG_CHECKS
-        if (P.ticks.T[k0] != t || clock != t) {  // invariant t_k == T[k] at a tick start
-          if (leader) atomicCAS(P.out.error, kErrNone, kErrTickTable);
-          use_tab = false;
-        } else
-#endif
-        {
-          const double t_after = P.ticks.T[k0 + K];  // issued early, used after the sweep
-          const double* __restrict__ DTk = P.ticks.DT + k0;
-          // min_pf stays exact: the same per-pass chain min_pf -= dt
-          {
-            SEC_BEGIN();
-            min_pf = streak_slots<G>(S, sub, A, npre, speed_A, DTk, K, min_pf);
-            SEC_END(1);
-          }
-          if (A > npre) rem_lb = rem_lb - static_cast<double>(K) * delta;
-          rem_exact = false;
-          if (gate_streak) {
-            const int hc = high.count();
-            SEC_BEGIN();
-            gate_streak_decisions<G, kTrace, NW>(P, S, sub, gmask, high, MO, DL, draws, draw_pos,
-                                                 k0, K, gate_w, A, gate_pred, L, tr, INV);
-            SEC_END(0);
-            const int64_t extra = K - 1;
-            draw_pos += extra * (gate_w - 1);
-            rng_draws += static_cast<int32_t>(extra * (gate_w - 1));
-            cands += static_cast<int32_t>(extra * gate_w);
-            ledger_scanned += static_cast<int32_t>(extra * ledger_size);
-            refresh_entries += static_cast<int32_t>(extra * hc);
-          }
-#ifdef SABER_STREAK_STATS
-          st_ticks += K;
-          st_count += 1;
-#endif
-          ticks += K - 1;  // this tick was counted above
-          passes += K;
-          prefill_updates += K * npre;
-          decode_updates += K * (A - npre);
-          t = t_after;
-          clock = t;
-          continue;
-        }
-      }
-    }
-    const double nt = (horizon < t + tick) ? horizon : t + tick;
-
-    // Engine::advance_to(nt) (engine.cpp:51-127).
-#ifdef SABER_STREAK_STATS
-    const long long eng_t0 = clock64();
-#endif
-    while (clock < nt) {
-      if (A == 0) {
-        clock = nt;
-        break;
-      }
-      ++passes;
-      double dt = nt - clock;
-      const double speed = speed_A;
-      if (min_pf < dt) dt = min_pf;
-      // Quiet pass: no prefill ends (min_pf is exact) and the
-      // lower bound on min(max_out - generated) proves both that the decode
-      // boundary cannot bind and that no slot can satisfy the completion
-      // test.  Every slot then just advances, and the new minima follow from
-      // the scalars: min fl(pl - dt) == fl(min_pf - dt) (monotone rounding).
-      const double sdt0 = speed * dt;
-      const bool quiet = !(min_pf <= dt * kOnePlusTol) &&
-                         rem_lb >= sdt0 * (1.0 + 1e-9) + 1e-15 * (m_hi + sdt0 + 1.0);
-      if (quiet) {
-        const double sdt = sdt0;
-#pragma unroll 4
-        for (int k = sub, s = S.idx(sub); k < A; k += G, s += kWarp) {
-          const double g = S.g[s];
-          S.g[s] = g < 0.0 ? g + dt : g + sdt;
-        }
-        min_pf = min_pf - dt;  // == min over prefill slots of fl(pl - dt)
-        rem_lb = (rem_lb - sdt) - 1e-15 * (m_hi + sdt + fabs(rem_lb));
-        rem_exact = false;
-        prefill_updates += npre;
-        decode_updates += A - npre;
-        clock = clock + dt;
-#ifdef SABER_STREAK_STATS
-        st_quiet += 1;
-#endif
-        continue;
-      }
-      // Exact pass.  First make the decode minimum exact if it is a bound.
-      sblock = false;
-#ifdef SABER_STREAK_STATS
-      st_exact += 1;
-#endif
-      if (!rem_exact) {
-        double r = kInf;
-        for (int k = sub, s = S.idx(sub); k < A; k += G, s += kWarp) {
-          const double g = S.g[s];
-          if (g >= 0.0) r = dmin(r, bitsd(S.m[s] & ~kIdMask) - g);
-        }
-        rem_lb = group_min_pos<G>(r, gmask);
-        rem_exact = true;
-      }
-      // dt = min(dt, fl(min_rem / speed)); the divide can only bind when
-      // min_rem < speed * dt * (1 + 1e-12) (see header).
-      if (rem_lb < speed * dt * kOnePlusTol) {
-        const double bnd = rem_lb / speed;
-        if (bnd < dt) dt = bnd;
-      }
-      const double group = dt * kOnePlusTol;
-      const double sdt = speed * dt;
-      const double sgd = speed * (group - dt);
-      const double nclock = clock + dt;
-      double npf = kInf, nrem = kInf;
-      unsigned counts = 0;  // (done << 16) | still-in-prefill
-      int done_k = -1, done_id = -1;  // this lane's last completed slot / request
-      for (int k = sub, s = S.idx(sub); k < A; k += G, s += kWarp) {
-        double g = S.g[s];
-        const uint64_t mb = S.m[s];
-        const double m = bitsd(mb & ~kIdMask);
-        bool done;
-        if (g < 0.0) {  // prefill slot: g = -prefill_left
-          if (-g <= group) {
-            g = 0.0;  // decode starts at nclock
-            done = g + sgd >= m;
-          } else {
-            g = g + dt;  // == -(prefill_left - dt), exactly
-            npf = dmin(npf, -g);
-            ++counts;
-            done = false;
-          }
-        } else {
-          g = g + sdt;
-          done = g + sgd >= m;
-        }
-        if (!done) {
-          if (g >= 0.0) nrem = dmin(nrem, m - g);
-          S.g[s] = g;
-        } else {
-          S.g[s] = bitsd(kDoneMark);
-          done_id = static_cast<int>(mb & kIdMask);
-          done_k = k;
-          COMP[done_id] = nclock;
-          counts += 1u << 16;
-        }
-      }
-      prefill_updates += npre;
-      decode_updates += A - npre;
-      min_pf = group_min_pos<G>(npf, gmask);
-      rem_lb = group_min_pos<G>(nrem, gmask);
-      const unsigned tot = group_sum<G>(counts, gmask);
-      npre = static_cast<int>(tot & 0xFFFFu);
-      const unsigned ndone = tot >> 16;
-      if (ndone == 1) {
-        // One completion (the common event): fetch it from its owner lane,
-        // update the replicated ledger, and swap the last slot into its place.
-        unsigned owner = 0;
-        if (G > 1) owner = __ffs(__ballot_sync(gmask, done_k >= 0)) - 1;
-        const int k = G > 1 ? __shfl_sync(gmask, done_k, owner) : done_k;
-        const int id = G > 1 ? __shfl_sync(gmask, done_id, owner) : done_id;
-        if (saber && ledger.test(id)) {
-          ledger.reset(id);
-          --ledger_size;
-          double mx = -kInf;
-          for (int i = 0; i < NW; ++i) {
-            uint64_t b = ledger.word(i);
-            while (b) {
-              const int q = i * 64 + __ffsll(static_cast<long long>(b)) - 1;
-              b &= b - 1;
-              const double v = LNEED[q];
-              mx = (mx < v) ? v : mx;
-            }
-          }
-          ledger_max = mx;
-        }
-        if (k != A - 1) {
-          const int dst = S.idx(k), src = S.idx(A - 1);
-          __syncwarp(gmask);
-          if (leader) {
-            S.g[dst] = S.g[src];
-            S.m[dst] = S.m[src];
-          }
-          __syncwarp(gmask);
-        }
-        A -= 1;
-        retune();
-        completed += 1;
-      } else if (ndone) {
-        // Several completions in one pass (lockstep bursts): every lane
-        // replays them for the replicated scheduler state, then the leader
-        // compacts the slot array by swap-with-last.
-        __syncwarp(gmask);
-        bool dirty = false;
-        for (int k = 0; k < A; ++k) {
-          const int s = S.idx(k);
-          if (dbits(S.g[s]) != kDoneMark) continue;
-          const int id = static_cast<int>(S.m[s] & kIdMask);
-          if (saber && ledger.test(id)) {
-            ledger.reset(id);
-            --ledger_size;
-            dirty = true;
-          }
-        }
-        __syncwarp(gmask);
-        if (leader) {
-          int a = A;
-          for (int k = 0; k < a;) {
-            const int s = S.idx(k);
-            if (dbits(S.g[s]) != kDoneMark) {
-              ++k;
-              continue;
-            }
-            const int last = S.idx(a - 1);
-            S.g[s] = S.g[last];
-            S.m[s] = S.m[last];
-            --a;
-          }
-        }
-        __syncwarp(gmask);
-        A -= static_cast<int>(ndone);
-        retune();
-        completed += static_cast<int>(ndone);
-        if (dirty) {
-          double mx = -kInf;
-          for (int i = 0; i < NW; ++i) {
-            uint64_t b = ledger.word(i);
-            while (b) {
-              const int id = i * 64 + __ffsll(static_cast<long long>(b)) - 1;
-              b &= b - 1;
-              const double v = LNEED[id];
-              mx = (mx < v) ? v : mx;
-            }
-          }
-          ledger_max = mx;
-        }
-      }
-      clock = nclock;
-    }
-#ifdef SABER_STREAK_STATS
-    st_cyc[3] += clock64() - eng_t0;
-#endif
-    t = nt;
-    if (completed == n) break;
-  }
-
-  if (failed && leader) atomicCAS(P.out.error, kErrNone, kErrRngExhausted);
-  if (kRecords && P.out.generated) {
-    // fluid progress of the requests still running (Request::generated_tokens;
-    // a slot in prefill has generated nothing yet)
-    double* __restrict__ GEN = P.out.generated + d.row * nmax;
-    for (int k = sub, s = S.idx(sub); k < A; k += G, s += kWarp) {
-      const double g = S.g[s];
-      GEN[static_cast<int>(S.m[s] & kIdMask)] = g < 0.0 ? 0.0 : g;
-    }
-  }
-  if (leader) {
-    saber_traj_row* R = P.out.rows + d.row;
-    R->n = n;
-    R->decisions = L.n;
-    R->n_kind[0] = L.k0;
-    R->n_kind[1] = L.k1;
-    R->n_kind[2] = L.k2;
-    R->n_kind[3] = L.k3;
-    R->n_kind[4] = L.k4;
-    R->decision_hash = L.h;
-    R->ticks = ticks;
-    R->passes = passes;
-    R->decode_updates = decode_updates;
-    R->prefill_updates = prefill_updates;
-    R->refresh_entries = refresh_entries;
-    R->gate_candidates = cands;
-    R->ledger_scanned = ledger_scanned;
-    R->rng_draws = rng_draws;
-    R->last_arrival = n > 0 ? ARR[n - 1] : 0.0;
-    R->horizon = horizon;
-#ifdef SABER_STREAK_STATS
-    R->last_arrival = st_ticks;
-    R->horizon = st_count;
-    R->ratio_mean = static_cast<double>(clock64() - st_t0);  // overwritten by row metrics
-    R->n_kind[4] = clock64() - st_t0;
-    for (int q = 0; q < 4; ++q) R->n_kind[q] = st_cyc[q];
-    R->rng_draws = st_cyc[4];
-    R->gate_candidates = st_scans;
-    R->decision_hash = (static_cast<uint64_t>(st_quiet) << 32) | static_cast<uint32_t>(st_exact);
-#endif
-    if (kTrace && P.out.trace_count) P.out.trace_count[d.row] = L.n;
-  }
-}
-
-template <int NW, int G, bool kTrace, bool kRecords, int kSel>
-__global__ void __launch_bounds__(kSimBlock, kSel == kSelStatic  ? SABER_STATIC_MIN_BLOCKS
-                                             : kSel == kSelSaber ? SABER_SABER_MIN_BLOCKS
-                                                                 : SABER_SIM_MIN_BLOCKS)
-    sim_kernel(const SimParams P) {
-  extern __shared__ __align__(16) uint64_t smem[];
-  __shared__ uint32_t inv[kMaxWindow + 1];  // ceil(2^32 / d) for d = 2..16
-  if (threadIdx.x >= 2 && threadIdx.x <= kMaxWindow)
-    inv[threadIdx.x] = static_cast<uint32_t>((0x100000000ull + threadIdx.x - 1) / threadIdx.x);
-  __syncthreads();
-  const int lane = threadIdx.x & 31;
-  const int warp = threadIdx.x >> 5;
-  const int grp = lane / G;
-  const int sub = lane % G;
-  const unsigned gmask = (G == 32 ? 0xFFFFFFFFu : ((1u << G) - 1u)) << (grp * G);
-  const int rows = P.slot_rows;
-  uint64_t* tile = smem + static_cast<size_t>(warp) * rows * kWarp * 2;
-  Slots<G> S;
-  S.g = reinterpret_cast<double*>(tile);
-  S.m = tile + static_cast<size_t>(rows) * kWarp;
-  S.dbuf = reinterpret_cast<uint32_t*>(smem + static_cast<size_t>(kSimBlock / kWarp) * rows * kWarp * 2) +
-           static_cast<size_t>(warp) * kWarp * (kMaxWindow - 1) + grp * G * (kMaxWindow - 1);
-  S.col0 = grp * G;
-  const int64_t group_id =
-      (static_cast<int64_t>(blockIdx.x) * (kSimBlock / kWarp) + warp) * (kWarp / G) + grp;
-  if (group_id >= P.scratch.groups) {  // scratch sized for a smaller grid: loud, never silent
-    if (lane == 0) atomicCAS(P.out.error, kErrNone, kErrBadDesc);
-    return;
-  }
-  double* LNEED = P.scratch.ledger_need + group_id * P.wl.nmax;
-  uint16_t* LOW = P.scratch.low_fifo + group_id * P.wl.nmax;
-  for (;;) {
-    int ti = 0;
-    if (sub == 0) ti = P.first_traj + atomicAdd(P.next_traj, 1);
-    ti = __shfl_sync(gmask, ti, grp * G);
-    if (ti >= P.n_traj) break;
-    simulate_one<NW, G, kTrace, kRecords, kSel>(P, ti, S, sub, gmask, LNEED, LOW, inv);
-    __syncwarp(gmask);
   }
 }
 
@@ -1108,41 +174,12 @@ __global__ void __launch_bounds__(128) row_metrics_warp_kernel(const RowMetricsP
   }
 }
 
-template <int NW, int G, bool kTrace, bool kRecords, int kSel = kSelAny>
-void* kernel_ptr() {
-  return reinterpret_cast<void*>(&sim_kernel<NW, G, kTrace, kRecords, kSel>);
-}
-
-// Mode-specialised variants exist for the bench path only: G = 32, no trace,
-// no per-request records; everything else uses kSelAny.
-template <int NW, int G>
-void* pick_tr(bool trace, bool records, int sel) {
-  if (trace) return kernel_ptr<NW, G, true, true>();
-  if (records) return kernel_ptr<NW, G, false, true>();
-  if (G == kWarp && sel == kSelStatic) return kernel_ptr<NW, kWarp, false, false, kSelStatic>();
-  if (G == kWarp && sel == kSelSaber) return kernel_ptr<NW, kWarp, false, false, kSelSaber>();
-  return kernel_ptr<NW, G, false, false>();
-}
-
-template <int NW>
-void* pick_g(int g, bool trace, bool records, int sel) {
-  switch (g) {
-    case 1: return pick_tr<NW, 1>(trace, records, sel);
-    case 2: return pick_tr<NW, 2>(trace, records, sel);
-    case 4: return pick_tr<NW, 4>(trace, records, sel);
-    case 8: return pick_tr<NW, 8>(trace, records, sel);
-    case 16: return pick_tr<NW, 16>(trace, records, sel);
-    case 32: return pick_tr<NW, 32>(trace, records, sel);
-  }
-  return nullptr;
-}
-
 void* pick_kernel(int nw, int g, bool trace, bool records, int sel = kSelAny) {
   switch (nw) {
-    case 1: return pick_g<1>(g, trace, records, sel);
-    case 2: return pick_g<2>(g, trace, records, sel);
-    case 4: return pick_g<4>(g, trace, records, sel);
-    case 8: return pick_g<8>(g, trace, records, sel);
+    case 1: return pick_sim_nw1(g, trace, records, sel);
+    case 2: return pick_sim_nw2(g, trace, records, sel);
+    case 4: return pick_sim_nw4(g, trace, records, sel);
+    case 8: return pick_sim_nw8(g, trace, records, sel);
   }
   return nullptr;
 }
