@@ -274,6 +274,90 @@ __device__ __forceinline__ void gate_streak_decisions(
   L.k3 += static_cast<int32_t>(act);
 }
 
+// Whole-warp gate streak (G == 32): the same decisions as
+// gate_streak_decisions, in two phases per round of up to 32 ticks.  Phase A,
+// lane = tick: the tick's Fisher-Yates permutation of the window as packed
+// nibbles, parked in the draw staging buffer.  Phase B, lane = (tick,
+// position) pair: the candidate's need, kind and digest term — so the
+// per-decision work (a divide and the digest mix) runs on ~all 32 lanes
+// instead of one lane per tick.
+template <bool kTrace, int NW>
+__device__ __forceinline__ void gate_streak_warp(
+    const SimParams& P, const Slots<kWarp>& S, int sub, const Mask<NW>& high,
+    const double* __restrict__ MO, const double* __restrict__ DL,
+    const uint32_t* __restrict__ draws, int64_t draw_pos, int k0, int K, int w, int load,
+    double pred, DecisionLog& L, saber_decision* tr, const uint32_t* __restrict__ INV) {
+  int wid = 0;
+  double wm = 0.0, wdl = 0.0;
+  if (sub < w) {
+    wid = high.select(sub);
+    wm = MO[wid];
+    wdl = DL[wid];
+  }
+  const uint64_t pb = dbits(pred);
+  const int64_t n0 = L.n;
+  const uint32_t invw = w > 1 ? INV[w] : 0u;
+  uint64_t* __restrict__ ords = reinterpret_cast<uint64_t*>(S.dbuf);
+  uint64_t hs = 0;
+  unsigned own = 0;
+  for (int jb = 1; jb < K; jb += kWarp) {
+    const int nt = min(kWarp, K - jb);
+    const int nd = nt * (w - 1);
+    const uint32_t* __restrict__ src = draws + draw_pos + static_cast<int64_t>(jb - 1) * (w - 1);
+    for (int q = sub; q < nd; q += kWarp) S.dbuf[q] = src[q];
+    __syncwarp();
+    uint64_t ord = 0xFEDCBA9876543210ull;
+    if (sub < nt) {
+      const uint32_t* my = S.dbuf + sub * (w - 1);
+#pragma unroll 1
+      for (int q = 0; q < w - 1; ++q) {
+        const uint32_t x = my[q];
+        const uint32_t i = static_cast<uint32_t>(w - 1 - q);
+        const uint32_t jj = x - __umulhi(x, INV[i + 1]) * (i + 1);
+        const uint64_t a = (ord >> (4 * i)) & 15ull;
+        const uint64_t bb = (ord >> (4 * jj)) & 15ull;
+        const uint64_t x2 = a ^ bb;
+        ord ^= (x2 << (4 * i)) | (x2 << (4 * jj));
+      }
+    }
+    __syncwarp();  // every lane's draws are consumed before the buffer is reused
+    ords[sub] = ord;
+    __syncwarp();
+    const int np = nt * w;
+#pragma unroll 1
+    for (int p0 = 0; p0 < np; p0 += kWarp) {
+      const int p = p0 + sub;
+      const bool live = p < np;
+      const int jj = live ? (w > 1 ? static_cast<int>(__umulhi(static_cast<uint32_t>(p), invw)) : p) : 0;
+      const int c = p - jj * w;
+      const int pos = live ? static_cast<int>((ords[jj] >> (4 * c)) & 15ull) : 0;
+      const int id = __shfl_sync(0xFFFFFFFFu, wid, pos);
+      const double m = __shfl_sync(0xFFFFFFFFu, wm, pos);
+      const double dl = __shfl_sync(0xFFFFFFFFu, wdl, pos);
+      if (live) {
+        const int j = jb + jj;
+        const double tj = P.ticks.T[k0 + j];
+        const double need = queued_need(m, dl, tj);
+        const int kind = pred < need ? SABER_REJECT_OWN : SABER_REJECT_ACTIVE;
+        own += kind == SABER_REJECT_OWN;
+        const int64_t idx = n0 + static_cast<int64_t>(j - 1) * w + c;
+        const uint64_t tb = dbits(tj), rb = dbits(need);
+        hs += decision_term(static_cast<uint64_t>(idx), tb, decision_word(id, kind, load), pb, rb);
+        if (kTrace && tr != nullptr)
+          write_decision(tr, idx, P.out.trace_cap, P.out.error, tj, id, kind, load, pb, rb);
+      }
+    }
+    __syncwarp();  // the buffer is refilled next round
+  }
+  hs = warp_sum_u64(hs);
+  own = __reduce_add_sync(0xFFFFFFFFu, own);
+  const int32_t ndec = static_cast<int32_t>(K - 1) * w;
+  L.h += hs;
+  L.n += ndec;
+  L.k2 += static_cast<int32_t>(own);
+  L.k3 += ndec - static_cast<int32_t>(own);
+}
+
 // max over the ledger's needs (ActiveLedger, scheduler.hpp:30-44), -inf when
 // empty.  Needs are >= +0, so their bit patterns order like the values; with
 // a whole warp per trajectory every lane tests two ids of each mask word.
@@ -322,11 +406,6 @@ __device__ __forceinline__ void simulate_one(const SimParams& P, int ti, const S
   const int n = d.n;
   const int nmax = P.wl.nmax;
   const int64_t wo = static_cast<int64_t>(d.workload) * nmax;
-  const double* __restrict__ ARR = P.wl.arrival + wo;
-  const double* __restrict__ DL = P.wl.deadline + wo;
-  const double* __restrict__ MO = P.wl.max_out + wo;
-  const double* __restrict__ IN = P.wl.input + wo;
-  const double* __restrict__ DEM = P.wl.demote_after + wo;
   const double* __restrict__ GT = P.tables + d.gt_tab;
   const bool saber = kSel == kSelSaber ? true
                      : kSel == kSelStatic ? false
@@ -371,7 +450,7 @@ __device__ __forceinline__ void simulate_one(const SimParams& P, int ti, const S
   auto retune = [&]() { speed_A = GT[A]; };
 
   int next = 0;
-  double na_t = n > 0 ? ARR[0] : kInf;
+  double na_t = n > 0 ? P.wl.arrival[wo + 0] : kInf;
   int completed = 0;
   int64_t draw_pos = 0;
   bool failed = false;
@@ -383,8 +462,8 @@ __device__ __forceinline__ void simulate_one(const SimParams& P, int ti, const S
   // Engine::admit (engine.cpp:26-49): append slot A.  Every lane of the group
   // writes the same values, so the owning lane reads back its own write.
   auto admit = [&](int id, double now) {
-    const double pl = pr > 0.0 ? IN[id] / pr : 0.0;
-    const double m = MO[id];
+    const double pl = pr > 0.0 ? P.wl.input[wo + id] / pr : 0.0;
+    const double m = P.wl.max_out[wo + id];
     const int s = S.idx(A);
     if (pl == 0.0) {
       S.g[s] = 0.0;  // decode starts at admission
@@ -404,13 +483,11 @@ __device__ __forceinline__ void simulate_one(const SimParams& P, int ti, const S
 
   // Tick table: kh = first tick index at/after the horizon,
   // ka = first tick index at/after the next arrival (lazily, -1 = stale).
-  const int32_t* __restrict__ KA = P.wl.arr_tick ? P.wl.arr_tick + wo : nullptr;
-  const int32_t* __restrict__ KD = P.wl.dem_tick ? P.wl.dem_tick + wo : nullptr;
-  bool use_tab = !P.no_streak && P.ticks.len > 0 && tick == P.ticks.tick && KA != nullptr;
+  bool use_tab = !P.no_streak && P.ticks.len > 0 && tick == P.ticks.tick && P.wl.arr_tick != nullptr;
   const int kh = use_tab ? tick_index(P.ticks, horizon) : 0;
   // tick index of the next arrival, and of min_td (tick_index is monotone, so
   // it follows min_td's own updates: min at arrival, recomputed at a scan)
-  int ka = use_tab ? (n > 0 ? KA[0] : P.ticks.len) : 0;
+  int ka = use_tab ? (n > 0 ? P.wl.arr_tick[wo + 0] : P.ticks.len) : 0;
   int min_kd = 0x7FFFFFFF;
 #ifdef SABER_STREAK_STATS
   int st_ticks = 0, st_count = 0, st_quiet = 0, st_exact = 0;
@@ -424,11 +501,11 @@ __device__ __forceinline__ void simulate_one(const SimParams& P, int ti, const S
     // Arrivals due at t (simloop.cpp:79-85).
     while (na_t <= t) {
       high.set(next);
-      if (saber) min_td = dmin(min_td, DEM[next]);
-      if (saber && use_tab) min_kd = min(min_kd, KD[next]);
+      if (saber) min_td = dmin(min_td, P.wl.demote_after[wo + next]);
+      if (saber && use_tab) min_kd = min(min_kd, P.wl.dem_tick[wo + next]);
       ++next;
-      na_t = next < n ? ARR[next] : kInf;
-      if (use_tab) ka = next < n ? KA[next] : P.ticks.len;
+      na_t = next < n ? P.wl.arrival[wo + next] : kInf;
+      if (use_tab) ka = next < n ? P.wl.arr_tick[wo + next] : P.ticks.len;
     }
     ++ticks;
     const int load = A;
@@ -459,47 +536,41 @@ __device__ __forceinline__ void simulate_one(const SimParams& P, int ti, const S
           uint64_t key = dkey(kInf);
           uint64_t hterm = 0;
           int ndem = 0;
-#pragma unroll
-          for (int i = 0; i < NW; ++i) {
-            const uint64_t wd = high.word(i);
-            if (wd == 0) continue;
-            uint64_t dm = 0;
-#pragma unroll
-            for (int hh = 0; hh < 2; ++hh) {
-              const int bit = hh * 32 + sub;
-              const int id = i * 64 + bit;
-              const bool mem = ((wd >> bit) & 1ull) != 0;
-              bool demote = false;
-              double need = 0.0;
-              if (mem) {
-                const double T = DEM[id];
-                if (t >= T) {
-                  need = queued_need(MO[id], DL[id], t);
-                  demote = need > ceiling;
-                }
-                if (!demote) {
-                  key = key < dkey(T) ? key : dkey(T);
-                  if (use_tab) nkd = min(nkd, KD[id]);
-                }
+#pragma unroll 1
+          for (int q = 0; q < 2 * NW; ++q) {  // half-words of the tier mask
+            const uint32_t hw = static_cast<uint32_t>(high.word(q >> 1) >> ((q & 1) * 32));
+            if (hw == 0) continue;
+            const int id = q * 32 + sub;
+            const bool mem = ((hw >> sub) & 1u) != 0;
+            bool demote = false;
+            double need = 0.0;
+            if (mem) {
+              const double T = P.wl.demote_after[wo + id];
+              if (t >= T) {
+                need = queued_need(P.wl.max_out[wo + id], P.wl.deadline[wo + id], t);
+                demote = need > ceiling;
               }
-              const unsigned bal = __ballot_sync(0xFFFFFFFFu, demote);
-              if (bal) {
-                if (demote) {
-                  const int rank = ndem + __popc(bal & lanemask_lt());
-                  LOW[low_tail + rank] = static_cast<uint16_t>(id);
-                  const uint64_t rb = dbits(need), pb = dbits(ceiling);
-                  hterm += decision_term(static_cast<uint64_t>(L.n + rank), dbits(t),
-                                         decision_word(id, SABER_DEMOTE, load), pb, rb);
-                  if (kTrace && tr != nullptr)
-                    write_decision(tr, L.n + rank, P.out.trace_cap, P.out.error, t, id,
-                                   SABER_DEMOTE, load, pb, rb);
-                  if (kRecords && DEMO) DEMO[id] = 1;
-                }
-                ndem += __popc(bal);
-                dm |= static_cast<uint64_t>(bal) << (hh * 32);
+              if (!demote) {
+                key = key < dkey(T) ? key : dkey(T);
+                if (use_tab) nkd = min(nkd, P.wl.dem_tick[wo + id]);
               }
             }
-            high.andnot(i, dm);
+            const unsigned bal = __ballot_sync(0xFFFFFFFFu, demote);
+            if (bal) {
+              if (demote) {
+                const int rank = ndem + __popc(bal & lanemask_lt());
+                LOW[low_tail + rank] = static_cast<uint16_t>(id);
+                const uint64_t rb = dbits(need), pb = dbits(ceiling);
+                hterm += decision_term(static_cast<uint64_t>(L.n + rank), dbits(t),
+                                       decision_word(id, SABER_DEMOTE, load), pb, rb);
+                if (kTrace && tr != nullptr)
+                  write_decision(tr, L.n + rank, P.out.trace_cap, P.out.error, t, id,
+                                 SABER_DEMOTE, load, pb, rb);
+                if (kRecords && DEMO) DEMO[id] = 1;
+              }
+              ndem += __popc(bal);
+              high.andnot(q >> 1, static_cast<uint64_t>(bal) << ((q & 1) * 32));
+            }
           }
           if (ndem) {
             L.h += warp_sum_u64(hterm);
@@ -517,10 +588,10 @@ __device__ __forceinline__ void simulate_one(const SimParams& P, int ti, const S
             const int bit = __ffsll(static_cast<long long>(b)) - 1;
             b &= b - 1;
             const int id = i * 64 + bit;
-            const double T = DEM[id];
+            const double T = P.wl.demote_after[wo + id];
             bool demote = false;
             if (t >= T) {
-              const double need = queued_need(MO[id], DL[id], t);
+              const double need = queued_need(P.wl.max_out[wo + id], P.wl.deadline[wo + id], t);
               if (need > ceiling) {
                 demote = true;
                 high.andnot(i, 1ull << bit);
@@ -533,7 +604,7 @@ __device__ __forceinline__ void simulate_one(const SimParams& P, int ti, const S
             }
             if (!demote) {
               nm = dmin(nm, T);
-              if (use_tab) nkd = min(nkd, KD[id]);
+              if (use_tab) nkd = min(nkd, P.wl.dem_tick[wo + id]);
             }
           }
         }
@@ -587,7 +658,7 @@ __device__ __forceinline__ void simulate_one(const SimParams& P, int ti, const S
           cneed[0] = 0.0;
           if (sub < w) {
             cid[0] = high.select(pos);
-            cneed[0] = queued_need(MO[cid[0]], DL[cid[0]], t);
+            cneed[0] = queued_need(P.wl.max_out[wo + cid[0]], P.wl.deadline[wo + cid[0]], t);
             if (!(pred < cneed[0]) && !violates) okmask = 1u << sub;
           }
         } else {
@@ -614,7 +685,7 @@ __device__ __forceinline__ void simulate_one(const SimParams& P, int ti, const S
             cneed[q] = 0.0;
             if (c < w) {
               cid[q] = high.select(static_cast<int>((ord >> (4 * c)) & 15ull));
-              cneed[q] = queued_need(MO[cid[q]], DL[cid[q]], t);
+              cneed[q] = queued_need(P.wl.max_out[wo + cid[q]], P.wl.deadline[wo + cid[q]], t);
               if (!(pred < cneed[q]) && !violates) okmask |= 1u << c;
             }
           }
@@ -702,7 +773,7 @@ __device__ __forceinline__ void simulate_one(const SimParams& P, int ti, const S
         // admission_step, low tier (scheduler.cpp:97-108).
         const int id = LOW[low_head];
         ++low_head;
-        const double need = queued_need(MO[id], DL[id], t);
+        const double need = queued_need(P.wl.max_out[wo + id], P.wl.deadline[wo + id], t);
         admit(id, t);
         push_decision<kTrace>(L, t, id, SABER_ADMIT_LOW, load, kAbsent, dbits(need), tr,
                               P.out.trace_cap, P.out.error, leader);
@@ -787,8 +858,13 @@ __device__ __forceinline__ void simulate_one(const SimParams& P, int ti, const S
           if (gate_streak) {
             const int hc = high.count();
             SEC_BEGIN();
-            gate_streak_decisions<G, kTrace, NW>(P, S, sub, gmask, high, MO, DL, draws, draw_pos,
-                                                 k0, K, gate_w, A, gate_pred, L, tr, INV);
+            if constexpr (G == kWarp)
+              gate_streak_warp<kTrace, NW>(P, S, sub, high, P.wl.max_out + wo, P.wl.deadline + wo,
+                                           draws, draw_pos, k0, K, gate_w, A, gate_pred, L, tr, INV);
+            else
+              gate_streak_decisions<G, kTrace, NW>(P, S, sub, gmask, high, P.wl.max_out + wo,
+                                                   P.wl.deadline + wo, draws, draw_pos, k0, K,
+                                                   gate_w, A, gate_pred, L, tr, INV);
             SEC_END(0);
             const int64_t extra = K - 1;
             draw_pos += extra * (gate_w - 1);
@@ -1014,7 +1090,7 @@ __device__ __forceinline__ void simulate_one(const SimParams& P, int ti, const S
     R->gate_candidates = cands;
     R->ledger_scanned = ledger_scanned;
     R->rng_draws = rng_draws;
-    R->last_arrival = n > 0 ? ARR[n - 1] : 0.0;
+    R->last_arrival = n > 0 ? P.wl.arrival[wo + n - 1] : 0.0;
     R->horizon = horizon;
 #ifdef SABER_STREAK_STATS
     R->last_arrival = st_ticks;
