@@ -138,7 +138,10 @@ struct SimLaunch {
   int slot_rows;  // ceil(nmax / group)
   size_t smem;    // dynamic shared memory per block
 };
-constexpr int kSimBlock = 128;
+#ifndef SABER_SIM_BLOCK
+#define SABER_SIM_BLOCK 128
+#endif
+constexpr int kSimBlock = SABER_SIM_BLOCK;
 int plan_sim(int nmax, int group, SimLaunch* out);
 int launch_sim(const SimParams& p, const SimLaunch& l, void* stream);
 // Tick-table indices of every request's arrival and demote_after (quiet
