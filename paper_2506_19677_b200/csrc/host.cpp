@@ -334,13 +334,19 @@ int group_size() {
   return 32;
 }
 
+// The launch needs the wide kernel: more requests than the
+// register tier masks hold, or a window the nibble Fisher-Yates cannot shuffle.
+bool needs_wide(int nmax, int max_window) {
+  return nmax > kMaxRequests || max_window > kMaxWindow;
+}
+
 struct Scratch {
-  DevBuf ledger, low;
+  DevBuf ledger, low, wslot_g, wslot_m, wmask, wgate, wneed;
   SimLaunch launch{};
   GroupScratch view{};
   // Kernel configuration: G lanes per trajectory.
-  saber_status alloc(int device, int nmax) {
-    const int rc = plan_sim(nmax, group_size(), &launch);
+  saber_status alloc(int device, int nmax, bool wide = false) {
+    const int rc = plan_sim(nmax, group_size(), wide, &launch);
     if (rc != 0)
       return fail(SABER_ECUDA, "trajectory kernel configuration failed (" + std::to_string(rc) +
                                    "): " + cudaGetErrorString(cudaGetLastError()));
@@ -355,6 +361,21 @@ struct Scratch {
     view.ledger_need = ledger.as<double>();
     view.low_fifo = low.as<uint16_t>();
     view.groups = groups;
+    if (launch.wide) {
+      const int nw = (nmax + 63) / 64;
+      const size_t g = static_cast<size_t>(groups);
+      ALLOC_TRY(wslot_g, device, g * per * 8);
+      ALLOC_TRY(wslot_m, device, g * per * 8);
+      ALLOC_TRY(wmask, device, g * 2 * static_cast<size_t>(nw) * 8);
+      ALLOC_TRY(wgate, device, g * 3 * per * 4);
+      ALLOC_TRY(wneed, device, g * per * 8);
+      view.wslot_g = wslot_g.as<double>();
+      view.wslot_m = wslot_m.as<uint64_t>();
+      view.wmask = wmask.as<uint64_t>();
+      view.wgate = wgate.as<int32_t>();
+      view.wneed = wneed.as<double>();
+      view.wmask_nw = nw;
+    }
     return SABER_OK;
   }
 };
@@ -536,15 +557,12 @@ saber_status validate_sweep(const saber_sweep_desc& d) {
     for (int j = 0; j < i; ++j)
       if (d.caps[i] == d.caps[j]) return fail(SABER_EINVAL, "sweep: duplicate cap in the grid");
   if (d.num_requests < 1) return fail(SABER_EINVAL, "num_requests must be >= 1");
-  if (d.num_requests > kMaxRequests)
-    return fail(SABER_EINVAL, "num_requests > " + std::to_string(kMaxRequests) +
+  if (d.num_requests > kMaxRequestsWide)
+    return fail(SABER_EINVAL, "num_requests > " + std::to_string(kMaxRequestsWide) +
                                   " is not supported by the B200 engine");
   if (d.length_jitter < 0.0 || d.length_jitter >= 1.0)
     return fail(SABER_EINVAL, "length_jitter must be in [0, 1)");
   if (d.window_size < 1) return fail(SABER_EINVAL, "window_size must be >= 1");
-  if (d.window_size > kMaxWindow)
-    return fail(SABER_EINVAL, "window_size > " + std::to_string(kMaxWindow) +
-                                  " is not supported by the B200 engine");
   if (!(d.tick > 0.0)) return fail(SABER_EINVAL, "tick must be > 0");
   for (int i = 0; i < d.n_caps; ++i)
     if (d.caps[i] < 1) return fail(SABER_EINVAL, "static mode requires a positive batch size");
@@ -589,7 +607,8 @@ saber_status set_stream_lengths(saber_sweep_plan* P, int dev) {
     off[i] = P->total_draws;
     P->total_draws += P->stream_len[i];
   }
-  ALLOC_TRY(P->draws, dev, static_cast<size_t>(std::max<int64_t>(1, P->total_draws)) * 4);
+  ALLOC_TRY(P->draws, dev, static_cast<size_t>(std::max<int64_t>(1, P->total_draws)) *
+                             (P->scratch.launch.wide ? 8 : 4));
   CUDA_TRY(cudaMemcpy(P->s_off.p, off.data(), ns * 8, cudaMemcpyHostToDevice));
   CUDA_TRY(cudaMemcpy(P->s_len.p, P->stream_len.data(), ns * 8, cudaMemcpyHostToDevice));
   return SABER_OK;
@@ -723,7 +742,7 @@ saber_status saber_cuda_sweep_plan_create(const saber_sweep_desc* desc, saber_sw
     ALLOC_TRY(P->s_len, dev, P->stream_full.size() * 8);
   }
   tr.mark("device buffers");
-  if (saber_status s = P->scratch.alloc(dev, n)) return s;
+  if (saber_status s = P->scratch.alloc(dev, n, needs_wide(n, desc->window_size))) return s;
   tr.mark("scratch + kernel plan");
 
   // Execution order: every SABER trajectory first (they are
@@ -888,6 +907,7 @@ static saber_status plan_launch_impl(saber_sweep_plan* P, void* stream, bool wit
     RngGenParams rg{};
     rg.seeds = P->seeds.as<uint64_t>();
     rg.draws = P->draws.as<uint32_t>();
+    rg.wide = P->scratch.launch.wide;
     rg.off = P->s_off.as<int64_t>();
     rg.len = P->s_len.as<int64_t>();
     rg.n_streams = P->R;
@@ -923,6 +943,7 @@ static saber_status plan_launch_impl(saber_sweep_plan* P, void* stream, bool wit
   sp.wl = P->wl.view(P->n);
   sp.tables = P->tables.as<double>();
   sp.rng.draws = P->draws.as<uint32_t>();
+  sp.rng.wide = P->scratch.launch.wide;
   sp.rng.off = P->s_off.as<int64_t>();
   sp.rng.len = P->s_len.as<int64_t>();
   sp.scratch = P->scratch.view;
@@ -935,7 +956,7 @@ static saber_status plan_launch_impl(saber_sweep_plan* P, void* stream, bool wit
   sp.ticks = P->ticktab.view;
   CUDA_TRY(cudaEventRecord(P->sim.a, s));
   const bool split = P->n_saber_first > 0 && P->n_saber_first < P->rows_shard &&
-                     P->scratch.launch.group == 32 &&
+                     P->scratch.launch.group == 32 && !P->scratch.launch.wide &&
                      std::getenv("SABER_NO_SPLIT") == nullptr;
   if (split) {
     // SABER rows [0, ns) on the SABER-only kernel, static rows [ns, N) on the
@@ -1293,9 +1314,6 @@ namespace {
 
 saber_status validate_spec(const saber_traj_spec& s) {
   if (s.window_size < 1) return fail(SABER_EINVAL, "window_size must be >= 1");
-  if (s.window_size > kMaxWindow)
-    return fail(SABER_EINVAL, "window_size > " + std::to_string(kMaxWindow) +
-                                  " is not supported by the B200 engine");
   if (!(s.tick > 0.0)) return fail(SABER_EINVAL, "tick must be > 0");
   if (s.mode != SABER_MODE_SABER && s.mode != SABER_MODE_STATIC)
     return fail(SABER_EINVAL, "unknown scheduler mode");
@@ -1311,8 +1329,8 @@ saber_status validate_spec(const saber_traj_spec& s) {
     return fail(SABER_EINVAL, "engine ground truth must be positive");
   if (s.num_requests < 1)
     return fail(SABER_EINVAL, s.requests ? "run: no requests" : "num_requests must be >= 1");
-  if (s.num_requests > kMaxRequests)
-    return fail(SABER_EINVAL, "num_requests > " + std::to_string(kMaxRequests) +
+  if (s.num_requests > kMaxRequestsWide)
+    return fail(SABER_EINVAL, "num_requests > " + std::to_string(kMaxRequestsWide) +
                                   " is not supported by the B200 engine");
   if (!s.requests) {
     if (!(s.rps > 0.0)) return fail(SABER_EINVAL, "rps must be > 0");
@@ -1331,11 +1349,13 @@ extern "C" saber_status saber_cuda_run_batch(const saber_run_batch_desc* desc,
   const int T = desc->n_traj;
   if (T < 1) return fail(SABER_EINVAL, "run_batch: no trajectories");
   if (!out->rows) return fail(SABER_EINVAL, "run_batch: rows output required");
-  int nmax = 1;
+  int nmax = 1, wmax = 1;
   for (int k = 0; k < T; ++k) {
     if (saber_status s = validate_spec(desc->specs[k])) return s;
     nmax = std::max(nmax, desc->specs[k].num_requests);
+    if (desc->specs[k].mode == SABER_MODE_SABER) wmax = std::max(wmax, desc->specs[k].window_size);
   }
+  const bool wide = needs_wide(nmax, wmax);
   const bool want_states = out->states || out->cdf_latency || out->cdf_fraction ||
                            out->group_issued || out->group_met;
   if ((out->arrival_times || out->admit_times || out->completion_times || out->demoted ||
@@ -1495,9 +1515,9 @@ extern "C" saber_status saber_cuda_run_batch(const saber_run_batch_desc* desc,
     ALLOC_TRY(seeds_d, dev, seeds.size() * 8);
     ALLOC_TRY(off_d, dev, off.size() * 8);
     ALLOC_TRY(len_d, dev, len.size() * 8);
-    ALLOC_TRY(draws_d, dev, static_cast<size_t>(std::max<int64_t>(1, total_draws)) * 4);
+    ALLOC_TRY(draws_d, dev, static_cast<size_t>(std::max<int64_t>(1, total_draws)) * (wide ? 8 : 4));
   }
-  if (saber_status s = scratch.alloc(dev, nmax)) return s;
+  if (saber_status s = scratch.alloc(dev, nmax, wide)) return s;
   // One tick table, for the most common tick of the batch.
   TickTableBuf ticktab;
   {
@@ -1589,6 +1609,7 @@ extern "C" saber_status saber_cuda_run_batch(const saber_run_batch_desc* desc,
     RngGenParams rg{};
     rg.seeds = seeds_d.as<uint64_t>();
     rg.draws = draws_d.as<uint32_t>();
+    rg.wide = wide;
     rg.off = off_d.as<int64_t>();
     rg.len = len_d.as<int64_t>();
     rg.n_streams = static_cast<int32_t>(seeds.size());
@@ -1601,6 +1622,7 @@ extern "C" saber_status saber_cuda_run_batch(const saber_run_batch_desc* desc,
   sp.wl = wl.view(nmax);
   sp.tables = tables.as<double>();
   sp.rng.draws = draws_d.as<uint32_t>();
+  sp.rng.wide = wide;
   sp.rng.off = off_d.as<int64_t>();
   sp.rng.len = len_d.as<int64_t>();
   sp.scratch = scratch.view;
@@ -1911,15 +1933,12 @@ saber_status validate_mc(const saber_mc_desc& d) {
   for (int i = 0; i < d.n_caps; ++i)
     if (d.caps[i] < 1) return fail(SABER_EINVAL, "static mode requires a positive batch size");
   if (d.num_requests < 1) return fail(SABER_EINVAL, "num_requests must be >= 1");
-  if (d.num_requests > kMaxRequests)
-    return fail(SABER_EINVAL, "num_requests > " + std::to_string(kMaxRequests) +
+  if (d.num_requests > kMaxRequestsWide)
+    return fail(SABER_EINVAL, "num_requests > " + std::to_string(kMaxRequestsWide) +
                                   " is not supported by the B200 engine");
   if (d.length_jitter < 0.0 || d.length_jitter >= 1.0)
     return fail(SABER_EINVAL, "length_jitter must be in [0, 1)");
   if (d.window_size < 1) return fail(SABER_EINVAL, "window_size must be >= 1");
-  if (d.window_size > kMaxWindow)
-    return fail(SABER_EINVAL, "window_size > " + std::to_string(kMaxWindow) +
-                                  " is not supported by the B200 engine");
   if (!(d.tick > 0.0)) return fail(SABER_EINVAL, "tick must be > 0");
   if (saber_status s = validate_model(d.ground_truth, "ground truth")) return s;
   if (d.has_model)
@@ -2053,7 +2072,8 @@ extern "C" saber_status saber_cuda_mc_sweep(const saber_mc_desc* desc, saber_mc_
   ALLOC_TRY(cursor, dev, 16);
   ALLOC_TRY(err, dev, 16);
   if (saber_status s = wl.alloc(dev, chunk, n)) return s;
-  if (saber_status s = scratch.alloc(dev, n)) return s;
+  const bool wide = needs_wide(n, d.with_saber ? d.window_size : 1);
+  if (saber_status s = scratch.alloc(dev, n, wide)) return s;
   CUDA_TRY(cudaMemcpy(tables.p, tab.data(), tab.size() * 8, cudaMemcpyHostToDevice));
   CUDA_TRY(cudaMemcpy(rps_d.p, d.rps, static_cast<size_t>(d.n_rps) * 8, cudaMemcpyHostToDevice));
   if (d.n_caps > 0)
@@ -2132,13 +2152,14 @@ extern "C" saber_status saber_cuda_mc_sweep(const saber_mc_desc* desc, saber_mc_
     ALLOC_TRY(seeds_d, dev, seeds.size() * 8);
     ALLOC_TRY(off_d, dev, off.size() * 8);
     ALLOC_TRY(len_d, dev, lens.size() * 8);
-    ALLOC_TRY(draws_d, dev, static_cast<size_t>(std::max<int64_t>(1, len * pool)) * 4);
+    ALLOC_TRY(draws_d, dev, static_cast<size_t>(std::max<int64_t>(1, len * pool)) * (wide ? 8 : 4));
     CUDA_TRY(cudaMemcpy(seeds_d.p, seeds.data(), seeds.size() * 8, cudaMemcpyHostToDevice));
     CUDA_TRY(cudaMemcpy(off_d.p, off.data(), off.size() * 8, cudaMemcpyHostToDevice));
     CUDA_TRY(cudaMemcpy(len_d.p, lens.data(), lens.size() * 8, cudaMemcpyHostToDevice));
     RngGenParams rg{};
     rg.seeds = seeds_d.as<uint64_t>();
     rg.draws = draws_d.as<uint32_t>();
+    rg.wide = wide;
     rg.off = off_d.as<int64_t>();
     rg.len = len_d.as<int64_t>();
     rg.n_streams = pool;
@@ -2149,6 +2170,7 @@ extern "C" saber_status saber_cuda_mc_sweep(const saber_mc_desc* desc, saber_mc_
   if (out->rows) host_rows.resize(static_cast<size_t>(chunk));
   // split launches (SABER-only + static-only kernels) need both classes
   const bool split_ok = d.with_saber && d.n_caps > 0 && scratch.launch.group == 32 &&
+                        !scratch.launch.wide &&
                         std::getenv("SABER_NO_SPLIT") == nullptr;
   std::vector<int32_t> ord_h;
   DevBuf order_d;
@@ -2204,6 +2226,7 @@ extern "C" saber_status saber_cuda_mc_sweep(const saber_mc_desc* desc, saber_mc_
     sp.wl = wl.view(n);
     sp.tables = tables.as<double>();
     sp.rng.draws = draws_d.as<uint32_t>();
+    sp.rng.wide = wide;
     sp.rng.off = off_d.as<int64_t>();
     sp.rng.len = len_d.as<int64_t>();
     sp.scratch = scratch.view;

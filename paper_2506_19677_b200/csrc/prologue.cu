@@ -113,6 +113,7 @@ __global__ void __launch_bounds__(160) rng_stream_kernel(const RngGenParams p) {
   __syncthreads();
   const int64_t len = p.len[s];
   uint32_t* out = p.draws + p.off[s];
+  uint64_t* out64 = reinterpret_cast<uint64_t*>(p.draws) + p.off[s];  // wide plans
   constexpr uint64_t kUpper = 0xFFFFFFFF80000000ULL, kLower = 0x7FFFFFFFULL;
   constexpr uint64_t kMatrix = 0xB5026F5AA96619E9ULL;
   for (int64_t base = 0; base < len; base += 312) {
@@ -139,7 +140,8 @@ __global__ void __launch_bounds__(160) rng_stream_kernel(const RngGenParams p) {
         y ^= (y << 17) & 0x71D67FFFEDA60000ULL;
         y ^= (y << 37) & 0xFFF7EEE000000000ULL;
         y ^= y >> 43;
-        out[base + k] = static_cast<uint32_t>(y % kDrawModulus);
+        if (p.wide) out64[base + k] = y;
+        else out[base + k] = static_cast<uint32_t>(y % kDrawModulus);
       }
     }
     __syncthreads();

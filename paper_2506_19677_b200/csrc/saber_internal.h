@@ -14,12 +14,16 @@ namespace saberb200 {
 saber_status set_error(saber_status s, const std::string& msg);
 
 // Largest request count the register-bitmask trajectory kernel supports
-// (8 x 64-bit words of per-request tier masks).  Larger n is rejected with
-// SABER_EINVAL.
+// (8 x 64-bit words of per-request tier masks).  Larger n runs on the wide
+// kernel.
 constexpr int kMaxRequests = 512;
 // Largest admission window the register Fisher-Yates supports (4-bit nibbles
-// in one u64).  The reference default is 8 (types.hpp:80).
+// in one u64).  The reference default is 8 (types.hpp:80); wider windows run
+// on the wide kernel.
 constexpr int kMaxWindow = 16;
+// Request-count limit of the wide kernel: request ids travel in the low 16
+// bits of a slot word and in the u16 low-tier FIFO.
+constexpr int kMaxRequestsWide = 65536;
 // Lanes per warp; per-lane scratch is interleaved with this stride.
 constexpr int kWarp = 32;
 
@@ -58,10 +62,13 @@ struct TrajDesc {
 // Scheduler RNG streams: stream s holds draws [off[s], off[s] + len[s]).
 // Each draw is mt19937_64() % 720720 (= lcm(1..16)), exact for every
 // `% (i+1)` with i+1 <= 16 the Fisher-Yates needs.
+// A wide plan (window > 16) stores the raw 64-bit draws instead
+// (`draws` then points at u64 words; off/len count draws either way).
 struct RngStreams {
   const uint32_t* draws;
   const int64_t* off;
   const int64_t* len;
+  int32_t wide;
 };
 
 constexpr uint32_t kDrawModulus = 720720u;  // lcm(1..16)
@@ -69,10 +76,19 @@ constexpr uint32_t kDrawModulus = 720720u;  // lcm(1..16)
 // Per-group scratch in global memory for the rarely touched queues
 // (DESIGN.md §2): the ledger's frozen requirements and the low-tier FIFO.
 // The hot per-slot state lives in shared memory (sim_kernel.cu).
+// The wide kernel (n > 512 or window > 16) keeps the
+// slots, both tier masks and the gate's window in per-group global memory.
 struct GroupScratch {
   double* ledger_need;  // [groups][nmax]
   uint16_t* low_fifo;   // [groups][nmax]
   int64_t groups;
+  // wide kernel only (null otherwise)
+  double* wslot_g;      // [groups][nmax] slot fluid progress
+  uint64_t* wslot_m;    // [groups][nmax] slot bits(max_out) | id
+  uint64_t* wmask;      // [groups][2][wmask_nw] high tier, ledger
+  int32_t* wgate;       // [groups][3][nmax] Fisher-Yates j, window order, candidate id
+  double* wneed;        // [groups][nmax] candidate needs
+  int32_t wmask_nw;     // ceil(nmax / 64)
 };
 
 // Outputs of the trajectory kernel.
@@ -137,12 +153,15 @@ struct SimLaunch {
   int grid_sel[3];  // persistent blocks per mode-specialised variant (G = 32)
   int slot_rows;  // ceil(nmax / group)
   size_t smem;    // dynamic shared memory per block
+  int wide;       // 1 = the wide kernel (global-memory slots and masks)
 };
 #ifndef SABER_SIM_BLOCK
 #define SABER_SIM_BLOCK 128
 #endif
 constexpr int kSimBlock = SABER_SIM_BLOCK;
-int plan_sim(int nmax, int group, SimLaunch* out);
+// `wide`: the launch needs the wide kernel (nmax > kMaxRequests or a window
+// > kMaxWindow).
+int plan_sim(int nmax, int group, bool wide, SimLaunch* out);
 int launch_sim(const SimParams& p, const SimLaunch& l, void* stream);
 // Tick-table indices of every request's arrival and demote_after (quiet
 // streak bounds without table searches on the trajectory's critical path).
@@ -155,6 +174,7 @@ struct RngGenParams {
   const int64_t* off;
   const int64_t* len;
   int32_t n_streams;
+  int32_t wide;           // 1 = store raw u64 draws (window > 16)
 };
 int launch_rng_streams(const RngGenParams& p, void* stream);
 
@@ -213,7 +233,11 @@ struct RowMetricsParams {
   const TrajDesc* traj;
   int32_t n_traj;
   int32_t narrow;  // 1 = a few single-warp blocks (beside the trajectory kernels)
+  // rows longer than kMaxRequests rank their latencies in global scratch,
+  // one [nmax] slice per warp of a fixed grid (kRowMetricsWideWarps)
+  double* lat_scratch;
 };
+constexpr int kRowMetricsWideWarps = 1184;  // 148 SMs x 8 warps
 int launch_row_metrics(const RowMetricsParams& p, void* stream);
 
 // run() epilogue (records.cu): the workload as saber_request, the final

@@ -133,6 +133,7 @@ __device__ __forceinline__ int select64(uint64_t x, int k) {
 // never turn into a local-memory access.
 template <int NW, int B = 0>
 struct Mask {
+  static constexpr bool kGlobal = false;
   uint64_t w;
   Mask<NW - 1, B + 1> r;
   __device__ __forceinline__ void clear() { w = 0; r.clear(); }
@@ -153,6 +154,8 @@ struct Mask {
     else r.andnot(i, m);
   }
   __device__ __forceinline__ bool any() const { return w != 0 || r.any(); }
+  __device__ __forceinline__ int word_begin() const { return 0; }
+  __device__ __forceinline__ int word_end() const { return NW; }
   __device__ __forceinline__ int count() const { return __popcll(w) + r.count(); }
   __device__ __forceinline__ int lowest() const {
     return w ? B * 64 + __ffsll(static_cast<long long>(w)) - 1 : r.lowest();
@@ -166,6 +169,7 @@ struct Mask {
 };
 template <int B>
 struct Mask<0, B> {
+  static constexpr bool kGlobal = false;
   __device__ __forceinline__ void clear() {}
   __device__ __forceinline__ void set(int) {}
   __device__ __forceinline__ void reset(int) {}
@@ -176,6 +180,73 @@ struct Mask<0, B> {
   __device__ __forceinline__ int count() const { return 0; }
   __device__ __forceinline__ int lowest() const { return -1; }
   __device__ __forceinline__ int select(int) const { return -1; }
+};
+
+// Tier mask of the wide kernel: `nw` 64-bit words in the
+// group's global scratch, plus scalar copies (identical on every lane) of
+// the member count, a lower bound `lo` on the first non-empty word and an
+// upper bound `hi` on the last one.  Every lane reads the words; lane 0
+// alone writes them, between two __syncwarp()s, so no lane ever observes a
+// half-applied update.  Whole-warp groups only (G = 32).
+struct GMask {
+  static constexpr bool kGlobal = true;
+  uint64_t* p;
+  int nw, cnt, lo, hi;
+  bool leader;
+  __device__ __forceinline__ void bind(uint64_t* words, int n_words, int sub) {
+    p = words;
+    nw = n_words;
+    leader = sub == 0;
+  }
+  __device__ __forceinline__ void clear() {
+    __syncwarp();
+    for (int i = static_cast<int>(threadIdx.x & 31); i < nw; i += 32) p[i] = 0;
+    __syncwarp();
+    cnt = 0;
+    lo = 0;
+    hi = 0;
+  }
+  __device__ __forceinline__ void put(int i, uint64_t v) {
+    __syncwarp();
+    if (leader) p[i] = v;
+    __syncwarp();
+  }
+  __device__ __forceinline__ void set(int id) {
+    const int i = id >> 6;
+    put(i, p[i] | (1ull << (id & 63)));
+    ++cnt;
+    hi = hi > i + 1 ? hi : i + 1;
+  }
+  __device__ __forceinline__ void reset(int id) {
+    const int i = id >> 6;
+    put(i, p[i] & ~(1ull << (id & 63)));
+    --cnt;
+  }
+  __device__ __forceinline__ bool test(int id) const { return ((p[id >> 6] >> (id & 63)) & 1ull) != 0; }
+  __device__ __forceinline__ uint64_t word(int i) const { return p[i]; }
+  __device__ __forceinline__ void andnot(int i, uint64_t m) {
+    const uint64_t w = p[i];
+    cnt -= __popcll(w & m);
+    put(i, w & ~m);
+  }
+  __device__ __forceinline__ bool any() const { return cnt > 0; }
+  __device__ __forceinline__ int count() const { return cnt; }
+  __device__ __forceinline__ int word_begin() const { return lo; }
+  __device__ __forceinline__ int word_end() const { return hi; }
+  // lowest member (cnt > 0); advances lo past empty words (uniform call)
+  __device__ __forceinline__ int lowest() {
+    while (p[lo] == 0) ++lo;
+    return lo * 64 + __ffsll(static_cast<long long>(p[lo])) - 1;
+  }
+  // k-th member in ascending id order (k < cnt); per-lane k may differ
+  __device__ __forceinline__ int select(int k) const {
+    for (int i = lo;; ++i) {
+      const uint64_t w = p[i];
+      const int c = __popcll(w);
+      if (k < c) return i * 64 + select64(w, k);
+      k -= c;
+    }
+  }
 };
 
 struct DecisionLog {

@@ -19,6 +19,7 @@ void* pick_sim_nw1(int g, bool trace, bool records, int sel);
 void* pick_sim_nw2(int g, bool trace, bool records, int sel);
 void* pick_sim_nw4(int g, bool trace, bool records, int sel);
 void* pick_sim_nw8(int g, bool trace, bool records, int sel);
+void* pick_sim_wide(bool trace, bool records);  // sim_inst_wide.cu
 
 namespace {
 
@@ -164,6 +165,16 @@ __device__ __forceinline__ void row_metrics_one(const RowMetricsParams& p, const
   }
 }
 
+// Rows longer than kMaxRequests: the same epilogue with each warp's
+// latencies in a global-memory slice (L1/L2-resident) instead of shared memory.
+__global__ void __launch_bounds__(128) row_metrics_wide_kernel(const RowMetricsParams p) {
+  const int lane = threadIdx.x & 31;
+  const int64_t gw = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t warps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  double* lat = p.lat_scratch + gw * p.wl.nmax;
+  for (int64_t i = gw; i < p.n_traj; i += warps) row_metrics_one(p, p.traj[i], lane, lat);
+}
+
 __global__ void __launch_bounds__(128) row_metrics_warp_kernel(const RowMetricsParams p) {
   __shared__ double lat_all[128 / kWarp][kMaxRequests];
   const int lane = threadIdx.x & 31;
@@ -186,8 +197,26 @@ void* pick_kernel(int nw, int g, bool trace, bool records, int sel = kSelAny) {
 
 }  // namespace
 
-int plan_sim(int nmax, int group, SimLaunch* out) {
+int plan_sim(int nmax, int group, bool wide, SimLaunch* out) {
   SimLaunch l{};
+  if (wide) {  // whole warps, everything in global scratch
+    l.wide = 1;
+    l.group = kWarp;
+    l.slot_rows = (nmax + kWarp - 1) / kWarp;
+    l.smem = 0;
+    int dev = 0, sms = 0, per_sm = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return 1;
+    if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) return 1;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pick_sim_wide(false, false),
+                                                      kSimBlock, 0) != cudaSuccess)
+      return 1;
+    if (per_sm < 1) return 3;
+    l.grid = sms * per_sm;
+    for (int v = 0; v < 3; ++v) l.grid_sel[v] = l.grid;
+    l.block = kSimBlock;
+    *out = l;
+    return 0;
+  }
   l.nwords = nmax <= 64 ? 1 : nmax <= 128 ? 2 : nmax <= 256 ? 4 : 8;
   // Widen the group until two blocks' slot tiles fit in shared memory.
   constexpr size_t kTileBudget = 100 * 1024;
@@ -234,9 +263,9 @@ int launch_sim(const SimParams& p, const SimLaunch& l, void* stream) {
   const bool trace = p.out.trace != nullptr;
   const bool records = p.out.admit != nullptr || p.out.demoted != nullptr;
   const int sel = p.mode_sel;
-  void* k = pick_kernel(l.nwords, l.group, trace, records, sel);
+  void* k = l.wide ? pick_sim_wide(trace, records) : pick_kernel(l.nwords, l.group, trace, records, sel);
   if (!k) return 1;
-  const int grid = (l.group == kWarp && !trace && !records) ? l.grid_sel[sel] : l.grid;
+  const int grid = (!l.wide && l.group == kWarp && !trace && !records) ? l.grid_sel[sel] : l.grid;
   SimParams q = p;
   q.no_streak = std::getenv("SABER_NO_STREAK") != nullptr;
   void* args[] = {&q};
@@ -259,6 +288,18 @@ int launch_tick_index(const WorkloadTables& wl, int64_t cells, const TickTable& 
 int launch_row_metrics(const RowMetricsParams& p, void* stream) {
   if (p.n_traj == 0) return 0;
   const int block = 128;
+  if (p.wl.nmax > kMaxRequests) {
+    // stream-ordered scratch: one latency slice per warp of a fixed grid
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    RowMetricsParams q = p;
+    void* lat = nullptr;
+    const size_t bytes = static_cast<size_t>(kRowMetricsWideWarps) * p.wl.nmax * sizeof(double);
+    if (cudaMallocAsync(&lat, bytes, st) != cudaSuccess) return 1;
+    q.lat_scratch = static_cast<double*>(lat);
+    row_metrics_wide_kernel<<<kRowMetricsWideWarps * kWarp / block, block, 0, st>>>(q);
+    const bool ok = cudaGetLastError() == cudaSuccess;
+    return cudaFreeAsync(lat, st) == cudaSuccess && ok ? 0 : 1;
+  }
   if (p.narrow) {  // one warp per block, so a block fits beside the trajectory kernels
     row_metrics_warp_kernel<<<296, kWarp, 0, static_cast<cudaStream_t>(stream)>>>(p);
   } else {

@@ -37,6 +37,7 @@
 #include <cmath>
 #include <cstdint>
 #include <cstdlib>
+#include <type_traits>
 
 #include "saber_internal.h"
 #include "sim_common.cuh"
@@ -365,11 +366,27 @@ __device__ __forceinline__ void gate_streak_warp(
 // max over the ledger's needs (ActiveLedger, scheduler.hpp:30-44), -inf when
 // empty.  Needs are >= +0, so their bit patterns order like the values; with
 // a whole warp per trajectory every lane tests two ids of each mask word.
-template <int G, int NW>
-__device__ __forceinline__ double ledger_max_of(const Mask<NW>& ledger, int size,
+template <int G, int NW, class MaskT>
+__device__ __forceinline__ double ledger_max_of(const MaskT& ledger, int size,
                                                 const double* __restrict__ LNEED, int sub) {
   if (size == 0) return -kInf;
-  if constexpr (G == kWarp) {
+  if constexpr (MaskT::kGlobal) {  // wide kernel: words [0, hi) in global memory
+    uint64_t k = 0;
+#pragma unroll 1
+    for (int i = 0; i < ledger.word_end(); ++i) {
+      const uint64_t wd = ledger.word(i);
+      if (wd == 0) continue;
+#pragma unroll
+      for (int hh = 0; hh < 2; ++hh) {
+        const int bit = hh * 32 + sub;
+        if ((wd >> bit) & 1ull) {
+          const uint64_t v = dbits(LNEED[i * 64 + bit]);
+          k = k < v ? v : k;
+        }
+      }
+    }
+    return bitsd(warp_max_u64(k));
+  } else if constexpr (G == kWarp) {
     uint64_t k = 0;
 #pragma unroll
     for (int i = 0; i < NW; ++i) {
@@ -400,12 +417,22 @@ __device__ __forceinline__ double ledger_max_of(const Mask<NW>& ledger, int size
 }
 
 // Simulates trajectory `ti` on this group.
-template <int NW, int G, bool kTrace, bool kRecords, int kSel>
+// Per-group global scratch of the wide kernel.
+struct WideScratch {
+  uint64_t* masks;   // [2][nw]: high tier, ledger
+  int nw;
+  int32_t* gate;     // [3][nmax]: Fisher-Yates j, window order, candidate id
+  double* need;      // [nmax] candidate needs
+};
+
+template <int NW, int G, bool kTrace, bool kRecords, int kSel, bool kWide = false>
 __device__ __forceinline__ void simulate_one(const SimParams& P, int ti, const Slots<G>& S,
                                              int sub, unsigned gmask,
                                              double* __restrict__ LNEED,
                                              uint16_t* __restrict__ LOW,
-                                             const uint32_t* __restrict__ INV) {
+                                             const uint32_t* __restrict__ INV,
+                                             const WideScratch& WS = WideScratch{}) {
+  static_assert(!kWide || (G == kWarp && kSel == kSelAny), "wide kernel: whole warps, any mode");
   const TrajDesc d = P.traj[P.order ? P.order[ti] : ti];
   const int n = d.n;
   const int nmax = P.wl.nmax;
@@ -433,9 +460,18 @@ __device__ __forceinline__ void simulate_one(const SimParams& P, int ti, const S
   const bool leader = sub == 0;
   saber_decision* tr = kTrace && P.out.trace ? P.out.trace + d.row * P.out.trace_cap : nullptr;
 
-  Mask<NW> high, ledger;
+  using MaskT = typename std::conditional<kWide, GMask, Mask<NW>>::type;
+  MaskT high, ledger;
+  if constexpr (kWide) {
+    high.bind(WS.masks, WS.nw, sub);
+    ledger.bind(WS.masks + WS.nw, WS.nw, sub);
+  }
   high.clear();
   ledger.clear();
+  // wide kernel: raw 64-bit scheduler draws (window > 16)
+  const uint64_t* __restrict__ draws64 =
+      kWide && saber ? reinterpret_cast<const uint64_t*>(P.rng.draws) + P.rng.off[d.stream]
+                     : nullptr;
   int ledger_size = 0;
   double ledger_max = -kInf;
   double min_td = kInf;  // lower bound on the earliest possible demotion
@@ -541,7 +577,7 @@ __device__ __forceinline__ void simulate_one(const SimParams& P, int ti, const S
           uint64_t hterm = 0;
           int ndem = 0;
 #pragma unroll 1
-          for (int q = 0; q < 2 * NW; ++q) {  // half-words of the tier mask
+          for (int q = 2 * high.word_begin(); q < 2 * high.word_end(); ++q) {  // half-words
             const uint32_t hw = static_cast<uint32_t>(high.word(q >> 1) >> ((q & 1) * 32));
             if (hw == 0) continue;
             const int id = q * 32 + sub;
@@ -619,7 +655,93 @@ __device__ __forceinline__ void simulate_one(const SimParams& P, int ti, const S
         st_cyc[4] += clock64() - scan_t0;
 #endif
       }
-      if (high.any()) {
+      if (kWide && high.any()) {
+        // admission_step, high tier (scheduler.cpp:58-95), any window: the
+        // Fisher-Yates j's lane-parallel (64-bit draws), the swaps by lane 0,
+        // then 32 window positions per round with the first passing one found
+        // by ballot.
+        const int hcount = high.count();
+        const int w = d.window < hcount ? d.window : hcount;
+        if (draw_pos + (w - 1) > draw_len) {
+          failed = true;
+          break;
+        }
+        int32_t* __restrict__ WJ = WS.gate;
+        int32_t* __restrict__ WO = WS.gate + nmax;
+        int32_t* __restrict__ WC = WS.gate + 2 * nmax;
+        double* __restrict__ WN = WS.need;
+        const double pred = MT[load + 1];
+        const bool violates = pred < ledger_max;  // ActiveLedger::violates
+        for (int q = sub; q < w - 1; q += kWarp)
+          WJ[q] = static_cast<int32_t>(draws64[draw_pos + q] % static_cast<uint64_t>(w - q));
+        for (int c = sub; c < w; c += kWarp) WO[c] = c;
+        __syncwarp();
+        if (leader) {
+          for (int q = 0; q < w - 1; ++q) {
+            const int i = w - 1 - q, j = WJ[q];
+            const int a = WO[i];
+            WO[i] = WO[j];
+            WO[j] = a;
+          }
+        }
+        __syncwarp();
+        int first = w;
+        for (int c0 = 0; c0 < w; c0 += kWarp) {
+          const int c = c0 + sub;
+          bool ok = false;
+          if (c < w) {
+            const int id = high.select(WO[c]);
+            const double need = queued_need(P.wl.max_out[wo + id], P.wl.deadline[wo + id], t);
+            WC[c] = id;
+            WN[c] = need;
+            ok = !(pred < need) && !violates;
+          }
+          const unsigned b = __ballot_sync(0xFFFFFFFFu, ok);
+          if (b) {
+            first = c0 + __ffs(b) - 1;
+            break;
+          }
+        }
+        __syncwarp();
+        draw_pos += w - 1;
+        rng_draws += w - 1;
+        ledger_scanned += ledger_size;
+        const int last = first < w ? first : w - 1;
+        uint64_t term = 0;
+        unsigned own = 0, act = 0;
+        for (int c = sub; c <= last; c += kWarp) {
+          const int id = WC[c];
+          const double need = WN[c];
+          const int kind = c < first ? (pred < need ? SABER_REJECT_OWN : SABER_REJECT_ACTIVE)
+                                     : SABER_ADMIT_HIGH;
+          const uint64_t pb = dbits(pred), rb = dbits(need);
+          term += decision_term(static_cast<uint64_t>(L.n + c), dbits(t),
+                                decision_word(id, kind, load), pb, rb);
+          if (kTrace && tr != nullptr)
+            write_decision(tr, L.n + c, P.out.trace_cap, P.out.error, t, id, kind, load, pb, rb);
+          own += kind == SABER_REJECT_OWN;
+          act += kind == SABER_REJECT_ACTIVE;
+        }
+        L.h += warp_sum_u64(term);
+        L.k2 += static_cast<int32_t>(__reduce_add_sync(0xFFFFFFFFu, own));
+        L.k3 += static_cast<int32_t>(__reduce_add_sync(0xFFFFFFFFu, act));
+        L.n += last + 1;
+        cands += last + 1;
+        if (first < w) {
+          const int id = WC[first];
+          const double need = WN[first];
+          __syncwarp();  // every lane has read the window before it is reused
+          admit(id, t);
+          ledger.set(id);
+          ++ledger_size;
+          if (leader) LNEED[id] = need;
+          __syncwarp();
+          ledger_max = (ledger_max < need) ? need : ledger_max;
+          high.reset(id);
+          L.k0 += 1;
+        }
+        __syncwarp();
+      } else if (!kWide && high.any()) {
         // admission_step, high tier (scheduler.cpp:58-95).
         const int hcount = high.count();
         const int w = d.window < hcount ? d.window : hcount;
@@ -814,7 +936,7 @@ __device__ __forceinline__ void simulate_one(const SimParams& P, int ti, const S
     // decisions are generated lane-parallel (gate_streak below).
     const bool gate_streak = saber && high.any();
     if (use_tab && !sblock && A > 0 &&
-        (saber ? (gate_streak ? (G >= kMaxWindow && gate_idle) : low_head == low_tail)
+        (saber ? (gate_streak ? (!kWide && G >= kMaxWindow && gate_idle) : low_head == low_tail)
                : !(A < d.cap && high.any()))) {
       const int k0 = ticks - 1;
       const double dtm = P.ticks.dt_max;
@@ -859,7 +981,7 @@ __device__ __forceinline__ void simulate_one(const SimParams& P, int ti, const S
           }
           if (A > npre) rem_lb = rem_lb - static_cast<double>(K) * delta;
           rem_exact = false;
-          if (gate_streak) {
+          if constexpr (!kWide) if (gate_streak) {
             const int hc = high.count();
             SEC_BEGIN();
             if constexpr (G == kWarp)
@@ -1148,6 +1270,43 @@ __global__ void __launch_bounds__(kSimBlock, kSel == kSelStatic  ? SABER_STATIC_
     if (ti >= P.n_traj) break;
     simulate_one<NW, G, kTrace, kRecords, kSel>(P, ti, S, sub, gmask, LNEED, LOW, inv);
     __syncwarp(gmask);
+  }
+}
+
+// The wide kernel: one trajectory per warp, slots, tier
+// masks and the gate window in the warp's global scratch (L1/L2-resident),
+// any n <= kMaxRequestsWide and any window.  No dynamic shared memory.
+template <bool kTrace, bool kRecords>
+__global__ void __launch_bounds__(kSimBlock) sim_kernel_wide(const SimParams P) {
+  const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
+  const int64_t group_id = static_cast<int64_t>(blockIdx.x) * (kSimBlock / kWarp) + warp;
+  if (group_id >= P.scratch.groups) {
+    if (lane == 0) atomicCAS(P.out.error, kErrNone, kErrBadDesc);
+    return;
+  }
+  const int64_t nmax = P.wl.nmax;
+  const int nw = P.scratch.wmask_nw;
+  Slots<kWarp> S;
+  S.g = P.scratch.wslot_g + group_id * nmax;
+  S.m = P.scratch.wslot_m + group_id * nmax;
+  S.dbuf = nullptr;
+  S.col0 = 0;
+  WideScratch WS;
+  WS.masks = P.scratch.wmask + group_id * 2 * nw;
+  WS.nw = nw;
+  WS.gate = P.scratch.wgate + group_id * 3 * nmax;
+  WS.need = P.scratch.wneed + group_id * nmax;
+  double* LNEED = P.scratch.ledger_need + group_id * nmax;
+  uint16_t* LOW = P.scratch.low_fifo + group_id * nmax;
+  for (;;) {
+    int ti = 0;
+    if (lane == 0) ti = P.first_traj + atomicAdd(P.next_traj, 1);
+    ti = __shfl_sync(0xFFFFFFFFu, ti, 0);
+    if (ti >= P.n_traj) break;
+    simulate_one<1, kWarp, kTrace, kRecords, kSelAny, true>(P, ti, S, lane, 0xFFFFFFFFu, LNEED,
+                                                            LOW, nullptr, WS);
+    __syncwarp();
   }
 }
 
