@@ -1,7 +1,8 @@
 #!/usr/bin/env python3
 """BASELINE config 4: batched USL/linear/logistic fitting + calibrate selection
 over synthetic profiled latency curves (SURVEY §8(d) recipe: truth usl
-v1~U[50,150], sigma~U[0,0.2], kappa~U[0,0.005], loads 1..50, 1% noise).
+v1~U[50,150], sigma~U[0,0.2], kappa~U[0,0.005], loads 1..50, 1% noise;
+mt19937_64(2026) + the reference's uniform01, benchmarks/recipes.py).
 
     python benchmarks/fit_bench.py [--curves 1000000] [--cpu-sample 2000]
 
@@ -22,16 +23,29 @@ import numpy as np
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 sys.path.insert(0, os.path.join(ROOT, "oracle"))
+sys.path.insert(0, os.path.join(ROOT, "benchmarks"))
+import recipes  # noqa: E402
 
 
 def curves(n, seed=2026, m=50):
-    rng = np.random.default_rng(seed)
-    truth = np.stack([rng.uniform(50, 150, n), rng.uniform(0, 0.2, n), rng.uniform(0, 0.005, n)], 1)
-    L = np.arange(1, m + 1, dtype=np.float64)
-    denom = 1.0 + truth[:, 1:2] * (L - 1.0) + truth[:, 2:3] * L * (L - 1.0)
-    speeds = truth[:, 0:1] / denom * (1.0 + 0.01 * (rng.random((n, m)) - 0.5))
-    loads = np.tile(np.arange(1, m + 1, dtype=np.int32), n)
-    return loads, speeds.reshape(-1), np.arange(0, n * m + 1, m, dtype=np.int64)
+    """SURVEY §8(d) config-4 recipe: mt19937_64(2026) + uniform01 (recipes.py)."""
+    loads, speeds, offsets, _ = recipes.config4_curves(n, seed, m)
+    return loads, speeds, offsets
+
+
+def algorithmic_fp64(res, offsets):
+    """SURVEY §8(d) K3 work from the in-kernel iteration / trial counts."""
+    m = np.diff(offsets).astype(np.float64)
+    W = 0.0
+    for fam, E in ((0, 7.0), (1, 8.0)):
+        ok = res.status[fam] >= 0
+        I = res.iterations[fam].astype(np.float64)
+        T = res.trials[fam].astype(np.float64)
+        W += float(np.sum((I * (m * (7 * E + 21) + 30) + T * (m * (E + 3) + 45) +
+                           m * (E + 4) + m * (E + 6) + (999 * E if fam == 1 else 0.0))[ok]))
+    W += float(np.sum((9 * m + 10)[res.status[2] >= 0]))
+    exps = float(np.sum(7 * m * res.iterations[1] + m * res.trials[1]))
+    return W, exps
 
 
 def main():
@@ -55,11 +69,23 @@ def main():
         per_family[name] = {"fits_per_s_device": args.curves / (r.device_ms / 1e3),
                             "ok": int((r.status[fam] == 0).sum()),
                             "mean_lm_iterations": float(r.iterations[fam].mean())}
+    W, exps = algorithmic_fp64(res, offsets)
+    peak = S.fp64_peak_tflops(0)
+    achieved = W / (min(devs) / 1e3) / 1e12
     out = {"config": "config4: fit usl+logistic+linear + calibrate over synthetic curves (m=50)",
            "curves": args.curves, "gpu_calibrations_per_s_e2e": args.curves / min(walls),
            "gpu_calibrations_per_s_device": args.curves / (min(devs) / 1e3),
            "device_ms": min(devs), "per_family": per_family,
-           "best_family_counts": np.bincount(res.best_family + 2, minlength=5).tolist()}
+           "best_family_counts": np.bincount(res.best_family + 2, minlength=5).tolist(),
+           "lm_counts": {f: {"iterations": int(res.iterations[k].sum()), "trials": int(res.trials[k].sum())}
+                         for k, f in ((0, "usl"), (1, "logistic"))},
+           "roofline": {"bound": "fp64", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                        "frac": achieved / peak, "algorithmic_fp64_ops": W, "exp_calls": exps,
+                        "kernel": "whole fit_batch (H2D, lm_kernel, select, calibrate, D2H) device time",
+                        "work": "SURVEY §8(d): per start I(m(7E+21)+30) + T(m(E+3)+45), E_usl=7, "
+                                "E_log=8 (exp as 1 op), + polish m(E+4), monotone 999E (non-USL), "
+                                "r2 m(E+6); linear 9m+10; I, T counted in-kernel",
+                        "peak_source": "measured live: DFMA microbenchmark (saber_cuda_fp64_peak)"}}
     import oracle as O
     if O.reference_available() and args.cpu_sample > 0:
         ref = O.Oracle("reference")

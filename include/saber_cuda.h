@@ -534,6 +534,9 @@ typedef struct {
   int32_t* iterations;     /* [3 * n_curves] total LM iterations over the 5 starts (or NULL) */
   double device_ms;
   int32_t kernel_launches;
+  int32_t* trials;         /* [3 * n_curves] total LM damping trials (solve + sse) over the
+                              5 starts (or NULL): with `iterations`, the in-kernel counts of
+                              the algorithmic FP64 work */
 } saber_fit_out;
 
 /* FitError reasons (estimator.cpp:208-346), i.e. FitError::what():

@@ -152,7 +152,7 @@ class saber_fit_out(C.Structure):
     _fields_ = [("params", C.POINTER(C.c_double)), ("r2", C.POINTER(C.c_double)),
                 ("status", C.POINTER(C.c_int32)), ("best_family", C.POINTER(C.c_int32)),
                 ("iterations", C.POINTER(C.c_int32)), ("device_ms", C.c_double),
-                ("kernel_launches", C.c_int32)]
+                ("kernel_launches", C.c_int32), ("trials", C.POINTER(C.c_int32))]
 
 
 SABER_MC_STATS = 8

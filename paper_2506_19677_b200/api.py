@@ -872,6 +872,7 @@ class FitBatchResult:
     iterations: np.ndarray   # [3][n_curves] LM iterations over the 5 starts
     device_ms: float
     kernel_launches: int
+    trials: Optional[np.ndarray] = None  # [3][n_curves] LM damping trials over the 5 starts
 
 
 def fit_batch(loads, speeds, offsets, family_mask: int = 0x7, calibrate: bool = False,
@@ -887,6 +888,7 @@ def fit_batch(loads, speeds, offsets, family_mask: int = 0x7, calibrate: bool = 
     status = np.zeros((3, n), dtype=np.int32)
     best = np.zeros(n, dtype=np.int32) if calibrate else None
     iters = np.zeros((3, n), dtype=np.int32)
+    trials = np.zeros((3, n), dtype=np.int32)
     d = N.saber_fit_desc()
     P = C.POINTER
     d.loads = loads.ctypes.data_as(P(C.c_int32))
@@ -903,8 +905,9 @@ def fit_batch(loads, speeds, offsets, family_mask: int = 0x7, calibrate: bool = 
     if calibrate:
         o.best_family = best.ctypes.data_as(P(C.c_int32))
     o.iterations = iters.ctypes.data_as(P(C.c_int32))
+    o.trials = trials.ctypes.data_as(P(C.c_int32))
     _check(N.lib().saber_cuda_fit_batch(C.byref(d), C.byref(o)))
-    return FitBatchResult(params, r2, status, best, iters, o.device_ms, o.kernel_launches)
+    return FitBatchResult(params, r2, status, best, iters, o.device_ms, o.kernel_launches, trials)
 
 
 def _samples_arrays(samples):

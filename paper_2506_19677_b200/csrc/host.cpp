@@ -1859,18 +1859,20 @@ extern "C" saber_status saber_cuda_fit_batch(const saber_fit_desc* desc, saber_f
     if (desc->loads[i] < 1) return fail(SABER_EDOMAIN, "predict: load must be >= 1");
   if (saber_status s = use_device(desc->device)) return s;
   const int dev = desc->device;
-  DevBuf loads, speeds, offs, scratch, conv, iters, params, r2, status, best, itc, cursor;
+  DevBuf loads, speeds, offs, scratch, conv, iters, trs, params, r2, status, best, itc, trc, cursor;
   ALLOC_TRY(loads, dev, static_cast<size_t>(std::max<int64_t>(1, M)) * 4);
   ALLOC_TRY(speeds, dev, static_cast<size_t>(std::max<int64_t>(1, M)) * 8);
   ALLOC_TRY(offs, dev, static_cast<size_t>(N + 1) * 8);
   ALLOC_TRY(scratch, dev, static_cast<size_t>(2) * N * 5 * 4 * 8);
   ALLOC_TRY(conv, dev, static_cast<size_t>(2) * N * 5 * 4);
   ALLOC_TRY(iters, dev, static_cast<size_t>(2) * N * 5 * 4);
+  ALLOC_TRY(trs, dev, static_cast<size_t>(2) * N * 5 * 4);
   ALLOC_TRY(params, dev, static_cast<size_t>(3) * N * 3 * 8);
   ALLOC_TRY(r2, dev, static_cast<size_t>(3) * N * 8);
   ALLOC_TRY(status, dev, static_cast<size_t>(3) * N * 4);
   ALLOC_TRY(best, dev, static_cast<size_t>(N) * 4);
   ALLOC_TRY(itc, dev, static_cast<size_t>(3) * N * 4);
+  ALLOC_TRY(trc, dev, static_cast<size_t>(3) * N * 4);
   ALLOC_TRY(cursor, dev, 16);
   Timer tm;
   if (saber_status s = tm.init()) return s;
@@ -1898,6 +1900,8 @@ extern "C" saber_status saber_cuda_fit_batch(const saber_fit_desc* desc, saber_f
   fp.lm_scratch = scratch.as<double>();
   fp.lm_conv = conv.as<int32_t>();
   fp.lm_iters = iters.as<int32_t>();
+  fp.lm_trials = trs.as<int32_t>();
+  fp.trials = trc.as<int32_t>();
   fp.cursor = cursor.as<int32_t>();
   int launches = 0;
   LAUNCH_TRY(launch_fit(fp, st, &launches));
@@ -1908,6 +1912,8 @@ extern "C" saber_status saber_cuda_fit_batch(const saber_fit_desc* desc, saber_f
     CUDA_TRY(cudaMemcpyAsync(out->best_family, best.p, static_cast<size_t>(N) * 4, cudaMemcpyDeviceToHost, st));
   if (out->iterations)
     CUDA_TRY(cudaMemcpyAsync(out->iterations, itc.p, static_cast<size_t>(3) * N * 4, cudaMemcpyDeviceToHost, st));
+  if (out->trials)
+    CUDA_TRY(cudaMemcpyAsync(out->trials, trc.p, static_cast<size_t>(3) * N * 4, cudaMemcpyDeviceToHost, st));
   CUDA_TRY(cudaEventRecord(tm.b, st));
   CUDA_TRY(cudaEventSynchronize(tm.b));
   float ms = 0.f;

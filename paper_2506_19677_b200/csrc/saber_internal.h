@@ -344,6 +344,8 @@ struct FitParams {
   double* lm_scratch;  // [3*n_curves*5][4]: per-start (p0,p1,p2,sse)
   int32_t* lm_conv;    // [3*n_curves*5]
   int32_t* lm_iters;   // [3*n_curves*5]
+  int32_t* lm_trials;  // [3*n_curves*5] damping trials per start
+  int32_t* trials;     // [3*n_curves] summed over the starts (or null)
   int32_t* cursor;     // work queue
 };
 int launch_fit(const FitParams& p, void* stream, int* launches);

@@ -168,12 +168,23 @@ __device__ __forceinline__ double streak_chunks(const Slots<G>& S, int sub, int 
 
 // kCompact (the SABER kernel): one chunk width for every slot count — a
 // smaller instruction footprint measured faster than the specialised widths
-// for that kernel (config 3: 839K -> 851K traj/s).
+// for that kernel.  SABER keeps the batch small (A <= 32 nearly always), so
+// the width is one slot per lane.
+#ifndef SABER_COMPACT_KC
+#define SABER_COMPACT_KC 1
+#endif
+#ifndef SABER_COMPACT_DEC
+#define SABER_COMPACT_DEC 1
+#endif
 template <int G, bool kCompact = false>
 __device__ __forceinline__ double streak_slots(const Slots<G>& S, int sub, int A, int npre,
                                                double speed, const double* __restrict__ DT, int K,
                                                double pf) {
-  if (kCompact) return streak_chunks<G, 4, false>(S, sub, A, speed, DT, K, pf);
+  if (kCompact) {
+    if (SABER_COMPACT_DEC && npre == 0)
+      return streak_chunks<G, SABER_COMPACT_KC, true>(S, sub, A, speed, DT, K, pf);
+    return streak_chunks<G, SABER_COMPACT_KC, false>(S, sub, A, speed, DT, K, pf);
+  }
   if (A <= G) return streak_chunks<G, 1, false>(S, sub, A, speed, DT, K, pf);
   if (npre == 0) {  // min_pf is +inf and stays so
     if (A <= 2 * G) return streak_chunks<G, 2, true>(S, sub, A, speed, DT, K, pf);
@@ -952,15 +963,48 @@ __device__ __forceinline__ void simulate_one(const SimParams& P, int ti, const S
       }
       // The bounds only shrink until the next admission / exact pass.
       if (Kb < 2) sblock = true;
+      // Arrivals that cannot change any scheduler step of the streak are
+      // absorbed into it: a SABER gate streak whose window
+      // is full (a new id enters the high tier behind the window, so every
+      // gate of the streak sees the same w candidates).  (Static streaks with
+      // a full batch could absorb arrivals too, but they end at the next
+      // prefill end / completion long before an arrival: measured no gain.)
+      const bool absorb = gate_streak && high.count() >= d.window;
       int K = 0;
       if (Kb >= 2) {
-        K = min(Kb, min(ka - k0, kh - 1 - k0));
+        K = min(Kb, kh - 1 - k0);
+        if (!absorb) K = min(K, ka - k0);
         if (gate_streak) {
           // no refresh scan (t < min_td) and enough scheduler draws
           K = min(K, min_kd - k0);
           if (gate_w > 1)
             K = static_cast<int>(min(static_cast<int64_t>(K),
                                      1 + (draw_len - draw_pos) / (gate_w - 1)));
+        }
+      }
+      const int hc_streak = gate_streak ? high.count() : 0;
+      int64_t arr_extra = 0;  // high-tier entries the absorbed arrivals add to later refreshes
+      if (absorb && K >= 2 && next < n && ka < k0 + K) {
+        // the streak must also end before any absorbed request's demotion
+        // bound tick (its refresh could demote it)
+        if (saber) {
+          for (int q = next; q < n && P.wl.arr_tick[wo + q] < k0 + K; ++q)
+            K = min(K, P.wl.dem_tick[wo + q] - k0);
+        }
+        if (K >= 2) {
+          while (next < n) {
+            const int a = P.wl.arr_tick[wo + next];
+            if (a >= k0 + K) break;
+            high.set(next);
+            if (saber) {
+              min_td = dmin(min_td, P.wl.demote_after[wo + next]);
+              min_kd = min(min_kd, P.wl.dem_tick[wo + next]);
+            }
+            arr_extra += k0 + K - a;
+            ++next;
+          }
+          na_t = next < n ? P.wl.arrival[wo + next] : kInf;
+          ka = next < n ? P.wl.arr_tick[wo + next] : P.ticks.len;
         }
       }
       if (K >= 2) {
@@ -982,7 +1026,6 @@ __device__ __forceinline__ void simulate_one(const SimParams& P, int ti, const S
           if (A > npre) rem_lb = rem_lb - static_cast<double>(K) * delta;
           rem_exact = false;
           if constexpr (!kWide) if (gate_streak) {
-            const int hc = high.count();
             SEC_BEGIN();
             if constexpr (G == kWarp)
               gate_streak_warp<kTrace, NW>(P, S, sub, high, P.wl.max_out + wo, P.wl.deadline + wo,
@@ -997,7 +1040,7 @@ __device__ __forceinline__ void simulate_one(const SimParams& P, int ti, const S
             rng_draws += static_cast<int32_t>(extra * (gate_w - 1));
             cands += static_cast<int32_t>(extra * gate_w);
             ledger_scanned += static_cast<int32_t>(extra * ledger_size);
-            refresh_entries += static_cast<int32_t>(extra * hc);
+            refresh_entries += static_cast<int32_t>(extra * hc_streak + arr_extra);
           }
 #ifdef SABER_STREAK_STATS
           st_ticks += K;

@@ -126,3 +126,38 @@ def test_profile_batch_matches_reference(engine, ref):
     # the full calibration pipeline on the device reproduces SURVEY §8(d)
     rep = S.calibrate(list(zip(got[0][0].tolist(), got[0][1].tolist())))
     assert list(rep.best.params) == [99.999999999997357, 0.049999999999992085, 0.0010000000000001078]
+
+
+def test_fit_config4_recipe_matches_compiled_reference(engine, ref):
+    """Config 4's own inputs (mt19937_64(2026) + uniform01,
+    benchmarks/recipes.py) against the compiled reference: USL and linear
+    parameters and r^2 bit-identical, logistic status and SSE within
+    LOGISTIC_SSE_RTOL, calibrate()'s selected family identical."""
+    import recipes
+    n = 160
+    loads, speeds, offsets, _ = recipes.config4_curves(n)
+    res = engine.fit_batch(loads, speeds, offsets, calibrate=True)
+    bad = []
+    for c in range(n):
+        lo, hi = offsets[c], offsets[c + 1]
+        cal = ref.calibrate(loads[lo:hi], speeds[lo:hi])
+        if res.best_family[c] != cal["best_family"]:
+            bad.append((c, "best", res.best_family[c], cal["best_family"]))
+        for f in (O.USL, O.LINEAR, O.LOGISTIC):
+            ok = cal["ok"][f] != 0
+            st = res.status[f, c]
+            if (st == 0) != ok:
+                bad.append((c, f, "status", st, ok))
+                continue
+            if not ok:
+                continue
+            got, want = res.params[f, c], cal["params"][f]
+            if f == O.LOGISTIC:
+                a = logistic_sse(got, loads[lo:hi].astype(float), speeds[lo:hi])
+                b = logistic_sse(want, loads[lo:hi].astype(float), speeds[lo:hi])
+                if abs(a - b) > LOGISTIC_SSE_RTOL * max(b, 1e-300):
+                    bad.append((c, f, "sse", a, b))
+            elif list(got) != list(want) or res.r2[f, c] != cal["r2"][f]:
+                bad.append((c, f, list(got), list(want), res.r2[f, c], cal["r2"][f]))
+    assert bad == []
+

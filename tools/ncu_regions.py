@@ -23,7 +23,8 @@ MARKS = [  # (region, first line containing the marker)
     ("prologue", "// Simulates trajectory"),
     ("arrivals", "    // Arrivals due at t"),
     ("refresh", "      const int hc = high.count();"),
-    ("gate", "      if (high.any()) {"),
+    ("gate", "      } else if (!kWide && high.any()) {"),
+    ("gate_wide", "      if (kWide && high.any()) {"),
     ("lowtier/static", "      } else if (low_head < low_tail) {"),
     ("streak_setup", "    if (t >= horizon) break;"),
     ("engine_quiet", "    const double nt = (horizon < t + tick)"),
