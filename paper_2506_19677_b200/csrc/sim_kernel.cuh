@@ -545,6 +545,10 @@ __device__ __forceinline__ void simulate_one(const SimParams& P, int ti, const S
   const long long st_t0 = clock64();
   long long st_cyc[5] = {0, 0, 0, 0, 0};
   int st_scans = 0;
+  // streak-end causes (stats build): [0..3] K >= 2 bound by Kb / arrival /
+  // demotion or draws / horizon; [4..7] the same for K < 2 attempts;
+  // [8..11] streak condition false: sblock / A == 0 / gate admitted / other
+  int st_cause[12] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
 #endif
 
   double t = 0.0;
@@ -946,6 +950,14 @@ __device__ __forceinline__ void simulate_one(const SimParams& P, int ti, const S
     // rejects the same window again (need = m / (dl - t) only grows), so its
     // decisions are generated lane-parallel (gate_streak below).
     const bool gate_streak = saber && high.any();
+#ifdef SABER_STREAK_STATS
+    {
+      const bool cond = saber ? (gate_streak ? (!kWide && G >= kMaxWindow && gate_idle) : low_head == low_tail)
+                              : !(A < d.cap && high.any());
+      if (use_tab && !(!sblock && A > 0 && cond))
+        st_cause[sblock ? 8 : A == 0 ? 9 : (gate_streak && !gate_idle) ? 10 : 11] += 1;
+    }
+#endif
     if (use_tab && !sblock && A > 0 &&
         (saber ? (gate_streak ? (!kWide && G >= kMaxWindow && gate_idle) : low_head == low_tail)
                : !(A < d.cap && high.any()))) {
@@ -982,6 +994,16 @@ __device__ __forceinline__ void simulate_one(const SimParams& P, int ti, const S
                                      1 + (draw_len - draw_pos) / (gate_w - 1)));
         }
       }
+#ifdef SABER_STREAK_STATS
+      {
+        const int kbv = Kb;
+        const int kav = absorb ? 1 << 30 : ka - k0;
+        const int kdv = gate_streak ? min(min_kd - k0, gate_w > 1 ? static_cast<int>(min(static_cast<int64_t>(1 << 30), 1 + (draw_len - draw_pos) / (gate_w - 1))) : 1 << 30) : 1 << 30;
+        const int base = K >= 2 ? 0 : 4;
+        const int Kc = Kb < 2 ? Kb : K;
+        st_cause[base + (Kc == kbv ? 0 : Kc == kav ? 1 : Kc == kdv ? 2 : 3)] += 1;
+      }
+#endif
       const int hc_streak = gate_streak ? high.count() : 0;
       int64_t arr_extra = 0;  // high-tier entries the absorbed arrivals add to later refreshes
       if (absorb && K >= 2 && next < n && ka < k0 + K) {
@@ -1046,6 +1068,14 @@ __device__ __forceinline__ void simulate_one(const SimParams& P, int ti, const S
           st_ticks += K;
           st_count += 1;
 #endif
+          // A streak that used up the engine bound leaves < 2 passes of it:
+          // the next attempt would fail, so none is made until the next
+          // event resets sblock (streaks are an optimisation; skipping one
+          // never changes a result).
+#ifndef SABER_SBLOCK_AFTER_KB
+#define SABER_SBLOCK_AFTER_KB 1
+#endif
+          if (SABER_SBLOCK_AFTER_KB && K == Kb) sblock = true;
           ticks += K - 1;  // this tick was counted above
           passes += K;
           prefill_updates += K * npre;
@@ -1270,6 +1300,14 @@ __device__ __forceinline__ void simulate_one(const SimParams& P, int ti, const S
     R->rng_draws = st_cyc[4];
     R->gate_candidates = st_scans;
     R->decision_hash = (static_cast<uint64_t>(st_quiet) << 32) | static_cast<uint32_t>(st_exact);
+    R->refresh_entries = 0;
+    R->ledger_scanned = 0;
+    R->prefill_updates = 0;
+    for (int q = 0; q < 4; ++q) {
+      R->refresh_entries |= static_cast<int64_t>(min(st_cause[q], 0xFFFF)) << (16 * q);
+      R->ledger_scanned |= static_cast<int64_t>(min(st_cause[4 + q], 0xFFFF)) << (16 * q);
+      R->prefill_updates |= static_cast<int64_t>(min(st_cause[8 + q], 0xFFFF)) << (16 * q);
+    }
 #endif
     if (kTrace && P.out.trace_count) P.out.trace_count[d.row] = L.n;
   }
