@@ -1086,6 +1086,23 @@ __device__ __forceinline__ void simulate_one(const SimParams& P, int ti, const S
         }
       }
     }
+    // Idle engine and empty queues: nothing happens before the tick of the
+    // next arrival, so those ticks (each: no scheduler action, advance_to
+    // with no active request) are skipped on the tick table.
+#ifndef SABER_IDLE_SKIP
+#define SABER_IDLE_SKIP 1
+#endif
+    if (SABER_IDLE_SKIP && use_tab && A == 0 && completed < n && !high.any() &&
+        low_head == low_tail) {
+      const int k0 = ticks - 1;
+      const int kj = min(ka, kh - 1);
+      if (kj - k0 >= 2) {
+        ticks += kj - k0 - 1;
+        t = P.ticks.T[kj];
+        clock = t;
+        continue;
+      }
+    }
     const double nt = (horizon < t + tick) ? horizon : t + tick;
 
     // Engine::advance_to(nt) (engine.cpp:51-127).
