@@ -160,11 +160,23 @@ struct Mask {
   __device__ __forceinline__ int lowest() const {
     return w ? B * 64 + __ffsll(static_cast<long long>(w)) - 1 : r.lowest();
   }
-  // k-th set bit in ascending id order (0-based); k < count().
-  __device__ __forceinline__ int select(int k) const {
+  // k-th set bit in ascending id order (0-based); k < count().  The word
+  // holding it is picked with selects (no per-word copy of select64).
+  __device__ __forceinline__ void pick(int& k, uint64_t& word, int& base) const {
     const int c = __popcll(w);
-    if (k < c) return B * 64 + select64(w, k);
-    return r.select(k - c);
+    if (k < c) {
+      word = w;
+      base = B * 64;
+    } else {
+      k -= c;
+      r.pick(k, word, base);
+    }
+  }
+  __device__ __forceinline__ int select(int k) const {
+    uint64_t word = w;
+    int base = 0;
+    pick(k, word, base);
+    return base + select64(word, k);
   }
 };
 template <int B>
@@ -180,6 +192,7 @@ struct Mask<0, B> {
   __device__ __forceinline__ int count() const { return 0; }
   __device__ __forceinline__ int lowest() const { return -1; }
   __device__ __forceinline__ int select(int) const { return -1; }
+  __device__ __forceinline__ void pick(int&, uint64_t&, int&) const {}
 };
 
 // Tier mask of the wide kernel: `nw` 64-bit words in the

@@ -1151,6 +1151,7 @@ __device__ __forceinline__ void simulate_one(const SimParams& P, int ti, const S
 #endif
       if (!rem_exact) {
         double r = kInf;
+#pragma unroll 1
         for (int k = sub, s = S.idx(sub); k < A; k += G, s += kWarp) {
           const double g = S.g[s];
           if (g >= 0.0) r = dmin(r, bitsd(S.m[s] & ~kIdMask) - g);
@@ -1238,6 +1239,7 @@ __device__ __forceinline__ void simulate_one(const SimParams& P, int ti, const S
         // compacts the slot array by swap-with-last.
         __syncwarp(gmask);
         bool dirty = false;
+#pragma unroll 1
         for (int k = 0; k < A; ++k) {
           const int s = S.idx(k);
           if (dbits(S.g[s]) != kDoneMark) continue;
