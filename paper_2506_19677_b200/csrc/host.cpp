@@ -381,7 +381,7 @@ struct Scratch {
 };
 
 struct Workloads {
-  DevBuf arr, dl, sla, mo, in, task, dem, hor, items, seed_base, th, tt, tl;
+  DevBuf arr, dl, sla, mo, in, pf, task, dem, hor, items, seed_base, th, tt, tl;
   DevBuf ka, kd;  // tick-table indices of arrival / demote_after (launch_tick_index)
   WorkloadTables view(int nmax) const {
     WorkloadTables w;
@@ -390,6 +390,7 @@ struct Workloads {
     w.sla = sla.as<double>();
     w.max_out = mo.as<double>();
     w.input = in.as<double>();
+    w.prefill = pf.as<double>();
     w.task = task.as<int8_t>();
     w.demote_after = dem.as<double>();
     w.horizon = hor.as<double>();
@@ -405,6 +406,7 @@ struct Workloads {
     ALLOC_TRY(sla, device, cells * 8);
     ALLOC_TRY(mo, device, cells * 8);
     ALLOC_TRY(in, device, cells * 8);
+    ALLOC_TRY(pf, device, cells * 8);
     ALLOC_TRY(task, device, cells);
     ALLOC_TRY(dem, device, cells * 8);
     ALLOC_TRY(hor, device, static_cast<size_t>(n_work) * 8);
@@ -684,6 +686,7 @@ saber_status saber_cuda_sweep_plan_create(const saber_sweep_desc* desc, saber_sw
         it.rps = P->rps[static_cast<size_t>(ri)];
         it.jitter = desc->length_jitter;
         it.ceiling = desc->with_saber ? P->ceiling : std::nan("");
+        it.prefill_rate = desc->prefill_rate;
       }
   std::vector<double> th(static_cast<size_t>(n_mixes) * 4);
   std::vector<int8_t> tt(static_cast<size_t>(n_mixes) * 4), tlast(static_cast<size_t>(n_mixes));
@@ -891,6 +894,7 @@ static saber_status plan_launch_impl(saber_sweep_plan* P, void* stream, bool wit
   wp.sla = P->wl.sla.as<double>();
   wp.max_out = P->wl.mo.as<double>();
   wp.input = P->wl.in.as<double>();
+  wp.prefill = P->wl.pf.as<double>();
   wp.demote_after = P->wl.dem.as<double>();
   wp.horizon = P->wl.hor.as<double>();
   wp.task = P->wl.task.as<int8_t>();
@@ -1417,6 +1421,7 @@ extern "C" saber_status saber_cuda_run_batch(const saber_run_batch_desc* desc,
     it.rps = s.rps;
     it.jitter = s.length_jitter;
     it.ceiling = ceiling;
+    it.prefill_rate = s.prefill_rate;
     double last_bound = 0.0, max_sla = 12.0;
     if (s.requests) {
       it.kind = 1;
@@ -1594,6 +1599,7 @@ extern "C" saber_status saber_cuda_run_batch(const saber_run_batch_desc* desc,
   wp.sla = wl.sla.as<double>();
   wp.max_out = wl.mo.as<double>();
   wp.input = wl.in.as<double>();
+  wp.prefill = wl.pf.as<double>();
   wp.demote_after = wl.dem.as<double>();
   wp.horizon = wl.hor.as<double>();
   wp.task = wl.task.as<int8_t>();
@@ -1771,6 +1777,7 @@ extern "C" saber_status saber_cuda_generate(const saber_workload_spec* specs, in
     it.rps = w.rps;
     it.jitter = w.length_jitter;
     it.ceiling = std::nan("");
+    it.prefill_rate = 0.0;
     TrajDesc& d = descs[static_cast<size_t>(k)];
     d = TrajDesc{};
     d.workload = k;
@@ -1810,6 +1817,7 @@ extern "C" saber_status saber_cuda_generate(const saber_workload_spec* specs, in
   wp.sla = wl.sla.as<double>();
   wp.max_out = wl.mo.as<double>();
   wp.input = wl.in.as<double>();
+  wp.prefill = wl.pf.as<double>();
   wp.demote_after = wl.dem.as<double>();
   wp.horizon = wl.hor.as<double>();
   wp.task = wl.task.as<int8_t>();
@@ -2116,6 +2124,7 @@ extern "C" saber_status saber_cuda_mc_sweep(const saber_mc_desc* desc, saber_mc_
   mp.sla = wl.sla.as<double>();
   mp.max_out = wl.mo.as<double>();
   mp.input = wl.in.as<double>();
+  mp.prefill = wl.pf.as<double>();
   mp.demote_after = wl.dem.as<double>();
   mp.horizon = wl.hor.as<double>();
   mp.task = wl.task.as<int8_t>();

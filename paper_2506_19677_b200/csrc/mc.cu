@@ -99,6 +99,7 @@ __global__ void mc_workloads_kernel(const McParams p) {
     p.sla[o + q] = sla;
     p.max_out[o + q] = static_cast<double>(out);
     p.input[o + q] = static_cast<double>(in);
+    p.prefill[o + q] = p.prefill_rate > 0.0 ? static_cast<double>(in) / p.prefill_rate : 0.0;
     p.task[o + q] = static_cast<int8_t>(task);
     double T = -kInf;  // demotion bound, as workloads_kernel (prologue.cu)
     if (saber && p.ceiling > 0.0) {

@@ -77,6 +77,9 @@ __global__ void __launch_bounds__(128) workloads_kernel(const WorkloadParams p) 
       p.sla[o + i] = sla;
       p.max_out[o + i] = static_cast<double>(out);
       p.input[o + i] = static_cast<double>(in);
+      // Engine::admit's prefill debt (engine.cpp:33-35), hoisted out of the
+      // trajectory kernel: every trajectory on this workload has this rate
+      p.prefill[o + i] = it.prefill_rate > 0.0 ? static_cast<double>(in) / it.prefill_rate : 0.0;
       p.task[o + i] = static_cast<int8_t>(task);
       p.demote_after[o + i] = demote_bound(static_cast<double>(out), dl, it.ceiling);
       max_sla = (max_sla < sla) ? sla : max_sla;
@@ -87,6 +90,7 @@ __global__ void __launch_bounds__(128) workloads_kernel(const WorkloadParams p) 
     for (int i = 0; i < it.n; ++i) {
       const double sla = p.sla[o + i];
       p.demote_after[o + i] = demote_bound(p.max_out[o + i], p.deadline[o + i], it.ceiling);
+      p.prefill[o + i] = it.prefill_rate > 0.0 ? p.input[o + i] / it.prefill_rate : 0.0;
       max_sla = (max_sla < sla) ? sla : max_sla;
       last = p.arrival[o + i];
     }

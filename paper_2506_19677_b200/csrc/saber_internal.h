@@ -35,6 +35,7 @@ struct WorkloadTables {
   const double* sla;       // [W][nmax]
   const double* max_out;   // [W][nmax]  (double: compared against fluid progress)
   const double* input;     // [W][nmax]
+  const double* prefill;   // [W][nmax] prefill debt input / prefill_rate (Engine::admit), 0 if rate <= 0
   const int8_t* task;      // [W][nmax]  catalog index or -1
   const double* demote_after;  // [W][nmax] safe lower bound on demotion time
   const double* horizon;   // [W]  last arrival + 10 * max sla (simloop.cpp:60-63)
@@ -191,6 +192,7 @@ struct WorkloadItem {
   double rps;
   double jitter;
   double ceiling;
+  double prefill_rate;  // EngineConfig::prefill_rate of every trajectory on this workload
 };
 struct WorkloadParams {
   const WorkloadItem* items;
@@ -201,6 +203,7 @@ struct WorkloadParams {
   const int8_t* mix_task;    // [mixes][4] task at each threshold slot (-1 unused)
   const int8_t* mix_last;    // [mixes] fallback task (last map entry)
   double *arrival, *deadline, *sla, *max_out, *input, *demote_after, *horizon;
+  double* prefill;
   int8_t* task;
   int32_t nmax;
 };
@@ -304,6 +307,7 @@ struct McParams {
   double tick, prefill_rate;
   int32_t model_tab, gt_tab;
   double *arrival, *deadline, *sla, *max_out, *input, *demote_after, *horizon;
+  double* prefill;
   int8_t* task;
   TrajDesc* descs;
 };

@@ -93,10 +93,15 @@ __device__ __forceinline__ uint64_t warp_max_u64(uint64_t v) {
   const unsigned mlo = __reduce_max_sync(0xFFFFFFFFu, hi == mhi ? static_cast<unsigned>(v) : 0u);
   return (static_cast<uint64_t>(mhi) << 32) | mlo;
 }
+// Sum mod 2^64 over the warp with three 32-bit REDUX.SUMs: the low word in
+// two 16-bit halves (each sum < 2^21, exact, so the carry into the high word
+// is exact) and the high word mod 2^32.
 __device__ __forceinline__ uint64_t warp_sum_u64(uint64_t v) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xFFFFFFFFu, v, o);
-  return v;
+  const unsigned lo = static_cast<unsigned>(v), hi = static_cast<unsigned>(v >> 32);
+  const unsigned s0 = __reduce_add_sync(0xFFFFFFFFu, lo & 0xFFFFu);
+  const unsigned s1 = __reduce_add_sync(0xFFFFFFFFu, lo >> 16);
+  const unsigned sh = __reduce_add_sync(0xFFFFFFFFu, hi);
+  return (static_cast<uint64_t>(sh) << 32) + (static_cast<uint64_t>(s1) << 16) + s0;
 }
 __device__ __forceinline__ unsigned lanemask_lt() {
   unsigned m;

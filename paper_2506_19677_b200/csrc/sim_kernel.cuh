@@ -320,6 +320,7 @@ __device__ __forceinline__ void gate_streak_warp(
     const int nt = min(kWarp, K - jb);
     const int nd = nt * (w - 1);
     const uint32_t* __restrict__ src = draws + draw_pos + static_cast<int64_t>(jb - 1) * (w - 1);
+#pragma unroll 1
     for (int q = sub; q < nd; q += kWarp) S.dbuf[q] = src[q];
     __syncwarp();
     uint64_t ord = 0xFEDCBA9876543210ull;
@@ -459,7 +460,6 @@ __device__ __forceinline__ void simulate_one(const SimParams& P, int ti, const S
   const double* __restrict__ MT = P.tables + (saber ? d.model_tab : d.gt_tab);
   const double horizon = isnan(d.horizon) ? P.wl.horizon[d.workload] : d.horizon;
   const double tick = d.tick;
-  const double pr = d.prefill_rate;
   const double ceiling = saber ? MT[1] : 0.0;  // max_speed = predict(model, 1)
   const uint32_t* __restrict__ draws =
       saber ? P.rng.draws + P.rng.off[d.stream] : nullptr;
@@ -513,7 +513,7 @@ __device__ __forceinline__ void simulate_one(const SimParams& P, int ti, const S
   // Engine::admit (engine.cpp:26-49): append slot A.  Every lane of the group
   // writes the same values, so the owning lane reads back its own write.
   auto admit = [&](int id, double now) {
-    const double pl = pr > 0.0 ? P.wl.input[wo + id] / pr : 0.0;
+    const double pl = P.wl.prefill[wo + id];  // input / prefill_rate (prologue)
     const double m = P.wl.max_out[wo + id];
     const int s = S.idx(A);
     if (pl == 0.0) {
