@@ -51,7 +51,7 @@ using namespace simdev;
 #define SABER_SIM_MIN_BLOCKS 4
 #endif
 #ifndef SABER_STATIC_MIN_BLOCKS
-#define SABER_STATIC_MIN_BLOCKS 5
+#define SABER_STATIC_MIN_BLOCKS 6
 #endif
 #ifndef SABER_SABER_MIN_BLOCKS
 #define SABER_SABER_MIN_BLOCKS 4
