@@ -479,6 +479,7 @@ __device__ __forceinline__ void simulate_one(const SimParams& P, int ti, const S
   }
   high.clear();
   ledger.clear();
+  int hn = 0;  // |high tier| (kept beside the mask: no popcount per query)
   // wide kernel: raw 64-bit scheduler draws (window > 16)
   const uint64_t* __restrict__ draws64 =
       kWide && saber ? reinterpret_cast<const uint64_t*>(P.rng.draws) + P.rng.off[d.stream]
@@ -556,6 +557,7 @@ __device__ __forceinline__ void simulate_one(const SimParams& P, int ti, const S
     // Arrivals due at t (simloop.cpp:79-85).
     while (na_t <= t) {
       high.set(next);
+      ++hn;
       if (saber) min_td = dmin(min_td, P.wl.demote_after[wo + next]);
       if (saber && use_tab) min_kd = min(min_kd, P.wl.dem_tick[wo + next]);
       ++next;
@@ -572,7 +574,7 @@ __device__ __forceinline__ void simulate_one(const SimParams& P, int ti, const S
     const long long sched_t0 = clock64();
 #endif
     if (saber) {
-      const int hc = high.count();
+      const int hc = hn;
       refresh_entries += hc;
       // refresh_tiers (scheduler.cpp:38-55): scan in queue (= id) order only
       // when some entry may have crossed its demotion bound.
@@ -625,6 +627,7 @@ __device__ __forceinline__ void simulate_one(const SimParams& P, int ti, const S
               }
               ndem += __popc(bal);
               high.andnot(q >> 1, static_cast<uint64_t>(bal) << ((q & 1) * 32));
+              hn -= __popc(bal);
             }
           }
           if (ndem) {
@@ -650,6 +653,7 @@ __device__ __forceinline__ void simulate_one(const SimParams& P, int ti, const S
               if (need > ceiling) {
                 demote = true;
                 high.andnot(i, 1ull << bit);
+                --hn;
                 LOW[low_tail] = static_cast<uint16_t>(id);
                 ++low_tail;
                 push_decision<kTrace>(L, t, id, SABER_DEMOTE, load, dbits(ceiling), dbits(need),
@@ -670,12 +674,12 @@ __device__ __forceinline__ void simulate_one(const SimParams& P, int ti, const S
         st_cyc[4] += clock64() - scan_t0;
 #endif
       }
-      if (kWide && high.any()) {
+      if (kWide && hn > 0) {
         // admission_step, high tier (scheduler.cpp:58-95), any window: the
         // Fisher-Yates j's lane-parallel (64-bit draws), the swaps by lane 0,
         // then 32 window positions per round with the first passing one found
         // by ballot.
-        const int hcount = high.count();
+        const int hcount = hn;
         const int w = d.window < hcount ? d.window : hcount;
         if (draw_pos + (w - 1) > draw_len) {
           failed = true;
@@ -753,12 +757,13 @@ __device__ __forceinline__ void simulate_one(const SimParams& P, int ti, const S
           __syncwarp();
           ledger_max = (ledger_max < need) ? need : ledger_max;
           high.reset(id);
+          --hn;
           L.k0 += 1;
         }
         __syncwarp();
-      } else if (!kWide && high.any()) {
+      } else if (!kWide && hn > 0) {
         // admission_step, high tier (scheduler.cpp:58-95).
-        const int hcount = high.count();
+        const int hcount = hn;
         const int w = d.window < hcount ? d.window : hcount;
         if (draw_pos + (w - 1) > draw_len) {
           failed = true;
@@ -871,6 +876,7 @@ __device__ __forceinline__ void simulate_one(const SimParams& P, int ti, const S
             LNEED[id] = need;
             ledger_max = (ledger_max < need) ? need : ledger_max;
             high.reset(id);
+            --hn;
             L.k0 += 1;
           }
         } else {
@@ -905,6 +911,7 @@ __device__ __forceinline__ void simulate_one(const SimParams& P, int ti, const S
             LNEED[id] = need;
             ledger_max = (ledger_max < need) ? need : ledger_max;
             high.reset(id);
+            --hn;
             push_decision<kTrace>(L, t, id, SABER_ADMIT_HIGH, load, dbits(pred), dbits(need), tr,
                                   P.out.trace_cap, P.out.error, leader);
           }
@@ -921,9 +928,10 @@ __device__ __forceinline__ void simulate_one(const SimParams& P, int ti, const S
       }
     } else {
       // StaticScheduler::static_step (scheduler.cpp:129-144).
-      while (A < d.cap && high.any()) {
+      while (A < d.cap && hn > 0) {
         const int id = high.lowest();
         high.reset(id);
+        --hn;
         const int before = A;
         admit(id, t);
         push_decision<kTrace>(L, t, id, SABER_ADMIT_HIGH, before, kAbsent, kAbsent, tr,
@@ -949,18 +957,18 @@ __device__ __forceinline__ void simulate_one(const SimParams& P, int ti, const S
     // high tier, load and ledger unchanged, every later tick of the streak
     // rejects the same window again (need = m / (dl - t) only grows), so its
     // decisions are generated lane-parallel (gate_streak below).
-    const bool gate_streak = saber && high.any();
+    const bool gate_streak = saber && hn > 0;
 #ifdef SABER_STREAK_STATS
     {
       const bool cond = saber ? (gate_streak ? (!kWide && G >= kMaxWindow && gate_idle) : low_head == low_tail)
-                              : !(A < d.cap && high.any());
+                              : !(A < d.cap && hn > 0);
       if (use_tab && !(!sblock && A > 0 && cond))
         st_cause[sblock ? 8 : A == 0 ? 9 : (gate_streak && !gate_idle) ? 10 : 11] += 1;
     }
 #endif
     if (use_tab && !sblock && A > 0 &&
         (saber ? (gate_streak ? (!kWide && G >= kMaxWindow && gate_idle) : low_head == low_tail)
-               : !(A < d.cap && high.any()))) {
+               : !(A < d.cap && hn > 0))) {
       const int k0 = ticks - 1;
       const double dtm = P.ticks.dt_max;
       // Kb passes keep both minima provably quiet: for pass j <= Kb - 1 the
@@ -981,7 +989,7 @@ __device__ __forceinline__ void simulate_one(const SimParams& P, int ti, const S
       // gate of the streak sees the same w candidates).  (Static streaks with
       // a full batch could absorb arrivals too, but they end at the next
       // prefill end / completion long before an arrival: measured no gain.)
-      const bool absorb = gate_streak && high.count() >= d.window;
+      const bool absorb = gate_streak && hn >= d.window;
       int K = 0;
       if (Kb >= 2) {
         K = min(Kb, kh - 1 - k0);
@@ -989,9 +997,10 @@ __device__ __forceinline__ void simulate_one(const SimParams& P, int ti, const S
         if (gate_streak) {
           // no refresh scan (t < min_td) and enough scheduler draws
           K = min(K, min_kd - k0);
-          if (gate_w > 1)
-            K = static_cast<int>(min(static_cast<int64_t>(K),
-                                     1 + (draw_len - draw_pos) / (gate_w - 1)));
+          // K - 1 further gates of gate_w - 1 draws each must fit the stream;
+          // the (64-bit) division only when they might not
+          if (gate_w > 1 && static_cast<int64_t>(K - 1) * (gate_w - 1) > draw_len - draw_pos)
+            K = static_cast<int>(1 + (draw_len - draw_pos) / (gate_w - 1));
         }
       }
 #ifdef SABER_STREAK_STATS
@@ -1004,7 +1013,7 @@ __device__ __forceinline__ void simulate_one(const SimParams& P, int ti, const S
         st_cause[base + (Kc == kbv ? 0 : Kc == kav ? 1 : Kc == kdv ? 2 : 3)] += 1;
       }
 #endif
-      const int hc_streak = gate_streak ? high.count() : 0;
+      const int hc_streak = gate_streak ? hn : 0;
       int64_t arr_extra = 0;  // high-tier entries the absorbed arrivals add to later refreshes
       if (absorb && K >= 2 && next < n && ka < k0 + K) {
         // the streak must also end before any absorbed request's demotion
@@ -1018,6 +1027,7 @@ __device__ __forceinline__ void simulate_one(const SimParams& P, int ti, const S
             const int a = P.wl.arr_tick[wo + next];
             if (a >= k0 + K) break;
             high.set(next);
+            ++hn;
             if (saber) {
               min_td = dmin(min_td, P.wl.demote_after[wo + next]);
               min_kd = min(min_kd, P.wl.dem_tick[wo + next]);
@@ -1092,7 +1102,7 @@ __device__ __forceinline__ void simulate_one(const SimParams& P, int ti, const S
 #ifndef SABER_IDLE_SKIP
 #define SABER_IDLE_SKIP 1
 #endif
-    if (SABER_IDLE_SKIP && use_tab && A == 0 && completed < n && !high.any() &&
+    if (SABER_IDLE_SKIP && use_tab && A == 0 && completed < n && hn == 0 &&
         low_head == low_tail) {
       const int k0 = ticks - 1;
       const int kj = min(ka, kh - 1);
