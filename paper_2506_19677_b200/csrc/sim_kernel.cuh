@@ -132,9 +132,34 @@ __device__ __forceinline__ double streak_chunks(const Slots<G>& S, int sub, int 
       mult[i] = g[i] < 0.0 ? 1.0 : speed;
     }
     int j = 0;
+#ifndef SABER_DT_VEC
+#define SABER_DT_VEC 1
+#endif
+    // 4-tick blocks of DT as two 16-byte loads: peel one tick first when
+    // DT + 0 is not 16-byte aligned (the per-tick update is the same either way)
+    if (SABER_DT_VEC && K >= 1 && (reinterpret_cast<uintptr_t>(DT) & 8u)) {
+      const double d0 = DT[0];
+#pragma unroll
+      for (int i = 0; i < kC; ++i) g[i] = g[i] + mult[i] * d0;  // mult == speed when kDec
+      if (!kDec && first) pf = pf - d0;
+      j = 1;
+    }
 #pragma unroll 1
     for (; j + 4 <= K; j += 4) {
-      const double d0 = DT[j], d1 = DT[j + 1], d2 = DT[j + 2], d3 = DT[j + 3];
+      double d0, d1, d2, d3;
+      if (SABER_DT_VEC) {
+        const double2 a = reinterpret_cast<const double2*>(DT + j)[0];
+        const double2 b = reinterpret_cast<const double2*>(DT + j)[1];
+        d0 = a.x;
+        d1 = a.y;
+        d2 = b.x;
+        d3 = b.y;
+      } else {
+        d0 = DT[j];
+        d1 = DT[j + 1];
+        d2 = DT[j + 2];
+        d3 = DT[j + 3];
+      }
       if (kDec) {
         const double s0 = speed * d0, s1 = speed * d1, s2 = speed * d2, s3 = speed * d3;
 #pragma unroll
