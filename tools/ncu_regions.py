@@ -15,16 +15,16 @@ import sys
 import tempfile
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-SRC = os.path.join(ROOT, "paper_2506_19677_b200", "csrc", "sim_kernel.cuh")
+SRC = os.environ.get('SABER_REGIONS_SRC', os.path.join(ROOT, 'paper_2506_19677_b200', 'csrc', 'sim_kernel.cuh'))
 MARKS = [  # (region, first line containing the marker)
     ("gate_streak_g", "__device__ __forceinline__ void gate_streak_decisions("),
     ("gate_streak", "__device__ __forceinline__ void gate_streak_warp("),
     ("ledger_max", "// max over the ledger"),
     ("prologue", "// Simulates trajectory"),
     ("arrivals", "    // Arrivals due at t"),
-    ("refresh", "      const int hc = high.count();"),
-    ("gate", "      } else if (!kWide && high.any()) {"),
-    ("gate_wide", "      if (kWide && high.any()) {"),
+    ("refresh", "      const int hc = hn;"),
+    ("gate", "      } else if (!kWide && hn > 0) {"),
+    ("gate_wide", "      if (kWide && hn > 0) {"),
     ("lowtier/static", "      } else if (low_head < low_tail) {"),
     ("streak_setup", "    if (t >= horizon) break;"),
     ("engine_quiet", "    const double nt = (horizon < t + tick)"),
