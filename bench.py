@@ -585,7 +585,7 @@ def engine_arm(args):
                             "async D2H of row stats + summary into pinned memory, 2 plans in flight",
                     "results_equal_value_run": e2e_same,
                     "one_shot": {"value": one_shot, "unit": "traj/s",
-                                 "path": "saber_cuda_sweep: host buffers in and out, nothing overlapped"}},
+                                 "path": "saber_cuda_sweep: host buffers in and out, nothing overlapped (the call reuses the previous call's device allocations; inputs are staged from the host every call)"}},
             "gpu_launches": launches_per_step * args.steps,
             "roofline": roofline_entry(issue_roofline(prof, sim_avg_ms, sm_count, clk), achieved, peak,
                                        fp64_ops, traffic, sim_avg_ms, total_ms / args.steps),

@@ -616,6 +616,32 @@ saber_status set_stream_lengths(saber_sweep_plan* P, int dev) {
   return SABER_OK;
 }
 
+namespace {
+// The one-shot saber_cuda_sweep's cached plan (see there).
+std::mutex g_oneshot_mu;
+saber_sweep_plan* g_oneshot = nullptr;
+
+bool same_model(const saber_model& a, const saber_model& b) {
+  return a.family == b.family && std::memcmp(a.params, b.params, sizeof(a.params)) == 0;
+}
+// Every descriptor field but the base seed.
+bool same_grid(const saber_sweep_desc& a, const saber_sweep_desc& b) {
+  auto same = [](const auto* x, const auto* y, int n) {
+    return n == 0 || std::memcmp(x, y, sizeof(*x) * static_cast<size_t>(n)) == 0;
+  };
+  return a.n_mixes == b.n_mixes && a.n_rps == b.n_rps && a.n_caps == b.n_caps &&
+         same(a.mixes, b.mixes, a.n_mixes) && same(a.rps, b.rps, a.n_rps) &&
+         same(a.caps, b.caps, a.n_caps) && a.with_saber == b.with_saber &&
+         a.num_requests == b.num_requests &&
+         std::memcmp(&a.length_jitter, &b.length_jitter, 8) == 0 && a.window_size == b.window_size &&
+         std::memcmp(&a.tick, &b.tick, 8) == 0 && a.has_model == b.has_model &&
+         (!a.has_model || same_model(a.model, b.model)) && same_model(a.ground_truth, b.ground_truth) &&
+         std::memcmp(&a.prefill_rate, &b.prefill_rate, 8) == 0 && a.has_horizon == b.has_horizon &&
+         (!a.has_horizon || std::memcmp(&a.horizon, &b.horizon, 8) == 0) && a.repeats == b.repeats &&
+         a.device == b.device && a.shard_index == b.shard_index && a.shard_count == b.shard_count;
+}
+}  // namespace
+
 extern "C" {
 
 int64_t saber_cuda_sweep_rows(const saber_sweep_desc* d) {
@@ -1245,6 +1271,13 @@ void saber_cuda_sweep_plan_destroy(saber_sweep_plan* P) {
 }
 
 saber_status saber_cuda_release_cache(int32_t device) {
+  {
+    std::lock_guard<std::mutex> lk1(g_oneshot_mu);
+    if (g_oneshot && g_oneshot->device == device) {
+      saber_cuda_sweep_plan_destroy(g_oneshot);
+      g_oneshot = nullptr;
+    }
+  }
   std::lock_guard<std::mutex> lk(g_pool_mu);
   auto it = g_free.find(device);
   if (it == g_free.end()) return SABER_OK;
@@ -1256,9 +1289,27 @@ saber_status saber_cuda_release_cache(int32_t device) {
 
 saber_status saber_cuda_sweep(const saber_sweep_desc* desc, saber_sweep_out* out) {
   if (!desc || !out) return fail(SABER_EINVAL, "null argument");
+  if (saber_status s = validate_sweep(*desc)) return s;
+  // One-shot calls with the same grid reuse the last call's plan (its device
+  // buffers, streams and tick table); the inputs are still staged from the
+  // host every call (reseed: host prologue + H2D), so nothing is cached but
+  // allocations.  A concurrent caller gets a private plan.
+  std::unique_lock<std::mutex> lk(g_oneshot_mu, std::try_to_lock);
   saber_sweep_plan* P = nullptr;
-  if (saber_status s = saber_cuda_sweep_plan_create(desc, &P)) return s;
-  std::unique_ptr<saber_sweep_plan, void (*)(saber_sweep_plan*)> guard(P, saber_cuda_sweep_plan_destroy);
+  std::unique_ptr<saber_sweep_plan, void (*)(saber_sweep_plan*)> guard(nullptr,
+                                                                        saber_cuda_sweep_plan_destroy);
+  if (lk.owns_lock() && g_oneshot && same_grid(g_oneshot->desc, *desc)) {
+    P = g_oneshot;
+    if (saber_status s = saber_cuda_sweep_plan_reseed(P, desc->seed, nullptr)) return s;
+  } else {
+    if (saber_status s = saber_cuda_sweep_plan_create(desc, &P)) return s;
+    if (lk.owns_lock()) {
+      if (g_oneshot) saber_cuda_sweep_plan_destroy(g_oneshot);
+      g_oneshot = P;
+    } else {
+      guard.reset(P);
+    }
+  }
   if (saber_status s = saber_cuda_sweep_plan_run(P, nullptr)) return s;
   const bool want_summary = out->summary || out->best_cap_by_rps;
   if (want_summary) {
