@@ -301,6 +301,9 @@ void seed_draws(uint64_t seed, int n, double* out4, double* neglog_sum) {
 // Upper bound on scheduler draws for a trajectory whose horizon is <= hb:
 // ticks <= hb/tick + 3 (t = min(t+tick, horizon) accumulation), and each tick
 // consumes min(window, |high|) - 1 <= min(window, n) - 1 draws.
+// First draw-stream length of a run_batch trajectory (grown x8 on exhaustion).
+constexpr int64_t kBatchDrawCap = 1 << 18;
+
 int64_t draw_bound(double hb, double tick, int window, int n) {
   const int per = std::min(window, n) - 1;
   if (per <= 0) return 0;
@@ -1452,7 +1455,8 @@ extern "C" saber_status saber_cuda_run_batch(const saber_run_batch_desc* desc,
   std::vector<TrajDesc> descs(static_cast<size_t>(T));
   std::vector<std::pair<double, double>> tick_hb;  // (tick, horizon bound) per trajectory
   std::vector<uint64_t> seeds;
-  std::vector<int64_t> off, len;
+  std::vector<int64_t> off, len, stream_full;
+  std::vector<int> stream_traj;
   int64_t total_draws = 0;
   for (int k = 0; k < T; ++k) {
     const saber_traj_spec& s = desc->specs[k];
@@ -1517,12 +1521,25 @@ extern "C" saber_status saber_cuda_run_batch(const saber_run_batch_desc* desc,
     if (s.mode == SABER_MODE_SABER) {
       d.stream = static_cast<int32_t>(seeds.size());
       seeds.push_back(s.seed ^ kSchedulerSeedSalt);
-      off.push_back(total_draws);
-      const int64_t l = draw_bound(hb, s.tick, s.window_size, n);
-      len.push_back(l);
-      total_draws += l;
+      // Streams start at min(bound, cap) draws and grow x8 (up to the
+      // provable bound) for the trajectories that exhaust them, the batch then
+      // rerunning — as the sweep plans do.  Long horizons
+      // with wide windows bound at 10^8+ draws; a few thousand are used.
+      const int64_t full = draw_bound(hb, s.tick, s.window_size, n);
+      stream_full.push_back(full);
+      stream_traj.push_back(k);
+      len.push_back(std::min<int64_t>(full, kBatchDrawCap));
     }
   }
+  auto layout_streams = [&]() {
+    off.assign(len.size(), 0);
+    total_draws = 0;
+    for (size_t q = 0; q < len.size(); ++q) {
+      off[q] = total_draws;
+      total_draws += len[q];
+    }
+  };
+  layout_streams();
 
   Workloads wl;
   DevBuf tables, seeds_d, off_d, len_d, draws_d, descs_d, rows_d, comp_d, admit_d, demo_d, cursor_d,
@@ -1624,6 +1641,10 @@ extern "C" saber_status saber_cuda_run_batch(const saber_run_batch_desc* desc,
   cudaStream_t st = nullptr;
   SyncOnExit sync_guard(&st);
   int launches = 0;
+  int32_t err = 0;
+  float ms = 0.f;
+  for (;;) {  // reruns only after a draw stream grew
+  launches = 0;
   CUDA_TRY(cudaEventRecord(tm.a, st));
   CUDA_TRY(cudaMemsetAsync(rows_d.p, 0, rows_d.bytes, st));
   CUDA_TRY(cudaMemsetAsync(cursor_d.p, 0, 16, st));
@@ -1738,10 +1759,27 @@ extern "C" saber_status saber_cuda_run_batch(const saber_run_batch_desc* desc,
   }
   CUDA_TRY(cudaEventRecord(tm.b, st));
   CUDA_TRY(cudaEventSynchronize(tm.b));
-  float ms = 0.f;
   CUDA_TRY(cudaEventElapsedTime(&ms, tm.a, tm.b));
-  int32_t err = 0;
   CUDA_TRY(cudaMemcpy(&err, err_d.p, 4, cudaMemcpyDeviceToHost));
+  if (err != kErrRngExhausted) break;
+  // grow the streams the failed trajectories ran out of, then rerun
+  std::vector<saber_traj_row> rr(static_cast<size_t>(T));
+  CUDA_TRY(cudaMemcpy(rr.data(), rows_d.p, rr.size() * sizeof(saber_traj_row), cudaMemcpyDeviceToHost));
+  bool grew = false;
+  for (size_t q = 0; q < len.size(); ++q) {
+    const int k = stream_traj[q];
+    const int64_t need_more = static_cast<int64_t>(desc->specs[k].window_size) - 1;
+    if (rr[static_cast<size_t>(k)].rng_draws + need_more > len[q] && len[q] < stream_full[q]) {
+      len[q] = std::min<int64_t>(stream_full[q], len[q] * 8);
+      grew = true;
+    }
+  }
+  if (!grew) break;  // a genuine bound violation: reported below
+  layout_streams();
+  ALLOC_TRY(draws_d, dev, static_cast<size_t>(std::max<int64_t>(1, total_draws)) * (wide ? 8 : 4));
+  CUDA_TRY(cudaMemcpy(off_d.p, off.data(), off.size() * 8, cudaMemcpyHostToDevice));
+  CUDA_TRY(cudaMemcpy(len_d.p, len.data(), len.size() * 8, cudaMemcpyHostToDevice));
+  }
 
   CUDA_TRY(cudaMemcpy(out->rows, rows_d.p, static_cast<size_t>(T) * sizeof(saber_traj_row),
                       cudaMemcpyDeviceToHost));

@@ -87,7 +87,8 @@ def compare_row(row, o, counters=True):
     return errs
 
 
-def random_configs(count, seed=1234, n_choices=(1, 7, 50, 100, 130), allow_logistic=True):
+def random_configs(count, seed=1234, n_choices=(1, 7, 50, 100, 130), allow_logistic=True,
+                   windows=(1, 2, 3, 8, 8, 16)):
     rng = random.Random(seed)
     out = []
     models = [CAL_USL, CAL_LIN] + ([CAL_LOG, (1, (90.0, 0.06, 35.0))] if allow_logistic else []) + \
@@ -97,7 +98,7 @@ def random_configs(count, seed=1234, n_choices=(1, 7, 50, 100, 130), allow_logis
         out.append(sim_config(
             mix=rng.choice(["w1", "w2", "w3"]), rps=rng.choice([0.5, 1, 2, 4, 8, 15, 20, 35]),
             n=rng.choice(n_choices), seed=rng.randrange(1 << 40), mode=mode,
-            cap=rng.choice([1, 3, 10, 40, 100]), window=rng.choice([1, 2, 3, 8, 8, 16]),
+            cap=rng.choice([1, 3, 10, 40, 100]), window=rng.choice(windows),
             tick=rng.choice([0.01, 0.01, 0.05, 0.003]), model=rng.choice(models),
             gt=rng.choice([GT, (0, (80.0, 0.12, 0.002)), (1, (120.0, 0.1, 30.0))]),
             prefill_rate=rng.choice([2000.0, 2000.0, 0.0, 500.0]), jitter=rng.choice([0.2, 0.0, 0.5])))

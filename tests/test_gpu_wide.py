@@ -111,3 +111,14 @@ def test_wide_latency_percentiles(engine, orc):
             j = next(i for i in range(n) if (i + 1) / n >= p)
             want = lat[j] if lat[j] != float("inf") else float("nan")
             assert same_float(float(res.rows[k]["latency_q"][t]), want)
+
+
+def test_long_wide_trajectory_grows_its_draw_stream(engine, ref):
+    """n = 2500 at 0.5 rps with a 64-wide window: the provable draw bound is
+    ~10^8 draws; run_batch starts each stream at 2^18 and grows it x8 when a
+    trajectory exhausts it (the batch reruns), ending bit-exact."""
+    cfg = sim_config("w2", 0.5, 2500, 11, window=64)
+    res = engine.run_batch([cfg])
+    assert int(res.rows[0]["rng_draws"]) > 1 << 18
+    assert compare_row(res.rows[0], ref.run(orc_config(cfg)).out, counters=False) == []
+

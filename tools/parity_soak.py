@@ -27,10 +27,14 @@ def main():
     ap.add_argument("--ref-sample", type=int, default=400)
     ap.add_argument("--seed", type=int, default=1)
     ap.add_argument("--batch", type=int, default=500)
+    ap.add_argument("--n-choices", default="1,7,50,100,130")
+    ap.add_argument("--windows", default="1,2,3,8,8,16")
     a = ap.parse_args()
     orc = O.Oracle("restatement")
     ref = O.Oracle("reference") if O.reference_available() else None
-    cfgs = random_configs(a.configs, seed=a.seed)
+    nch = tuple(int(x) for x in a.n_choices.split(","))
+    wins = tuple(int(x) for x in a.windows.split(","))
+    cfgs = random_configs(a.configs, seed=a.seed, n_choices=nch, windows=wins)
     bad, decisions, checked_ref, t0 = [], 0, 0, time.time()
     for b0 in range(0, len(cfgs), a.batch):
         chunk = cfgs[b0:b0 + a.batch]
@@ -52,8 +56,8 @@ def main():
     print(json.dumps({"trajectories": len(cfgs), "mismatches": len(bad), "first_mismatches": bad[:10],
                       "decisions_compared": decisions, "vs_compiled_reference": checked_ref,
                       "generator": f"tests/helpers.py random_configs(seed={a.seed}): mixes w1-w3, rps 0.5-35, "
-                                   "n in {1,7,50,100,130}, saber/static, caps 1-100, windows 1-16, ticks "
-                                   "0.003-0.05, prefill 0/500/2000, jitter 0-0.5, usl/linear/logistic models",
+                                   f"n in {{{a.n_choices}}}, saber/static, caps 1-100, windows {{{a.windows}}}, "
+                                   "ticks 0.003-0.05, prefill 0/500/2000, jitter 0-0.5, usl/linear/logistic models",
                       "seconds": round(time.time() - t0, 1)}))
 
 
