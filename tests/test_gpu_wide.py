@@ -114,10 +114,10 @@ def test_wide_latency_percentiles(engine, orc):
 
 
 def test_long_wide_trajectory_grows_its_draw_stream(engine, ref):
-    """n = 2500 at 0.5 rps with a 64-wide window: the provable draw bound is
+    """n = 2500 at 20 rps, 3 ms ticks, a 64-wide window: the provable draw bound is
     ~10^8 draws; run_batch starts each stream at 2^18 and grows it x8 when a
     trajectory exhausts it (the batch reruns), ending bit-exact."""
-    cfg = sim_config("w2", 0.5, 2500, 11, window=64)
+    cfg = sim_config("w2", 20.0, 2500, 11, window=64, tick=0.003)
     res = engine.run_batch([cfg])
     assert int(res.rows[0]["rng_draws"]) > 1 << 18
     assert compare_row(res.rows[0], ref.run(orc_config(cfg)).out, counters=False) == []
