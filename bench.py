@@ -607,7 +607,7 @@ def engine_arm(args):
     return 0
 
 
-def _one_shot(S, grid, base, device):
+def _one_shot(S, grid, base, device, results=False):
     """One saber_cuda_sweep call: host buffers in and out (what the drop-in
     saber::cuda::sweep issues, include/saber_cuda_adapter.hpp)."""
     import ctypes as C
@@ -646,6 +646,11 @@ def _one_shot(S, grid, base, device):
     o.best_cap_by_rps = best.ctypes.data_as(C.POINTER(C.c_int32))
     S.api._check(N.lib().saber_cuda_sweep(C.byref(d), C.byref(o)))
     del p
+    if results:
+        raw = np.ctypeslib.as_array(C.cast(stats, C.POINTER(C.c_double)), shape=(n_rows * 4,)).copy()
+        sm = [[x.saber_mean_goodput, x.best_static_mean_goodput, x.delta, x.saber_pooled_cv,
+               x.best_static_pooled_cv, x.saber_rps_mean_cv, x.best_static_rps_mean_cv] for x in summ]
+        return raw, np.array(sm), best.copy()
     return int(o.h2d_bytes), int(o.d2h_bytes)
 
 

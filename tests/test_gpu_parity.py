@@ -276,3 +276,31 @@ def test_large_trajectories_match_restatement(engine, orc, n):
         if errs:
             bad.append((k, errs[:4]))
     assert bad == []
+
+
+def test_one_shot_sweep_plan_reuse_is_exact(engine):
+    """saber_cuda_sweep reuses the previous call's plan for the same grid (new
+    inputs staged every call): seeds A, B, A give A's results twice and B's
+    equal to a freshly created plan's."""
+    import bench
+    import paper_2506_19677_b200 as S
+    grid = S.SweepGrid(["w1", "w3"], [2.0, 12.0], [20, 60], True)
+    base = sim_config("w2", 1.0, 80, 42)
+    base.repeats = 4
+    a1 = bench._one_shot(S, grid, base, 0, results=True)
+    base.seed = 977
+    b = bench._one_shot(S, grid, base, 0, results=True)
+    base.seed = 42
+    a2 = bench._one_shot(S, grid, base, 0, results=True)
+    for x, y in zip(a1, a2):
+        assert np.array_equal(np.asarray(x).view(np.uint8), np.asarray(y).view(np.uint8))
+    base.seed = 977
+    plan = S.SweepPlan(grid, base)
+    plan.run()
+    plan.summarize()
+    rows, _, summ, best = plan.fetch()
+    plan.close()
+    st = b[0].reshape(-1, 4)
+    for k, f in enumerate(("goodput", "ratio_mean", "ratio_std", "cv")):
+        assert np.array_equal(st[:, k], rows[f].astype(np.float64), equal_nan=True), f
+    assert np.array_equal(b[2], np.asarray(best))
