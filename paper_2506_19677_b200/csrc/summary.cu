@@ -18,12 +18,18 @@
 #include <cmath>
 #include <cstdlib>
 
+#include "exact_sum.cuh"
 #include "saber_internal.h"
 
 namespace saberb200 {
 namespace {
 
+using exactsum::block_exact_seq_sum;
+using exactsum::kExactK;
+using exactsum::kExactThreads;
+
 constexpr int kCellScratch = 6;
+constexpr int kMaxSegments = 512;  // rps values of one pool the exact-sum kernel indexes
 constexpr unsigned kFull = 0xFFFFFFFFu;
 
 __global__ void __launch_bounds__(256) ratios_kernel(const SummaryParams p) {
@@ -479,6 +485,216 @@ __global__ void __launch_bounds__(32) summary_mix_warp_kernel(const SummaryParam
   }
 }
 
+// Exact parallel sum and count of one contiguous block of ratios (NaN =
+// never completed: not in the pool, an exact +0 in the sum).
+__device__ void block_ratio_sum(const double* v, int64_t len, double& sum, int64_t& cnt) {
+  __shared__ unsigned long long c_sh;
+  if (threadIdx.x == 0) c_sh = 0;
+  __syncthreads();
+  int64_t c = 0;
+  for (int64_t i = threadIdx.x; i < len; i += blockDim.x) c += !isnan(v[i]);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(kFull, c, o);
+  if ((threadIdx.x & 31) == 0) atomicAdd(&c_sh, static_cast<unsigned long long>(c));
+  __syncthreads();
+  cnt = static_cast<int64_t>(c_sh);
+  sum = block_exact_seq_sum(
+      len,
+      [&](int64_t b, double (&t)[kExactK]) {
+#pragma unroll
+        for (int j = 0; j < kExactK; ++j) {
+          const double x = b + j < len ? v[b + j] : 0.0;
+          t[j] = isnan(x) ? 0.0 : x;
+        }
+      },
+      [&](int64_t i) {
+        const double x = v[i];
+        return isnan(x) ? 0.0 : x;
+      });
+  __syncthreads();  // c_sh is reused by the next call
+}
+
+// S1 with the exact parallel sums: one block per (mix, rps) cell.
+__global__ void __launch_bounds__(kExactThreads) summary_cells_exact_kernel(const SummaryParams p) {
+  const int cell = blockIdx.x;
+  const int R = p.repeats;
+  const int per_rps = p.n_caps * R + (p.with_saber ? R : 0);
+  const int64_t base = static_cast<int64_t>(cell) * per_rps;
+  const int64_t len = static_cast<int64_t>(R) * p.n;
+  __shared__ int best_cap_sh;
+  __shared__ double best_mean_sh;
+  double out[kCellScratch];
+  const double nanv = nan("");
+  out[0] = out[1] = out[2] = out[3] = nanv;
+  out[4] = out[5] = 0.0;
+  if (p.n_caps > 0) {
+    if (threadIdx.x == 0) {  // unique caps ascending (std::map order), ties to the smaller
+      double best_mean = -1.0;
+      int best_cap = 0;
+      long long prev = LLONG_MIN;
+      for (;;) {
+        long long cap = LLONG_MAX;
+        for (int w = 0; w < p.n_caps; ++w)
+          if (p.caps[w] > prev && p.caps[w] < cap) cap = p.caps[w];
+        if (cap == LLONG_MAX) break;
+        prev = cap;
+        double sm = 0.0;
+        int64_t c = 0;
+        for (int w = 0; w < p.n_caps; ++w) {
+          if (p.caps[w] != cap) continue;
+          for (int i = 0; i < R; ++i) {
+            sm += p.rows[base + static_cast<int64_t>(w) * R + i].goodput;
+            ++c;
+          }
+        }
+        const double m = sm / static_cast<double>(c);
+        if (m > best_mean) {
+          best_mean = m;
+          best_cap = static_cast<int>(cap);
+        }
+      }
+      best_cap_sh = best_cap;
+      best_mean_sh = best_mean;
+    }
+    __syncthreads();
+    const int best_cap = best_cap_sh;
+    out[1] = best_mean_sh;
+    int wb = 0;
+    while (p.caps[wb] != best_cap) ++wb;  // caps are unique (validate_sweep)
+    double sm;
+    int64_t c;
+    block_ratio_sum(p.ratios + (base + static_cast<int64_t>(wb) * R) * p.n, len, sm, c);
+    if (c > 0) {
+      out[3] = sm / static_cast<double>(c);
+      out[5] = 1.0;
+    }
+    if (threadIdx.x == 0) p.best_cap[cell] = best_cap;
+  } else if (threadIdx.x == 0) {
+    p.best_cap[cell] = 0;
+  }
+  if (p.with_saber) {
+    const int64_t sb = base + static_cast<int64_t>(p.n_caps) * R;
+    double g = 0.0;
+    for (int i = 0; i < R; ++i) g += p.rows[sb + i].goodput;
+    out[0] = g / static_cast<double>(R);
+    double sm;
+    int64_t c;
+    block_ratio_sum(p.ratios + sb * p.n, len, sm, c);
+    if (c > 0) {
+      out[2] = sm / static_cast<double>(c);
+      out[4] = 1.0;
+    }
+  }
+  if (threadIdx.x == 0)
+    for (int k = 0; k < kCellScratch; ++k) p.scratch[static_cast<int64_t>(cell) * kCellScratch + k] = out[k];
+}
+
+// Pooled CV terms of one (mix, variant) with the exact parallel sums: one block.
+__global__ void __launch_bounds__(kExactThreads) summary_mix_exact_kernel(const SummaryParams p) {
+  __shared__ const double* seg[kMaxSegments];
+  const int mi = blockIdx.x >> 1;
+  const int variant = blockIdx.x & 1;  // 0 = saber, 1 = best static
+  const int lane = threadIdx.x & 31;
+  const double* sc = p.scratch + static_cast<int64_t>(mi) * p.n_rps * kCellScratch;
+  const bool present = variant == 0 ? p.with_saber != 0 : p.n_caps > 0;
+  const double nanv = nan("");
+  double mean_goodput = nanv, pooled = nanv, rps_cv = nanv;
+  if (present) {
+    // the pool: segments of R x n ratios (rps in grid order, the chosen cell)
+    __shared__ int nseg_sh;
+    if (threadIdx.x == 0) {
+      int k = 0;
+      SegmentWalk walk;
+      const double* sp;
+      int64_t slen;
+      while (walk.next(p, mi, variant, &sp, &slen) && k < kMaxSegments) seg[k++] = sp;
+      nseg_sh = k;
+    }
+    __syncthreads();
+    const int nseg = nseg_sh;
+    const int64_t L = static_cast<int64_t>(p.repeats) * p.n;
+    const int64_t total = static_cast<int64_t>(nseg) * L;
+    const double invL = 1.0 / static_cast<double>(L);
+    // segment and offset of pooled index i without a 64-bit division
+    auto locate = [&](int64_t i, int64_t& sg, int64_t& off) {
+      sg = static_cast<int64_t>(static_cast<double>(i) * invL);
+      off = i - sg * L;
+      while (off < 0) { --sg; off += L; }
+      while (off >= L) { ++sg; off -= L; }
+    };
+    auto at = [&](int64_t i) {
+      int64_t sg, off;
+      locate(i, sg, off);
+      return seg[sg][off];
+    };
+    // K consecutive pooled values from b (NaN beyond the pool)
+    auto load_run = [&](int64_t b, double (&t)[kExactK]) {
+      int64_t sg, off;
+      locate(b, sg, off);
+#pragma unroll
+      for (int j = 0; j < kExactK; ++j) {
+        t[j] = b + j < total ? seg[sg][off] : nan("");
+        if (++off == L) { ++sg; off = 0; }
+      }
+    };
+    __shared__ unsigned long long cnt_sh;
+    if (threadIdx.x == 0) cnt_sh = 0;
+    __syncthreads();
+    int64_t cnt = 0;
+    for (int k = 0; k < nseg; ++k)
+      for (int64_t o = threadIdx.x; o < L; o += kExactThreads) cnt += !isnan(seg[k][o]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(kFull, cnt, o);
+    if (lane == 0) atomicAdd(&cnt_sh, static_cast<unsigned long long>(cnt));
+    __syncthreads();
+    cnt = static_cast<int64_t>(cnt_sh);
+    const double sum = block_exact_seq_sum(
+        total,
+        [&](int64_t b, double (&t)[kExactK]) {
+          load_run(b, t);
+#pragma unroll
+          for (int j = 0; j < kExactK; ++j) t[j] = isnan(t[j]) ? 0.0 : t[j];
+        },
+        [&](int64_t i) {
+          const double v = at(i);
+          return isnan(v) ? 0.0 : v;
+        });
+    if (cnt > 0) {
+      const double mean = sum / static_cast<double>(cnt);
+      if (mean != 0.0) {
+        const double acc = block_exact_seq_sum(
+            total,
+            [&](int64_t b, double (&t)[kExactK]) {
+              load_run(b, t);
+#pragma unroll
+              for (int j = 0; j < kExactK; ++j)
+                t[j] = isnan(t[j]) ? 0.0 : (t[j] - mean) * (t[j] - mean);
+            },
+            [&](int64_t i) {
+              const double v = at(i);
+              return isnan(v) ? 0.0 : (v - mean) * (v - mean);
+            });
+        pooled = sqrt(acc / static_cast<double>(cnt)) / mean;
+      }
+    }
+    double s = 0.0;
+    for (int ri = 0; ri < p.n_rps; ++ri) s += sc[ri * kCellScratch + (variant == 0 ? 0 : 1)];
+    mean_goodput = s / static_cast<double>(p.n_rps);
+    rps_cv = cv_cells(sc, p.n_rps, variant == 0 ? 2 : 3, variant == 0 ? 4 : 5);
+  }
+  if (threadIdx.x != 0) return;
+  saber_mix_summary* out = p.summary + mi;
+  if (variant == 0) {
+    out->saber_mean_goodput = mean_goodput;
+    out->saber_pooled_cv = pooled;
+    out->saber_rps_mean_cv = rps_cv;
+  } else {
+    out->best_static_mean_goodput = mean_goodput;
+    out->best_static_pooled_cv = pooled;
+    out->best_static_rps_mean_cv = rps_cv;
+  }
+}
+
 // delta = saber - best static (simloop.cpp:262), after both variants wrote.
 __global__ void summary_delta_kernel(const SummaryParams p) {
   const int mi = blockIdx.x * blockDim.x + threadIdx.x;
@@ -497,17 +713,24 @@ int launch_summary(const SummaryParams& p, void* stream) {
   // kernels (bench.py pipelining) — small blocks that fit in the register
   // file those kernels leave free (the static kernel leaves 4,096 registers
   // per SM: one warp of the cells kernel or two of the ratios kernel fit)
+  const bool chain = std::getenv("SABER_SUMMARY_CHAIN") != nullptr;
   if (p.narrow) {
     ratios_kernel<<<148, 64, 0, s>>>(p);
-    summary_cells_kernel<<<cells, 32, 0, s>>>(p);
   } else {
     ratios_kernel<<<1184, 256, 0, s>>>(p);
-    summary_cells_kernel<<<(cells * 32 + 127) / 128, 128, 0, s>>>(p);
   }
+  if (chain && p.narrow)
+    summary_cells_kernel<<<cells, 32, 0, s>>>(p);
+  else if (chain)
+    summary_cells_kernel<<<(cells * 32 + 127) / 128, 128, 0, s>>>(p);
+  else
+    summary_cells_exact_kernel<<<cells, kExactThreads, 0, s>>>(p);
   if (std::getenv("SABER_SUMMARY_RING"))
     summary_mix_kernel<<<2 * p.n_mixes, 64, 0, s>>>(p);
-  else
+  else if (std::getenv("SABER_SUMMARY_CHAIN") || p.n_rps > kMaxSegments)
     summary_mix_warp_kernel<<<2 * p.n_mixes, 32, 0, s>>>(p);
+  else
+    summary_mix_exact_kernel<<<2 * p.n_mixes, kExactThreads, 0, s>>>(p);
   summary_delta_kernel<<<1, 32, 0, s>>>(p);
   return cudaGetLastError() == cudaSuccess ? 0 : 1;
 }
