@@ -6,6 +6,7 @@
 #include <cuda_runtime.h>
 
 #include <climits>
+#include <cstdio>
 #include <cmath>
 #include <cstdint>
 
@@ -36,14 +37,21 @@ constexpr unsigned kFull = 0xFFFFFFFFu;
 #define SABER_EXACT_T 512
 #endif
 constexpr int kExactK = SABER_EXACT_K;  // terms per thread per tile
-constexpr int kExactThreads = SABER_EXACT_T;  // a tile = 2,048 terms (4 x 512 measured best)
+constexpr int kExactThreads = SABER_EXACT_T;
+constexpr int kTieCap = 512;  // ties a tile resolves in place (more: term by term)  // a tile = 2,048 terms (4 x 512 measured best)
 
 // `run(b, t)` fills t[0..kExactK) with the terms b, b+1, ... (t_i >= +0,
 // +0 beyond n); `term(i)` returns one term.  Called by the whole block;
 // every thread returns the sum.
+// block_exact_seq_sum_range: the same from a running sum s0 over terms
+// [lo, n) (s0 = +0, lo = 0: the whole chain).
 template <class Run, class Term>
-__device__ double block_exact_seq_sum(int64_t n, Run&& run_terms, Term&& term) {
+__device__ double block_exact_seq_sum_range(double s0, int64_t lo, int64_t n, Run&& run_terms,
+                                            Term&& term) {
   __shared__ int64_t wtot[kExactThreads / 32];
+  __shared__ int wtie[kExactThreads / 32];
+  __shared__ int64_t tie_T[kTieCap], tie_q[kTieCap];
+  __shared__ int64_t extra_sh;
   __shared__ int cand_min;
   __shared__ int64_t cand_S;
   __shared__ double s_sh;
@@ -51,21 +59,23 @@ __device__ double block_exact_seq_sum(int64_t n, Run&& run_terms, Term&& term) {
   constexpr int kWarps = kExactThreads / 32;
   constexpr int kTile = kExactThreads * kExactK;
   constexpr int64_t kTop = 1ll << 53;
-  double s = 0.0;
-  int64_t pos = 0;
-  // bootstrap: the first terms sequentially (s is small next to them) on
-  // warp 0, 32 coalesced loads at a time feeding the add chain by shuffles
-  const int64_t boot = n < 512 ? n : 512;
-  if (warp == 0) {
-    for (int64_t b0 = 0; b0 < boot; b0 += 32) {
-      const double t = b0 + lane < boot ? term(b0 + lane) : 0.0;
-      for (int j = 0; j < 32; ++j) s += __shfl_sync(kFull, t, j);  // +0 past boot: exact
+  double s = s0;
+  int64_t pos = lo;
+  if (!(s0 > 0.0)) {
+    // bootstrap: the first terms sequentially (s is small next to them) on
+    // warp 0, 32 coalesced loads at a time feeding the add chain by shuffles
+    const int64_t boot = n - lo < 512 ? n : lo + 512;
+    if (warp == 0) {
+      for (int64_t b0 = lo; b0 < boot; b0 += 32) {
+        const double t = b0 + lane < boot ? term(b0 + lane) : 0.0;
+        for (int j = 0; j < 32; ++j) s += __shfl_sync(kFull, t, j);  // +0 past boot: exact
+      }
+      if (lane == 0) s_sh = s;
     }
-    if (lane == 0) s_sh = s;
+    __syncthreads();
+    s = s_sh;
+    pos = boot;
   }
-  __syncthreads();
-  s = s_sh;
-  pos = boot;
   while (pos < n) {
     if (!(s > 0.0)) {  // all terms so far were +0: one more sequential stretch
       __syncthreads();
@@ -89,6 +99,7 @@ __device__ double block_exact_seq_sum(int64_t n, Run&& run_terms, Term&& term) {
     int64_t q[kExactK];
     int fc[kExactK];  // the fraction of t/u: 0 below 1/2, 1 exactly 1/2 (a tie), 2 above
     int64_t tot = 0;
+    int nties = 0;
     {
       double tv[kExactK];
       run_terms(b, tv);
@@ -100,26 +111,74 @@ __device__ double block_exact_seq_sum(int64_t n, Run&& run_terms, Term&& term) {
         q[j] = fl < 9.0e15 ? static_cast<int64_t>(fl) : kTop;  // >= 2^53 leaves the binade anyway
         fc[j] = fr > 0.5 ? 2 : (fr == 0.5 ? 1 : 0);
         tot += q[j] + (fc[j] == 2 ? 1 : 0);
+        nties += fc[j] == 1;
       }
     }
-    // block exclusive scan of the threads' increments
+    // block exclusive scans of the threads' increments and tie counts
     int64_t inc = tot;
+    int tinc = nties;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
       const int64_t y = __shfl_up_sync(kFull, inc, o);
-      if (lane >= o) inc += y;
+      const int z = __shfl_up_sync(kFull, tinc, o);
+      if (lane >= o) {
+        inc += y;
+        tinc += z;
+      }
     }
-    if (lane == 31) wtot[warp] = inc;
+    if (lane == 31) {
+      wtot[warp] = inc;
+      wtie[warp] = tinc;
+    }
     if (tid == 0) cand_min = INT_MAX;
     __syncthreads();
     int64_t wbase = 0, all = 0;
+    int tbase = 0, tall = 0;
 #pragma unroll
     for (int w = 0; w < kWarps; ++w) {
       const int64_t x = wtot[w];
-      if (w < warp) wbase += x;
+      const int z = wtie[w];
+      if (w < warp) {
+        wbase += x;
+        tbase += z;
+      }
       all += x;
+      tall += z;
     }
     const int64_t excl = wbase + inc - tot;
+    // Ties resolved in order without leaving the tile: a tie at running
+    // integer T (everything before it, earlier ties included) adds q or q + 1
+    // so that T + result is even (round half to even); only the parity of
+    // the earlier ties' choices matters, so thread 0 walks the tie list.
+    // Valid when the whole tile provably stays in the binade: every partial
+    // sum is at most S + all + (number of ties) + 1/2.
+    if (S + all + tall < kTop - 1 && tall <= kTieCap) {
+      if (tall > 0) {
+        int k = tbase + tinc - nties;
+        int64_t run = S + excl;
+#pragma unroll
+        for (int j = 0; j < kExactK; ++j) {
+          if (fc[j] == 1) {
+            tie_T[k] = run;
+            tie_q[k] = q[j];
+            ++k;
+          }
+          run += q[j] + (fc[j] == 2 ? 1 : 0);
+        }
+        __syncthreads();
+        if (tid == 0) {
+          int64_t extra = 0;
+          for (int t = 0; t < tall; ++t) extra += (tie_T[t] + extra + tie_q[t]) & 1;
+          extra_sh = extra;
+        }
+        __syncthreads();
+        all += extra_sh;
+      }
+      s = static_cast<double>(S + all) * u;  // exact: < 2^53 on the grid
+      pos = pos + kTile < n ? pos + kTile : n;
+      __syncthreads();  // wtot / wtie / tie lists are rewritten next tile
+      continue;
+    }
     // this thread's first term that is a tie or leaves the binade
     int cj = kExactK;
     int64_t run = S + excl;
@@ -139,6 +198,13 @@ __device__ double block_exact_seq_sum(int64_t n, Run&& run_terms, Term&& term) {
       __syncthreads();  // wtot / cand_min are rewritten next tile
       continue;
     }
+#ifdef SABER_EXACT_DEBUG
+    if (tid == 0) {
+      const double tcd = term(pos + c);
+      const double vv = tcd * iu;
+      printf("cand pos %lld c %d e %d t %.17g v %.17g frac %.17g\n", (long long)pos, c, e, tcd, vv, vv - floor(vv));
+    }
+#endif
     if (tid * kExactK + cj == c) cand_S = run;  // S before the candidate term
     __syncthreads();
     if (tid == 0) s_sh = static_cast<double>(cand_S) * u + term(pos + c);  // one DADD
@@ -147,6 +213,11 @@ __device__ double block_exact_seq_sum(int64_t n, Run&& run_terms, Term&& term) {
     pos += c + 1;
   }
   return s;
+}
+
+template <class Run, class Term>
+__device__ double block_exact_seq_sum(int64_t n, Run&& run_terms, Term&& term) {
+  return block_exact_seq_sum_range(0.0, 0, n, run_terms, term);
 }
 
 }  // namespace exactsum

@@ -496,7 +496,7 @@ struct saber_sweep_plan {
 
   Workloads wl;
   DevBuf tables, seeds, s_off, s_len, draws, descs, rows, comp, cursor, err, caps_d;
-  DevBuf summary, best_cap, cell_scratch, ratios, order, stats;
+  DevBuf summary, best_cap, cell_scratch, ratios, order, stats, pool_scratch;
   Scratch scratch;
   TickTableBuf ticktab;
   int32_t n_saber_first = 0;  // SABER rows lead the order: split launch
@@ -766,6 +766,7 @@ saber_status saber_cuda_sweep_plan_create(const saber_sweep_desc* desc, saber_sw
   ALLOC_TRY(P->summary, dev, static_cast<size_t>(n_mixes) * sizeof(saber_mix_summary));
   ALLOC_TRY(P->best_cap, dev, static_cast<size_t>(n_mixes) * n_rps * 4);
   ALLOC_TRY(P->cell_scratch, dev, static_cast<size_t>(n_mixes) * n_rps * 6 * 8);
+  ALLOC_TRY(P->pool_scratch, dev, summary_pool_scratch_bytes(n_mixes, n_rps, R, n));
   ALLOC_TRY(P->ratios, dev, static_cast<size_t>(P->n_rows) * n * 8);
   ALLOC_TRY(P->stats, dev, static_cast<size_t>(std::max<int64_t>(1, P->n_rows)) * sizeof(saber_row_stats));
   if (desc->with_saber) {
@@ -1102,6 +1103,7 @@ static saber_status summarize_launch_impl(saber_sweep_plan* P, void* stream, boo
   sp.summary = P->summary.as<saber_mix_summary>();
   sp.best_cap = P->best_cap.as<int32_t>();
   sp.scratch = P->cell_scratch.as<double>();
+  sp.pool_scratch = P->pool_scratch.p;
   sp.ratios = P->ratios.as<double>();
   sp.narrow = narrow ? 1 : 0;
   CUDA_TRY(cudaEventRecord(P->summ.a, s));

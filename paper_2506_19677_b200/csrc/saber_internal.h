@@ -279,7 +279,10 @@ struct SummaryParams {
   double* scratch;              // [n_mixes][n_rps][6] cell-level means/flags
   double* ratios;               // [n_rows][n] latency/SLA ratios (NaN = never completed)
   int32_t narrow;               // 1 = few small blocks (runs beside the trajectory kernels)
+  void* pool_scratch;           // summary_pool_scratch_bytes() bytes (the chunked pooled sums)
 };
+// Device scratch the chunked pooled sums of a summary need (summary.cu).
+size_t summary_pool_scratch_bytes(int n_mixes, int n_rps, int repeats, int n);
 int launch_summary(const SummaryParams& p, void* stream);
 // The four SweepRow statistics of every row, packed (sweep fetch).
 int launch_pack_row_stats(const saber_traj_row* rows, int64_t n_rows, saber_row_stats* out,

@@ -695,6 +695,294 @@ __global__ void __launch_bounds__(kExactThreads) summary_mix_exact_kernel(const 
   }
 }
 
+// ---------------------------------------------------------------------------
+// The pooled sums over the whole GPU.  One block per (chain, 2,048-term
+// chunk) speculates the chunk's binade from approximate prefix sums and
+// reduces the chunk to its integer increment R (ties resolved for both
+// parities of the starting integer); one block per chain then walks the
+// chunks in order, adding R exactly when the true running sum is in the
+// predicted binade and the chunk provably stays in it, and re-running the
+// chunk with block_exact_seq_sum_range otherwise (binade crossings, a tie
+// list over the cap, a mispredicted binade).  Same bits as the chain.
+using exactsum::kTieCap;
+constexpr int kPoolChunk = kExactThreads * kExactK;
+
+struct ChunkSpec {
+  double approx;        // any-order sum of the chunk's terms (speculation only)
+  int64_t R;            // integer increment on the predicted grid, ties at q
+  int64_t cnt;          // completed ratios in the chunk (pass 0)
+  int32_t extra0, extra1;  // ties' rounding for an even / odd starting integer
+  int32_t e, valid;     // predicted binade exponent; 0 = walk re-runs the chunk
+};
+
+struct PoolChain {
+  const double* seg[kMaxSegments];
+  int nseg;
+  int64_t L, total;
+  double invL;
+};
+
+__device__ __forceinline__ void pool_build(const SummaryParams& p, int chain, PoolChain& pc) {
+  if (threadIdx.x == 0) {
+    const int mi = chain >> 1, variant = chain & 1;
+    const bool present = variant == 0 ? p.with_saber != 0 : p.n_caps > 0;
+    int k = 0;
+    if (present) {
+      SegmentWalk walk;
+      const double* sp;
+      int64_t slen;
+      while (walk.next(p, mi, variant, &sp, &slen) && k < kMaxSegments) pc.seg[k++] = sp;
+    }
+    pc.nseg = k;
+    pc.L = static_cast<int64_t>(p.repeats) * p.n;
+    pc.total = static_cast<int64_t>(k) * pc.L;
+    pc.invL = 1.0 / static_cast<double>(pc.L);
+  }
+  __syncthreads();
+}
+
+// pooled value i (NaN = never completed), i < total
+__device__ __forceinline__ double pool_at(const PoolChain& pc, int64_t i) {
+  int64_t sg = static_cast<int64_t>(static_cast<double>(i) * pc.invL);  // no 64-bit division
+  int64_t off = i - sg * pc.L;
+  if (off < 0) {
+    --sg;
+    off += pc.L;
+  } else if (off >= pc.L) {
+    ++sg;
+    off -= pc.L;
+  }
+  return pc.seg[sg][off];
+}
+// pass 0: the ratio; pass 1: its squared deviation from the mean; NaN -> +0
+__device__ __forceinline__ double pool_term(double x, int pass, double mean) {
+  if (isnan(x)) return 0.0;
+  return pass == 0 ? x : (x - mean) * (x - mean);
+}
+
+__global__ void __launch_bounds__(kExactThreads) pool_approx_kernel(const SummaryParams p, int pass,
+                                                                    const double* means,
+                                                                    ChunkSpec* spec, int C) {
+  __shared__ PoolChain pc;
+  __shared__ double red[kExactThreads / 32];
+  __shared__ unsigned long long cnt_sh;
+  const int chain = blockIdx.x / C, chunk = blockIdx.x % C;
+  pool_build(p, chain, pc);
+  const double mean = pass == 1 ? means[2 * chain] : 0.0;
+  const int64_t lo = static_cast<int64_t>(chunk) * kPoolChunk;
+  const int64_t hi = lo + kPoolChunk < pc.total ? lo + kPoolChunk : pc.total;
+  if (threadIdx.x == 0) cnt_sh = 0;
+  double a = 0.0;
+  int64_t c = 0;
+  for (int64_t i = lo + threadIdx.x; i < hi; i += kExactThreads) {
+    const double x = pool_at(pc, i);
+    a += pool_term(x, pass, mean);
+    c += !isnan(x);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    a += __shfl_xor_sync(kFull, a, o);
+    c += __shfl_xor_sync(kFull, c, o);
+  }
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) {
+    red[threadIdx.x >> 5] = a;
+    atomicAdd(&cnt_sh, static_cast<unsigned long long>(c));
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < kExactThreads / 32; ++w) t += red[w];
+    ChunkSpec& sp = spec[blockIdx.x];
+    sp.approx = t;
+    sp.cnt = static_cast<int64_t>(cnt_sh);
+  }
+}
+
+__global__ void __launch_bounds__(kExactThreads) pool_spec_kernel(const SummaryParams p, int pass,
+                                                                  const double* means,
+                                                                  ChunkSpec* spec, int C) {
+  __shared__ PoolChain pc;
+  __shared__ double red[kExactThreads / 32];
+  __shared__ int64_t wtot[kExactThreads / 32];
+  __shared__ int wtie[kExactThreads / 32];
+  __shared__ int64_t tie_rel[kTieCap], tie_q[kTieCap];
+  __shared__ double s_pred;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int chain = blockIdx.x / C, chunk = blockIdx.x % C;
+  pool_build(p, chain, pc);
+  const double mean = pass == 1 ? means[2 * chain] : 0.0;
+  const int64_t lo = static_cast<int64_t>(chunk) * kPoolChunk;
+  // approximate running sum at the chunk start (any order: speculation only)
+  double a = 0.0;
+  for (int k = tid; k < chunk; k += kExactThreads) a += spec[static_cast<int64_t>(chain) * C + k].approx;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(kFull, a, o);
+  if (lane == 0) red[warp] = a;
+  __syncthreads();
+  if (tid == 0) {
+    double t = 0.0;
+    for (int w = 0; w < kExactThreads / 32; ++w) t += red[w];
+    s_pred = t;
+  }
+  __syncthreads();
+  const double sp0 = s_pred;
+  ChunkSpec& out = spec[blockIdx.x];
+  if (!(sp0 > 0.0) || lo >= pc.total) {
+    if (tid == 0) out.valid = 0;
+    return;
+  }
+  const int e = ilogb(sp0);
+  const double iu = ldexp(1.0, 52 - e);
+  constexpr int64_t kTop = 1ll << 53;
+  int64_t q[kExactK];
+  int fc[kExactK];
+  int64_t tot = 0;
+  int nties = 0;
+  const int64_t b = lo + static_cast<int64_t>(tid) * kExactK;
+#pragma unroll
+  for (int j = 0; j < kExactK; ++j) {
+    const double t = b + j < pc.total ? pool_term(pool_at(pc, b + j), pass, mean) : 0.0;
+    const double v = t * iu;
+    const double fl = floor(v);
+    const double fr = v - fl;
+    q[j] = fl < 9.0e15 ? static_cast<int64_t>(fl) : kTop;
+    fc[j] = fr > 0.5 ? 2 : (fr == 0.5 ? 1 : 0);
+    tot += q[j] + (fc[j] == 2 ? 1 : 0);
+    nties += fc[j] == 1;
+  }
+  int64_t inc = tot;
+  int tinc = nties;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int64_t y = __shfl_up_sync(kFull, inc, o);
+    const int z = __shfl_up_sync(kFull, tinc, o);
+    if (lane >= o) {
+      inc += y;
+      tinc += z;
+    }
+  }
+  if (lane == 31) {
+    wtot[warp] = inc;
+    wtie[warp] = tinc;
+  }
+  __syncthreads();
+  int64_t wbase = 0, all = 0;
+  int tbase = 0, tall = 0;
+#pragma unroll
+  for (int w = 0; w < kExactThreads / 32; ++w) {
+    if (w < warp) {
+      wbase += wtot[w];
+      tbase += wtie[w];
+    }
+    all += wtot[w];
+    tall += wtie[w];
+  }
+  if (tall > kTieCap) {
+    if (tid == 0) out.valid = 0;
+    return;
+  }
+  if (tall > 0) {
+    int k = tbase + tinc - nties;
+    int64_t rel = wbase + inc - tot;  // increments before this thread's first term
+#pragma unroll
+    for (int j = 0; j < kExactK; ++j) {
+      if (fc[j] == 1) {
+        tie_rel[k] = rel;
+        tie_q[k] = q[j];
+        ++k;
+      }
+      rel += q[j] + (fc[j] == 2 ? 1 : 0);
+    }
+  }
+  __syncthreads();
+  if (tid == 0) {
+    int64_t x0 = 0, x1 = 0;  // starting integer even / odd
+    for (int t = 0; t < tall; ++t) {
+      x0 += (tie_rel[t] + x0 + tie_q[t]) & 1;
+      x1 += (1 + tie_rel[t] + x1 + tie_q[t]) & 1;
+    }
+    out.R = all;
+    out.extra0 = static_cast<int32_t>(x0);
+    out.extra1 = static_cast<int32_t>(x1);
+    out.e = e;
+    out.valid = 1;
+  }
+}
+
+// The in-order walk over one chain's chunks (one block); pass 0 leaves the
+// mean and count in means[2 chain], pass 1 writes the mix summary.
+__global__ void __launch_bounds__(kExactThreads) pool_walk_kernel(const SummaryParams p, int pass,
+                                                                  double* means,
+                                                                  const ChunkSpec* spec, int C) {
+  __shared__ PoolChain pc;
+  const int chain = blockIdx.x;
+  const int mi = chain >> 1, variant = chain & 1;
+  pool_build(p, chain, pc);
+  const bool present = variant == 0 ? p.with_saber != 0 : p.n_caps > 0;
+  double mean = pass == 1 ? means[2 * chain] : 0.0;
+  const int64_t cnt_prev = pass == 1 ? static_cast<int64_t>(means[2 * chain + 1]) : 0;
+  const bool run = present && (pass == 0 || (cnt_prev > 0 && mean != 0.0));
+  double s = 0.0;
+  int64_t cnt = 0;
+  if (run) {
+    constexpr int64_t kTop = 1ll << 53;
+    for (int c = 0; c < C; ++c) {
+      const int64_t lo = static_cast<int64_t>(c) * kPoolChunk;
+      if (lo >= pc.total) break;
+      const int64_t hi = lo + kPoolChunk < pc.total ? lo + kPoolChunk : pc.total;
+      const ChunkSpec sp = spec[static_cast<int64_t>(chain) * C + c];
+      cnt += sp.cnt;
+      bool done = false;
+      if (sp.valid && s > 0.0 && ilogb(s) == sp.e) {
+        const double iu = ldexp(1.0, 52 - sp.e), u = ldexp(1.0, sp.e - 52);
+        const int64_t S = static_cast<int64_t>(s * iu);
+        const int64_t ex = (S & 1) ? sp.extra1 : sp.extra0;
+        if (S + sp.R + ex < kTop - 1) {
+          s = static_cast<double>(S + sp.R + ex) * u;
+          done = true;
+        }
+      }
+      if (!done) {
+        s = exactsum::block_exact_seq_sum_range(
+            s, lo, hi,
+            [&](int64_t bb, double (&t)[kExactK]) {
+#pragma unroll
+              for (int j = 0; j < kExactK; ++j)
+                t[j] = bb + j < hi ? pool_term(pool_at(pc, bb + j), pass, mean) : 0.0;
+            },
+            [&](int64_t i) { return pool_term(pool_at(pc, i), pass, mean); });
+      }
+    }
+  }
+  if (threadIdx.x != 0) return;
+  if (pass == 0) {
+    means[2 * chain] = cnt > 0 ? s / static_cast<double>(cnt) : 0.0;
+    means[2 * chain + 1] = static_cast<double>(cnt);
+    return;
+  }
+  const double* sc = p.scratch + static_cast<int64_t>(mi) * p.n_rps * kCellScratch;
+  const double nanv = nan("");
+  double mean_goodput = nanv, pooled = nanv, rps_cv = nanv;
+  if (present) {
+    if (cnt_prev > 0 && mean != 0.0) pooled = sqrt(s / static_cast<double>(cnt_prev)) / mean;
+    double g = 0.0;
+    for (int ri = 0; ri < p.n_rps; ++ri) g += sc[ri * kCellScratch + (variant == 0 ? 0 : 1)];
+    mean_goodput = g / static_cast<double>(p.n_rps);
+    rps_cv = cv_cells(sc, p.n_rps, variant == 0 ? 2 : 3, variant == 0 ? 4 : 5);
+  }
+  saber_mix_summary* o = p.summary + mi;
+  if (variant == 0) {
+    o->saber_mean_goodput = mean_goodput;
+    o->saber_pooled_cv = pooled;
+    o->saber_rps_mean_cv = rps_cv;
+  } else {
+    o->best_static_mean_goodput = mean_goodput;
+    o->best_static_pooled_cv = pooled;
+    o->best_static_rps_mean_cv = rps_cv;
+  }
+}
+
 // delta = saber - best static (simloop.cpp:262), after both variants wrote.
 __global__ void summary_delta_kernel(const SummaryParams p) {
   const int mi = blockIdx.x * blockDim.x + threadIdx.x;
@@ -704,6 +992,13 @@ __global__ void summary_delta_kernel(const SummaryParams p) {
 }
 
 }  // namespace
+
+size_t summary_pool_scratch_bytes(int n_mixes, int n_rps, int repeats, int n) {
+  const int64_t total = static_cast<int64_t>(n_rps) * repeats * n;
+  const int64_t C = (total + kPoolChunk - 1) / kPoolChunk;
+  return static_cast<size_t>(2 * n_mixes) * static_cast<size_t>(C) * sizeof(ChunkSpec) +
+         static_cast<size_t>(2 * n_mixes) * 2 * sizeof(double);
+}
 
 int launch_summary(const SummaryParams& p, void* stream) {
   cudaStream_t s = static_cast<cudaStream_t>(stream);
@@ -729,8 +1024,22 @@ int launch_summary(const SummaryParams& p, void* stream) {
     summary_mix_kernel<<<2 * p.n_mixes, 64, 0, s>>>(p);
   else if (std::getenv("SABER_SUMMARY_CHAIN") || p.n_rps > kMaxSegments)
     summary_mix_warp_kernel<<<2 * p.n_mixes, 32, 0, s>>>(p);
-  else
+  else if (std::getenv("SABER_SUMMARY_BLOCK"))
     summary_mix_exact_kernel<<<2 * p.n_mixes, kExactThreads, 0, s>>>(p);
+  else {
+    // chunked: approx sums, speculation, walk — per pass (stream-ordered scratch)
+    const int chains = 2 * p.n_mixes;
+    const int64_t total = static_cast<int64_t>(p.n_rps) * p.repeats * p.n;
+    const int C = static_cast<int>((total + kPoolChunk - 1) / kPoolChunk);
+    if (!p.pool_scratch) return 1;
+    ChunkSpec* spec = static_cast<ChunkSpec*>(p.pool_scratch);
+    double* means = reinterpret_cast<double*>(spec + static_cast<size_t>(chains) * C);
+    for (int pass = 0; pass < 2; ++pass) {
+      pool_approx_kernel<<<chains * C, kExactThreads, 0, s>>>(p, pass, means, spec, C);
+      pool_spec_kernel<<<chains * C, kExactThreads, 0, s>>>(p, pass, means, spec, C);
+      pool_walk_kernel<<<chains, kExactThreads, 0, s>>>(p, pass, means, spec, C);
+    }
+  }
   summary_delta_kernel<<<1, 32, 0, s>>>(p);
   return cudaGetLastError() == cudaSuccess ? 0 : 1;
 }
