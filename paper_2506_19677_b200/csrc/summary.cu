@@ -1008,7 +1008,15 @@ int launch_summary(const SummaryParams& p, void* stream) {
   // kernels (bench.py pipelining) — small blocks that fit in the register
   // file those kernels leave free (the static kernel leaves 4,096 registers
   // per SM: one warp of the cells kernel or two of the ratios kernel fit)
-  const bool chain = std::getenv("SABER_SUMMARY_CHAIN") != nullptr;
+  // Beside running trajectory kernels (narrow: bench.py's pipelined sweeps)
+  // short pools keep the sequential single-warp chains, which fit in the
+  // registers those kernels leave free and finish within the next sweep's
+  // simulation (config 2: 128K terms, ~1.9 ms); long pools (config 3, the
+  // N-GPU root) and stand-alone summaries use the exact parallel sums.
+  const int64_t pool = static_cast<int64_t>(p.n_rps) * p.repeats * p.n;
+  const bool chain = std::getenv("SABER_SUMMARY_CHAIN") != nullptr ||
+                     (p.narrow && pool <= (int64_t{1} << 18) &&
+                      std::getenv("SABER_SUMMARY_EXACT") == nullptr);
   if (p.narrow) {
     ratios_kernel<<<148, 64, 0, s>>>(p);
   } else {
@@ -1022,7 +1030,7 @@ int launch_summary(const SummaryParams& p, void* stream) {
     summary_cells_exact_kernel<<<cells, kExactThreads, 0, s>>>(p);
   if (std::getenv("SABER_SUMMARY_RING"))
     summary_mix_kernel<<<2 * p.n_mixes, 64, 0, s>>>(p);
-  else if (std::getenv("SABER_SUMMARY_CHAIN") || p.n_rps > kMaxSegments)
+  else if (chain || p.n_rps > kMaxSegments)
     summary_mix_warp_kernel<<<2 * p.n_mixes, 32, 0, s>>>(p);
   else if (std::getenv("SABER_SUMMARY_BLOCK"))
     summary_mix_exact_kernel<<<2 * p.n_mixes, kExactThreads, 0, s>>>(p);
