@@ -557,8 +557,10 @@ saber_status saber_cuda_predict_table(const saber_model* model, int32_t max_load
  * Misc.
  * -------------------------------------------------------------------------- */
 const char* saber_cuda_last_error(void);
-/* Device blocks freed by finished calls are cached for reuse; this returns
- * the cached blocks of `device` to the driver. */
+/* Device blocks freed by finished calls are cached for reuse, and the
+ * one-shot saber_cuda_sweep keeps its last plan for calls with the same grid;
+ * this destroys that plan and returns the cached blocks of `device` to the
+ * driver. */
 saber_status saber_cuda_release_cache(int32_t device);
 int32_t saber_cuda_abi_version(void);
 /* Number of usable sm_100 devices (0 on a CPU-only host). */
