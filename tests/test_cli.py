@@ -133,6 +133,9 @@ RUN_CASES = [
      "--tick", "0.05", "--prefill-rate", "0", "--horizon", "40", "--seed", "1234567"],
     ["--mix", "w1", "--rps", "30", "--requests", "250", "--scheduler", "saber", "--horizon", "5",
      "--seed", "3"],
+    # the wide kernel: more requests than the register masks, a 24-wide window
+    ["--mix", "w2", "--rps", "15", "--requests", "700", "--scheduler", "saber", "--window", "24",
+     "--seed", "5"],
 ]
 
 
