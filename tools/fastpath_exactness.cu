@@ -3,8 +3,12 @@
 //   exp_bounded(x) == exp(x)            for random x in [-700, 700]
 //   div_fast(x, d) == x / d             whenever div_fast reports ok
 //   Markstein q' (RN(1/d) reciprocal)   == x / d   (div_by's fast path)
+//   div_unchecked(x, d, rcp_unchecked(d)) == x / d   for d in the exponent
+//       window [2^-256, 2^256) (window_bits) and x = +0 or any x whose
+//       quotient is normal in (2^-900, 2^900) — the LM passes' condition
 // Operands: random mantissas incl. all-ones / power-of-two / near-boundary
-// patterns, exponents over 2^-100..2^100.  Prints mismatches, exit 1 if any.
+// patterns, exponents over 2^-100..2^100 (the window case: d over 2^-260..
+// 2^260, x over 2^-660..2^660).  Prints mismatches, exit 1 if any.
 #include <cstdint>
 #include <cstdio>
 #include <cstdlib>
@@ -30,6 +34,14 @@ __device__ double make(uint64_t r, int emin, int erange) {
   const uint64_t bits = (static_cast<uint64_t>(e + 1023) << 52) | m | ((r >> 63) << 63);
   return __longlong_as_double(static_cast<long long>(bits));
 }
+// make() with the exponent drawn from a second word (any range width)
+__device__ double make_w(uint64_t r, uint64_t re, int emin, int erange) {
+  const double v = make(r, 0, 1);
+  const int e = emin + static_cast<int>(re % static_cast<uint64_t>(erange));
+  const uint64_t bits = (__double_as_longlong(v) & 0x800FFFFFFFFFFFFFull) |
+                        (static_cast<uint64_t>(e + 1023) << 52);
+  return __longlong_as_double(static_cast<long long>(bits));
+}
 __global__ void k(uint64_t seed, int64_t n, unsigned long long* bad, unsigned long long* used,
                   double* ex) {
   unsigned long long u = 0;
@@ -51,6 +63,22 @@ __global__ void k(uint64_t seed, int64_t n, unsigned long long* bad, unsigned lo
       if (__double_as_longlong(q1) != __double_as_longlong(x / d)) {
         const unsigned long long q = atomicAdd(bad, 1ull);
         if (q < 8) { ex[3 * q] = 1; ex[3 * q + 1] = x; ex[3 * q + 2] = d; }
+      }
+    }
+    // the window-checked unchecked quotient (fit_kernel.cu Div)
+    {
+      const uint64_t a2 = mix(a ^ 0x5bd1e995ull), b2 = mix(b ^ 0x5bd1e995ull);
+      const double dw = make_w(b2, mix(b2), -260, 520);
+      const double xw = (mix(a2) & 63) == 0 ? 0.0 : make_w(a2, mix(a2) >> 6, -660, 1320);
+      if (window_ok(window_bits(dw))) {
+        const double q = xw / dw, aq = fabs(q);
+        if (xw == 0.0 || (aq > 0x1.0p-900 && aq < 0x1.0p900)) {
+          ++u;
+          if (__double_as_longlong(div_unchecked(xw, dw, rcp_unchecked(dw))) != __double_as_longlong(q)) {
+            const unsigned long long qq = atomicAdd(bad, 1ull);
+            if (qq < 8) { ex[3 * qq] = 3; ex[3 * qq + 1] = xw; ex[3 * qq + 2] = dw; }
+          }
+        }
       }
     }
     // Markstein with a correctly rounded reciprocal (fit_kernel.cu div_by)
