@@ -2002,6 +2002,13 @@ extern "C" saber_status saber_cuda_fit_batch(const saber_fit_desc* desc, saber_f
   fp.lm_trials = trs.as<int32_t>();
   fp.trials = trc.as<int32_t>();
   fp.cursor = cursor.as<int32_t>();
+  {
+    // Verification switch (tests/test_gpu_fit.py): the LM passes take the
+    // IEEE-division, clamped-exponent path only, which the fast paths must
+    // reproduce bit for bit.
+    const char* e = std::getenv("SABER_LM_IEEE");
+    fp.ieee_only = (e && e[0] == '1') ? 1 : 0;
+  }
   int launches = 0;
   LAUNCH_TRY(launch_fit(fp, st, &launches));
   CUDA_TRY(cudaMemcpyAsync(out->params, params.p, static_cast<size_t>(3) * N * 3 * 8, cudaMemcpyDeviceToHost, st));

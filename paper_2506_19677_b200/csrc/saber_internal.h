@@ -354,6 +354,7 @@ struct FitParams {
   int32_t* lm_trials;  // [3*n_curves*5] damping trials per start
   int32_t* trials;     // [3*n_curves] summed over the starts (or null)
   int32_t* cursor;     // work queue
+  int32_t ieee_only;   // SABER_LM_IEEE=1: LM passes skip the fast paths (checks)
 };
 int launch_fit(const FitParams& p, void* stream, int* launches);
 

@@ -161,3 +161,38 @@ def test_fit_config4_recipe_matches_compiled_reference(engine, ref):
                 bad.append((c, f, list(got), list(want), res.r2[f, c], cal["r2"][f]))
     assert bad == []
 
+
+
+def _steep_logistic_curves(n=1500, m=40, seed=7):
+    """Steep logistic curves over wide load ranges: exponent arguments far
+    beyond the +-700 clamp, quotients near the fast paths' windows."""
+    rng = np.random.default_rng(seed)
+    loads = np.concatenate([np.sort(rng.integers(1, 3000, m)).astype(np.int32) for _ in range(n)])
+    K, r, x0 = rng.uniform(50, 200, n), rng.uniform(0.01, 5.0, n), rng.uniform(-100, 3000, n)
+    Lf = loads.reshape(n, m).astype(np.float64)
+    sp = K[:, None] / (1.0 + np.exp(np.clip(r[:, None] * (Lf - x0[:, None]), -700, 700)))
+    sp = np.maximum(sp * (1 + 0.01 * (rng.random((n, m)) - 0.5)), 1e-3).reshape(-1)
+    return loads, sp, np.arange(0, n * m + 1, m, dtype=np.int64)
+
+
+@pytest.mark.parametrize("which", ["config4", "steep"])
+def test_lm_fast_paths_bit_identical_to_ieee_path(engine, monkeypatch, which):
+    """The LM kernel's fast passes (csrc/fit_kernel.cu: family-specialised,
+    window-checked unchecked division, clamp-free exponent when the arguments
+    are provably bounded) against the same kernel with SABER_LM_IEEE=1 (IEEE
+    division, clamped exponent, every pass): parameters, r^2, status, selected
+    family and the in-kernel iteration / trial counts bit-identical."""
+    import recipes
+    if which == "config4":
+        loads, speeds, offsets, _ = recipes.config4_curves(3000)
+    else:
+        loads, speeds, offsets = _steep_logistic_curves()
+    fast = engine.fit_batch(loads, speeds, offsets, calibrate=True)
+    monkeypatch.setenv("SABER_LM_IEEE", "1")
+    slow = engine.fit_batch(loads, speeds, offsets, calibrate=True)
+    assert np.array_equal(fast.params.view(np.uint64), slow.params.view(np.uint64))
+    assert np.array_equal(fast.r2.view(np.uint64), slow.r2.view(np.uint64))
+    assert np.array_equal(fast.status, slow.status)
+    assert np.array_equal(fast.best_family, slow.best_family)
+    assert np.array_equal(fast.iterations, slow.iterations)
+    assert np.array_equal(fast.trials, slow.trials)
