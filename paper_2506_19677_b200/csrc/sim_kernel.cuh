@@ -1184,7 +1184,11 @@ __device__ __forceinline__ void simulate_one(const SimParams& P, int ti, const S
 #ifdef SABER_STREAK_STATS
       st_exact += 1;
 #endif
-      if (!rem_exact) {
+      // (Only needed when the bound cannot already show that the decode
+      // boundary does not bind this pass: min_rem >= rem_lb >= speed*dt*(1+1e-12)
+      // gives fl(min_rem / speed) > dt.  The pass below recomputes the exact
+      // minimum either way.)
+      if (!rem_exact && rem_lb < speed * dt * kOnePlusTol) {
         double r = kInf;
 #pragma unroll 1
         for (int k = sub, s = S.idx(sub); k < A; k += G, s += kWarp) {
@@ -1241,6 +1245,7 @@ __device__ __forceinline__ void simulate_one(const SimParams& P, int ti, const S
       decode_updates += A - npre;
       min_pf = group_min_pos<G>(npf, gmask);
       rem_lb = group_min_pos<G>(nrem, gmask);
+      rem_exact = true;
       const unsigned tot = group_sum<G>(counts, gmask);
       npre = static_cast<int>(tot & 0xFFFFu);
       const unsigned ndone = tot >> 16;
