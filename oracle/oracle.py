@@ -217,6 +217,20 @@ class Oracle:
                      "profile", "sweep"):
             f(name).restype = C.c_int
 
+    def latency_quantiles(self, cfg: OrcSimConfig, ps=(0.5, 0.9, 0.99)) -> list:
+        """Reference only: p-quantiles of latency over every issued request,
+        read off saber::cdf (metrics.cpp:61-85) of saber::run(cfg)'s records."""
+        if self.which != "reference":
+            raise OracleError("latency_quantiles: reference harness only")
+        f = self._f("latency_quantiles")
+        f.argtypes = [C.POINTER(OrcSimConfig), C.POINTER(C.c_double), C.c_int32,
+                      C.POINTER(C.c_double)]
+        f.restype = C.c_int
+        pa = (C.c_double * len(ps))(*ps)
+        q = (C.c_double * len(ps))()
+        self._check(f(C.byref(cfg), pa, len(ps), q))
+        return list(q)
+
     def _f(self, name):
         return getattr(self.lib, self.p + name)
 

@@ -202,6 +202,26 @@ int ref_run(const orc_sim_config* cfg, orc_traj_out* out, orc_record* records,
   });
 }
 
+// The engine's per-row latency quantiles (p50/p90/p99 over every issued
+// request) read off the reference's own cdf (metrics.cpp:61-85): the records
+// of saber::run(cfg), relabelled to one task so that cdf() pools them; q[i] =
+// the smallest latency whose cumulative fraction reaches p[i] (NaN if none).
+int ref_latency_quantiles(const orc_sim_config* cfg, const double* p, int32_t np, double* q) {
+  return guarded([&] {
+    saber::RunOutput o = saber::run(to_config(*cfg));
+    for (auto& r : o.records) r.task = "all";
+    const auto pts = saber::cdf(o.records, "all");
+    for (int32_t i = 0; i < np; ++i) {
+      q[i] = std::nan("");
+      for (const auto& [lat, frac] : pts)
+        if (frac >= p[i]) {
+          q[i] = lat;
+          break;
+        }
+    }
+  });
+}
+
 int ref_run_with_requests(const orc_sim_config* cfg, const orc_request* rq,
                           int32_t n, orc_traj_out* out, orc_record* records,
                           orc_decision* decisions, int64_t dec_cap,

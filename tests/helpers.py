@@ -103,3 +103,19 @@ def random_configs(count, seed=1234, n_choices=(1, 7, 50, 100, 130), allow_logis
             gt=rng.choice([GT, (0, (80.0, 0.12, 0.002)), (1, (120.0, 0.1, 30.0))]),
             prefill_rate=rng.choice([2000.0, 2000.0, 0.0, 500.0]), jitter=rng.choice([0.2, 0.0, 0.5])))
     return out
+
+
+def quantiles_from_records(records):
+    """The reference's cdf (metrics.cpp:61-85) over all issued requests:
+    smallest latency x with (#latencies <= x) / issued >= p."""
+    issued = len(records)
+    lat = sorted(r.completion_time - r.arrival_time for r in records if not math.isnan(r.completion_time))
+    out = []
+    for p in (0.5, 0.9, 0.99):
+        got = float("nan")
+        for i, x in enumerate(lat):
+            if (i + 1) / issued >= p:
+                got = x
+                break
+        out.append(got)
+    return out

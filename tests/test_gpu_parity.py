@@ -10,8 +10,8 @@ import numpy as np
 import pytest
 
 import oracle as O
-from helpers import (CAL_USL, GT, compare_row, orc_config, orc_requests, random_configs,
-                     same_float, sim_config)
+from helpers import (CAL_USL, GT, compare_row, orc_config, orc_requests, quantiles_from_records,
+                     random_configs, same_float, sim_config)
 
 pytestmark = pytest.mark.gpu
 
@@ -224,29 +224,27 @@ def test_draw_streams_grow_on_exhaustion(engine, monkeypatch):
     assert a.traj_rows.tobytes() == b.traj_rows.tobytes()
 
 
-def _quantiles_from_records(records):
-    """The reference's cdf (metrics.cpp:61-85) over all issued requests:
-    smallest latency x with (#latencies <= x) / issued >= p."""
-    issued = len(records)
-    lat = sorted(r.completion_time - r.arrival_time for r in records if not math.isnan(r.completion_time))
-    out = []
-    for p in (0.5, 0.9, 0.99):
-        got = float("nan")
-        for i, x in enumerate(lat):
-            if (i + 1) / issued >= p:
-                got = x
-                break
-        out.append(got)
-    return out
-
-
 def test_latency_percentiles_match_restatement(engine, orc):
     cfgs = random_configs(160, seed=4242)
     res = engine.run_batch(cfgs)
     bad = []
     for k, cfg in enumerate(cfgs):
         o = orc.run(orc_config(cfg), records=True)
-        want = _quantiles_from_records(o.records)
+        want = quantiles_from_records(o.records)
+        got = list(res.rows[k]["latency_q"])
+        if not all(same_float(a, b) for a, b in zip(got, want)):
+            bad.append((k, got, want))
+    assert bad == []
+
+
+def test_latency_percentiles_match_reference_cdf(engine, ref):
+    """p50/p90/p99 of every row against the compiled reference's own cdf
+    (saber::cdf over all records of saber::run, oracle/ref_harness.cpp)."""
+    cfgs = random_configs(120, seed=5151)
+    res = engine.run_batch(cfgs)
+    bad = []
+    for k, cfg in enumerate(cfgs):
+        want = ref.latency_quantiles(orc_config(cfg))
         got = list(res.rows[k]["latency_q"])
         if not all(same_float(a, b) for a, b in zip(got, want)):
             bad.append((k, got, want))

@@ -7,7 +7,8 @@ import numpy as np
 import pytest
 
 import oracle as O
-from helpers import CAL_USL, compare_row, orc_config, random_configs, sim_config
+from helpers import (CAL_USL, compare_row, orc_config, quantiles_from_records, random_configs,
+                     sim_config)
 
 
 def test_mt19937_64_known_answer(orc):
@@ -128,3 +129,14 @@ def test_sweep_matches_reference(orc, ref):
     for k in ("goodput", "ratio_mean", "ratio_std", "cv", "summary"):
         assert np.array_equal(a[k], b[k], equal_nan=True), k
     assert np.array_equal(a["best_cap"], b["best_cap"])
+
+
+def test_latency_quantiles_match_reference_cdf(orc, ref):
+    """The quantile rule the GPU percentile tests apply to the restatement's
+    records equals the reference's own cdf (saber::cdf over every record of
+    saber::run, metrics.cpp:61-85)."""
+    for cfg in random_configs(60, seed=777):
+        oc = orc_config(cfg)
+        want = ref.latency_quantiles(oc)
+        got = quantiles_from_records(orc.run(oc, records=True).records)
+        assert all((math.isnan(a) and math.isnan(b)) or a == b for a, b in zip(got, want)), (got, want)
