@@ -156,8 +156,12 @@ struct SimLaunch {
   size_t smem;    // dynamic shared memory per block
   int wide;       // 1 = the wide kernel (global-memory slots and masks)
 };
+// One warp (= one trajectory at a time) per block: ptxas allocates the
+// single-warp kernels with fewer spills (SABER kernel 8 B vs 44 B at 128
+// registers) and the SMs fill block by block (config 2 +1.2%, config 3 +1.2%
+// over 128-thread blocks).
 #ifndef SABER_SIM_BLOCK
-#define SABER_SIM_BLOCK 128
+#define SABER_SIM_BLOCK 32
 #endif
 constexpr int kSimBlock = SABER_SIM_BLOCK;
 // `wide`: the launch needs the wide kernel (nmax > kMaxRequests or a window

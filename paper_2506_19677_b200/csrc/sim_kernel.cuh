@@ -47,14 +47,17 @@ namespace {
 
 using namespace simdev;
 
+// Blocks per SM for the register budget (kSimBlock-thread blocks): generic
+// and SABER kernels 16 warps (128 registers), static kernel 25 (ptxas: 72
+// registers, 28 warps fit).
 #ifndef SABER_SIM_MIN_BLOCKS
-#define SABER_SIM_MIN_BLOCKS 4
+#define SABER_SIM_MIN_BLOCKS (512 / SABER_SIM_BLOCK)
 #endif
 #ifndef SABER_STATIC_MIN_BLOCKS
-#define SABER_STATIC_MIN_BLOCKS 6
+#define SABER_STATIC_MIN_BLOCKS (800 / SABER_SIM_BLOCK)
 #endif
 #ifndef SABER_SABER_MIN_BLOCKS
-#define SABER_SABER_MIN_BLOCKS 4
+#define SABER_SABER_MIN_BLOCKS (512 / SABER_SIM_BLOCK)
 #endif
 
 #ifdef SABER_STREAK_STATS
