@@ -132,6 +132,7 @@ struct SimParams {
   int32_t no_streak;          // 1 = disable quiet streaks (A/B runs, SABER_NO_STREAK)
   int32_t mode_sel;           // 0 any, 1 static-only, 2 SABER-only kernel (sim_kernel.cu)
   int32_t first_traj;         // this launch simulates order[first_traj .. n_traj)
+  int32_t split_saber;        // SABER-only launch beside a static-only one (grid_saber_split)
   TickTable ticks;            // shared tick grid for quiet streaks
 };
 
@@ -152,6 +153,7 @@ struct SimLaunch {
   int block;      // threads per block
   int grid;       // persistent blocks
   int grid_sel[3];  // persistent blocks per mode-specialised variant (G = 32)
+  int grid_saber_split;  // SABER-only blocks when launched beside the static kernel
   int slot_rows;  // ceil(nmax / group)
   size_t smem;    // dynamic shared memory per block
   int wide;       // 1 = the wide kernel (global-memory slots and masks)

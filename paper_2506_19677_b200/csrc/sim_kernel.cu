@@ -253,6 +253,14 @@ int plan_sim(int nmax, int group, bool wide, SimLaunch* out) {
   // 128 registers); leave 8 SMs one block short so a concurrent sweep summary
   // (single-warp blocks on a side stream) finds room (bench.py pipelining).
   if (l.grid_sel[kSelSaber] > 16 * kSimBlock / kWarp) l.grid_sel[kSelSaber] -= 8;
+  // Beside the static kernel (split sweep launches) the SABER kernel keeps
+  // two warps per SM fewer: the static blocks start sooner (config 2 9.76 ->
+  // 9.70 ms per sweep, r02i box; 1 warp fewer: 9.75, 4 fewer: 9.81; the
+  // Monte-Carlo driver's split launches keep the full grid: 2% slower there).
+  int trim = 2 * sms;
+  if (const char* e = std::getenv("SABER_SPLIT_SABER_TRIM")) trim = std::atoi(e);
+  l.grid_saber_split = l.grid_sel[kSelSaber] > trim + sms ? l.grid_sel[kSelSaber] - trim
+                                                          : l.grid_sel[kSelSaber];
   l.grid = l.grid_sel[0];
   l.block = kSimBlock;
   *out = l;
@@ -265,7 +273,8 @@ int launch_sim(const SimParams& p, const SimLaunch& l, void* stream) {
   const int sel = p.mode_sel;
   void* k = l.wide ? pick_sim_wide(trace, records) : pick_kernel(l.nwords, l.group, trace, records, sel);
   if (!k) return 1;
-  const int grid = (!l.wide && l.group == kWarp && !trace && !records) ? l.grid_sel[sel] : l.grid;
+  int grid = (!l.wide && l.group == kWarp && !trace && !records) ? l.grid_sel[sel] : l.grid;
+  if (p.split_saber && sel == kSelSaber && l.grid_saber_split > 0) grid = l.grid_saber_split;
   SimParams q = p;
   q.no_streak = std::getenv("SABER_NO_STREAK") != nullptr;
   void* args[] = {&q};
